@@ -1,0 +1,110 @@
+"""Golden-case tables and oracle-only input builders.
+
+Shared by ``make_golden.py`` (build container, runs the reference) and the
+tests (any box).  Inputs are rebuilt from seeds with the oracle's generator
+recipes; each fixture stores a digest of its inputs so a drifting generator is
+caught before any comparison.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+from types import SimpleNamespace
+
+import numpy as np
+
+from oracle import tvkit_oracle as orc
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+ALIGN_CASES = [
+    # name, ubm seed, C, F, mean sd, frame seed, n frames, frame scale, top_k, prune
+    ("c8f3", 30, 8, 3, 3.0, 31, 1000, 3.0, 5, 0.025),
+    ("c8f3_noprune", 30, 8, 3, 3.0, 32, 200, 3.0, 4, 0.0),
+    ("c8f3_degenerate", 30, 8, 3, 3.0, 33, 200, 3.0, 8, 0.9999),
+    ("c64f20", 40, 64, 20, 0.5, 41, 2000, 1.5, 20, 0.025),
+    ("c256f60", 50, 256, 60, 0.3, 51, 600, 1.2, 20, 0.025),
+    ("c2048f60", 60, 2048, 60, 0.3, 61, 300, 1.2, 20, 0.025),
+]
+
+TVM_CASES = [
+    # name, formulation, seed, C, F, D, speakers, utts/spk, frames, within, rank
+    ("aug_c4f6", "augmented", 3, 4, 6, 4, 6, 2, (80, 140), 1.0, 4),
+    ("std_c4f6", "standard", 4, 4, 6, 4, 6, 2, (80, 140), 1.0, 3),
+    ("aug_c16f8", "augmented", 5, 16, 8, 6, 10, 2, (60, 120), 0.5, 6),
+]
+
+TRAIN_CASES = [
+    # name, formulation, seed, C, F, D, spk, upc, frames, rank, iters, min_div, sigma, update_mean, realign
+    ("aug", "augmented", 7, 8, 6, 4, 10, 3, (60, 100), 5, 3, True, True, False, 0),
+    ("aug_realign", "augmented", 8, 8, 6, 4, 10, 3, (60, 100), 4, 3, True, True, False, 1),
+    ("std_mean", "standard", 9, 8, 6, 4, 10, 3, (60, 100), 4, 3, True, False, True, 1),
+]
+
+CONFIG1 = dict(n_comp=64, dim=20, rank=100, speakers=50, upc=4, frames=(300, 300), seed=0,
+               within=0.3, iterations=5)
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:32]
+
+
+def load(name):
+    """Fixture ``name`` as {case: {key: array}}."""
+    raw = np.load(os.path.join(HERE, f"{name}.npz"))
+    out = {}
+    for k in raw.files:
+        case, key = k.split("__", 1)
+        out.setdefault(case, {})[key] = raw[k]
+    return out
+
+
+def align_inputs(case):
+    """(diag, full, frames f32, top_k, prune, center) for an ALIGN_CASES row."""
+    name, us, c, f, sd, fs, n, sc, k, pr = case
+    diag, full, _ = orc.posterior_ubm(c, f, sd, us)
+    x = np.random.default_rng(fs).normal(0.0, sc, (n, f)).astype(np.float32)
+    center = np.random.default_rng(us + 1000).normal(0.0, 1.0, (c, f))
+    return diag, full, x, k, pr, center
+
+
+def corpus(formulation, seed, c, f, d, spk, ups, frames, within):
+    """Oracle restatement of ``synth.sample_corpus`` (bit-identical, asserted at generation)."""
+    rng = np.random.default_rng(seed)
+    gen = orc.generator_model(c, f, d, formulation, 8.0, 100.0, rng)
+    ids, feats, spk_of = orc.sample_utterances(gen, spk, ups, frames, within, rng)
+    pc = orc.predictive_covariances(gen)
+    diag = (gen.ubm_weights, gen.ubm_means, np.ascontiguousarray(np.diagonal(pc, axis1=1, axis2=2)))
+    full = (gen.ubm_weights, gen.ubm_means, pc)
+    return SimpleNamespace(ids=ids, features=feats, speakers=spk_of, gen=gen, diag=diag, full=full)
+
+
+def tvm_inputs(case):
+    name, form, seed, c, f, d, spk, ups, frames, within, rank = case
+    cor = corpus(form, seed, c, f, d, spk, ups, frames, within)
+    model = orc.init_model(cor.full[0], cor.full[1], cor.full[2], rank, form, seed + 1)
+    return cor, model, min(4, c)
+
+
+def train_inputs(case):
+    (name, form, seed, c, f, d, spk, upc, frames, rank, iters, md, su, um, ri) = case
+    cor = corpus(form, seed, c, f, d, spk, upc, frames, 0.5)
+    cfg = SimpleNamespace(formulation=form, latent_dim=rank, iterations=iters, min_div=md,
+                          sigma_update=su, update_mean=um, realign_interval=ri, top_k=4,
+                          prune=0.025, prior_offset=100.0, batch_size_utts=4)
+    return cor, cfg
+
+
+def config1_inputs():
+    p = CONFIG1
+    rng = np.random.default_rng(p["seed"])
+    gen = orc.generator_model(p["n_comp"], p["dim"], p["rank"], "augmented", 8.0, 100.0, rng)
+    ids, feats, _ = orc.sample_utterances(gen, p["speakers"], p["upc"], p["frames"], p["within"], rng)
+    cfg = SimpleNamespace(formulation="augmented", latent_dim=p["rank"], iterations=p["iterations"],
+                          min_div=True, sigma_update=True, update_mean=False, realign_interval=0,
+                          top_k=20, prune=0.025, prior_offset=100.0, batch_size_utts=8)
+    return ids, feats, cfg
