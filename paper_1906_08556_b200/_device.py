@@ -1,0 +1,131 @@
+"""Device-resident building blocks shared by the API functions and the corpus drivers.
+
+Every function here takes/returns torch CUDA tensors and calls libtvk; shapes
+follow the reference (C components, F feature dims, D latent dims).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream
+
+
+def _f64(a):
+    return _lib.to_dev(a, torch.float64)
+
+
+class DiagTable:
+    """(2F+1) x C coefficient table of a diagonal GMM (gmm.py:56-67)."""
+
+    def __init__(self, weights, means, variances):
+        w, mu, var = _f64(weights), _f64(means), _f64(variances)
+        self.C, self.F = mu.shape
+        self.table = _lib.empty((2 * self.F + 1, self.C))
+        call("tvk_diag_table", ptr(w), ptr(mu), ptr(var), self.C, self.F, ptr(self.table), stream())
+
+
+class FullTable:
+    """Q x C quadratic-feature table of a full-covariance GMM (gmm.py:106-119)."""
+
+    def __init__(self, weights, means, covariances):
+        w, mu, cov = _f64(weights), _f64(means), _f64(covariances)
+        self.C, self.F = mu.shape
+        q = 1 + self.F + self.F * (self.F + 1) // 2
+        self.table = _lib.empty((q, self.C))
+        self.status = _lib.empty((self.C,), torch.int32)
+        call("tvk_full_table", ptr(w), ptr(mu), ptr(cov), self.C, self.F, ptr(self.table), ptr(self.status),
+             stream())
+
+    def bad_components(self):
+        return np.flatnonzero(_lib.to_host(self.status) != _lib.ITEM_OK)
+
+
+def frames_to_device(features):
+    """Frames as a device matrix; float32 stays float32 (exact in f64), anything else f64."""
+    if isinstance(features, torch.Tensor):
+        x = features
+        if x.dtype not in (torch.float32, torch.float64):
+            x = x.to(torch.float64)
+        return x.to(_lib.device()).contiguous()
+    arr = np.asarray(features)
+    if arr.dtype != np.float32:
+        arr = arr.astype(np.float64, copy=False)
+    return _lib.to_dev(np.atleast_2d(arr), torch.float32 if arr.dtype == np.float32 else torch.float64)
+
+
+def dense_loglik(x, table, kind):
+    """T x C log-likelihoods = features(x) . table (kind 0 diag, 1 full)."""
+    T, F = x.shape
+    q, C = table.shape
+    feats = _lib.empty((T, q))
+    xp, xf = _lib.x_args(x)
+    call("tvk_frame_features", xp, xf, T, F, kind, ptr(feats), stream())
+    out = _lib.empty((T, C))
+    _lib.dgemm(feats, table, out, T, C, q)
+    return out
+
+
+def select_topk(x, diag_tab, k, values=False):
+    T, F = x.shape
+    sel = _lib.empty((T, k), torch.int32)
+    val = _lib.empty((T, k)) if values else None
+    xp, xf = _lib.x_args(x)
+    call("tvk_select_topk", xp, xf, T, F, ptr(diag_tab.table), diag_tab.C, k, ptr(sel), ptr(val), stream())
+    return sel, val
+
+
+class AlignResult:
+    """Device CSR alignment of a frame batch."""
+
+    def __init__(self, offsets, components, weights, n_entries):
+        self.offsets = offsets
+        self.components = components
+        self.weights = weights
+        self.n_entries = n_entries
+
+
+def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True):
+    """Frame posteriors for a device frame matrix (gmm.py:389-439), all on device."""
+    T, F = x.shape
+    C = diag_tab.C
+    k = min(top_k, C)
+    offsets = _lib.empty((T + 1,), torch.int64)
+    comps = _lib.empty((max(T * k, 1),), torch.int32)
+    wts = _lib.empty((max(T * k, 1),), torch.float32)
+    ws_bytes = int(_lib.load().tvk_align_workspace_bytes(T, k))
+    ws = _lib.empty((max(ws_bytes, 1),), torch.uint8)
+    sel = _lib.empty((T, k), torch.int32) if debug else None
+    sll = _lib.empty((T, k)) if debug else None
+    xp, xf = _lib.x_args(x)
+    call("tvk_align_frames", xp, xf, T, F, ptr(diag_tab.table), ptr(full_tab.table), C, k, float(prune), ptr(ws),
+         ws_bytes, ptr(offsets), ptr(comps), ptr(wts), ptr(sel), ptr(sll), stream())
+    n = int(offsets[T].item()) if sync_count else None
+    res = AlignResult(offsets, comps, wts, n)
+    if debug:
+        res.selected, res.sel_ll = sel, sll
+    return res
+
+
+def bw_stats(x, utt_frames, ali_offsets, comps, wts, C, center=None, want_S=False, ssum_acc=None,
+             entry_capacity=None):
+    """Per-utterance n (U x C), f (U x C x F) [, S (U x C x F x F)] on device (gmm.py:442-492).
+
+    ``utt_frames`` (U+1, int64 device) delimits utterances in ``x``; the alignment CSR covers
+    the same frames.  ``ssum_acc`` (C x F x F) is added to in place when given.
+    """
+    F = x.shape[1]
+    U = utt_frames.shape[0] - 1
+    if entry_capacity is None:
+        entry_capacity = comps.shape[0]
+    n = _lib.empty((U, C))
+    f = _lib.empty((U, C, F))
+    S = _lib.empty((U, C, F, F)) if want_S else None
+    ws_bytes = int(_lib.load().tvk_bw_workspace_bytes(entry_capacity, U, C))
+    ws = _lib.empty((max(ws_bytes, 1),), torch.uint8)
+    xp, xf = _lib.x_args(x)
+    call("tvk_bw_stats", xp, xf, F, ptr(utt_frames), U, ptr(ali_offsets), ptr(comps), ptr(wts), C, ptr(center),
+         ptr(n), ptr(f), ptr(S), ptr(ssum_acc), int(entry_capacity), ptr(ws), ws_bytes, stream())
+    return n, f, S

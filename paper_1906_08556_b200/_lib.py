@@ -1,0 +1,168 @@
+"""ctypes binding of libtvk.so (the C ABI declared in include/tvk.h).
+
+The product path has exactly one implementation: these CUDA kernels.  If the
+library or a CUDA device is missing every entry point raises; there is no CPU
+fallback.  Device memory, streams and host<->device copies are torch
+(plumbing); all arithmetic of the hot path happens inside libtvk.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtvk.so")
+
+TVK_OK = 0
+TVK_OUT_DENSE = 0
+TVK_OUT_PACKED_LOWER = 1
+ITEM_OK = 0
+ITEM_NOT_SPD = 1
+ITEM_CLAMPED = 2
+ITEM_SKIPPED = 4
+
+_p = ctypes.c_void_p
+_i = ctypes.c_int
+_i64 = ctypes.c_int64
+_d = ctypes.c_double
+
+# name -> (restype, argtypes); mirrors include/tvk.h
+SIGNATURES = {
+    "tvk_version": (_i, []),
+    "tvk_last_error": (_i, [ctypes.c_char_p, _i64]),
+    "tvk_dgemm": (_i, [_i, _i, _i, _i, _i, _d, _p, _i64, _i64, _p, _i64, _i64, _d, _p, _i64, _i64, _i, _i, _i,
+                       _p, _p]),
+    "tvk_spd_small": (_i, [_p, _i, _i, _p, _p, _p, _p, _p]),
+    "tvk_diag_table": (_i, [_p, _p, _p, _i, _i, _p, _p]),
+    "tvk_full_table": (_i, [_p, _p, _p, _i, _i, _p, _p, _p]),
+    "tvk_align_workspace_bytes": (_i64, [_i64, _i]),
+    "tvk_align_frames": (_i, [_p, _i, _i64, _i, _p, _p, _i, _i, _d, _p, _i64, _p, _p, _p, _p, _p, _p]),
+    "tvk_select_topk": (_i, [_p, _i, _i64, _i, _p, _i, _i, _p, _p, _p]),
+    "tvk_frame_features": (_i, [_p, _i, _i64, _i, _i, _p, _p]),
+    "tvk_bw_workspace_bytes": (_i64, [_i64, _i, _i]),
+    "tvk_bw_stats": (_i, [_p, _i, _i, _p, _i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i64, _p, _i64, _p]),
+    "tvk_posterior_workspace_bytes": (_i64, [_i, _i]),
+    "tvk_posterior": (_i, [_p, _p, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i64, _p]),
+    "tvk_spd_solve_rows": (_i, [_p, _p, _i, _i, _i, _p, _p, _p, _p, _i64, _p]),
+    "tvk_sigma_floor": (_i, [_p, _p, _p, _p, _i, _i, _d, _p, _p, _p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class TvkError(RuntimeError):
+    """A libtvk call failed (bad argument or CUDA error)."""
+
+
+def load():
+    """Load libtvk.so (raises if it is missing: the product path has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing; build it with `python -m paper_1906_08556_b200.build`")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name, None)
+                if fn is None:
+                    raise ImportError(f"{LIB_PATH} does not export {name}; rebuild the library")
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def last_error():
+    buf = ctypes.create_string_buffer(512)
+    load().tvk_last_error(buf, 512)
+    return buf.value.decode(errors="replace")
+
+
+def call(name, *args):
+    """Invoke a status-returning entry point; raise TvkError on failure."""
+    fn = getattr(load(), name)
+    st = fn(*args)
+    if fn.restype is _i and st != TVK_OK:
+        raise TvkError(f"{name} failed (status {st}): {last_error()}")
+    return st
+
+
+_DEVICE = None
+
+
+def device():
+    """The CUDA device the kernels run on (rank-local under torch.distributed)."""
+    global _DEVICE
+    if _DEVICE is None:
+        if not torch.cuda.is_available():
+            raise TvkError("libtvk needs a CUDA device (B200); no CPU fallback exists")
+        _DEVICE = torch.device("cuda", torch.cuda.current_device())
+    return _DEVICE
+
+
+def stream():
+    return ctypes.c_void_p(torch.cuda.current_stream(device()).cuda_stream)
+
+
+def ptr(t):
+    """Raw device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def to_dev(a, dtype=torch.float64):
+    """Host array -> contiguous device tensor (pinned staging for large copies)."""
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device(), dtype=dtype).contiguous()
+    arr = np.ascontiguousarray(a)
+    t = torch.from_numpy(arr)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.to(device(), non_blocking=False).contiguous()
+
+
+def empty(shape, dtype=torch.float64):
+    return torch.empty(shape, dtype=dtype, device=device())
+
+
+def zeros(shape, dtype=torch.float64):
+    return torch.zeros(shape, dtype=dtype, device=device())
+
+
+def to_host(t):
+    return t.detach().cpu().numpy()
+
+
+# ---------------------------------------------------------------------------- thin typed wrappers
+
+
+def dgemm(a, b, c, m, n, k, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0, lda=None, ldb=None, ldc=None,
+          batch=1, stride_a=0, stride_b=0, stride_c=0, out_mode=TVK_OUT_DENSE, splits=1, work=None):
+    """C = alpha op(A) op(B) + beta C (row-major, FP64, DMMA tensor pipe)."""
+    if lda is None:
+        lda = m if trans_a else k
+    if ldb is None:
+        ldb = k if trans_b else n
+    if ldc is None:
+        ldc = n
+    call("tvk_dgemm", int(trans_a), int(trans_b), m, n, k, alpha, ptr(a), lda, stride_a, ptr(b), ldb, stride_b,
+         beta, ptr(c), ldc, stride_c, batch, out_mode, splits, ptr(work), stream())
+    return c
+
+
+def x_args(x):
+    """(pointer, is_f64) for a float32/float64 device frame matrix."""
+    if x.dtype == torch.float64:
+        return ptr(x), 1
+    if x.dtype == torch.float32:
+        return ptr(x), 0
+    raise TypeError("frames must be float32 or float64")

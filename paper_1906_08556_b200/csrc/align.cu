@@ -1,0 +1,654 @@
+// Frame posteriors (gmm.py:389-439) as three FP64 tensor-pipe stages plus a CSR build:
+//   1. select_topk_kernel: diag log-likelihoods [x^2, x, 1] . Wdiag (DMMA) for 64 frames x
+//      all components, streamed in 64-component blocks, merged into a per-frame stable top-K
+//      (lower index wins ties, gmm.py:410);
+//   2. full_ll_kernel: quadratic-feature GEMM phi(x) . Wq (K = 1+F+F(F+1)/2) for 128 frames x
+//      128 components; the epilogue keeps only the K preselected components of each frame
+//      (gmm.py:412-413) so the T x C log-likelihood matrix never reaches HBM;
+//   3. finalize_kernel: softmax over the selection (scipy logsumexp), prune (post >= prune),
+//      degenerate rule (argmax in selection order), renormalize, sort by component (gmm.py:414-438);
+//   4. exclusive scan of the per-frame counts and a compaction into the CSR arrays.
+#include <math.h>
+
+#include "common.cuh"
+#include "gemm_f64.cuh"
+#include "internal.h"
+#include "spd_small.cuh"
+
+namespace tvk {
+
+constexpr int kMaxTopK = 32;
+
+// ----------------------------------------------------------------------------- tables
+
+__global__ void diag_table_kernel(const double* w, const double* mu, const double* var, int C, int F, double* tab) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double logvar = 0.0, m2 = 0.0;
+  for (int f = 0; f < F; f++) {
+    double p = 1.0 / var[(int64_t)c * F + f];
+    double m = mu[(int64_t)c * F + f];
+    tab[(int64_t)f * C + c] = -0.5 * p;
+    tab[(int64_t)(F + f) * C + c] = m * p;
+    logvar += log(var[(int64_t)c * F + f]);
+    m2 += m * m * p;
+  }
+  tab[(int64_t)(2 * F) * C + c] = log(w[c]) - 0.5 * (F * kLog2Pi + logvar) - 0.5 * m2;
+}
+
+// One CTA per component: Cholesky, precision P = Sigma^-1, log|Sigma|, then the column
+// [k_c, P mu, -P_ii/2 | -P_ij (i<j)] of the quadratic-feature table.
+__global__ void full_table_kernel(const double* w, const double* mu, const double* cov, int C, int F, double* tab,
+                                  int32_t* status) {
+  extern __shared__ double sm[];
+  double* a = sm;
+  double* y = sm + F * F;
+  double* pm = y + F * F;  // P mu
+  __shared__ int bad;
+  __shared__ double red[2];
+  const int c = blockIdx.x;
+  const double* src = cov + (int64_t)c * F * F;
+  for (int i = threadIdx.x; i < F * F; i += blockDim.x) a[i] = src[i];
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  block_cholesky(a, F, &bad);
+  if (bad) {
+    if (threadIdx.x == 0) status[c] = TVK_ITEM_NOT_SPD;
+    return;
+  }
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < F; i += 32) s += log(a[i * F + i]);
+    s = warp_sum(s);
+    if (threadIdx.x == 0) red[0] = 2.0 * s;
+  }
+  __syncthreads();
+  block_spd_inverse(a, y, F);
+  const double* m = mu + (int64_t)c * F;
+  for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < F; j++) s += a[i * F + j] * m[j];
+    pm[i] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < F; i += 32) s += m[i] * pm[i];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) red[1] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tab[c] = log(w[c]) - 0.5 * (F * kLog2Pi + red[0]) - 0.5 * red[1];
+    status[c] = TVK_ITEM_OK;
+  }
+  for (int i = threadIdx.x; i < F; i += blockDim.x) tab[(int64_t)(1 + i) * C + c] = pm[i];
+  // quadratic rows, pair order (i, j>=i) row-major
+  int npair = F * (F + 1) / 2;
+  for (int p = threadIdx.x; p < npair; p += blockDim.x) {
+    // invert p = i*F - i*(i-1)/2 + (j - i)
+    int i = 0, base = 0;
+    while (base + (F - i) <= p) {
+      base += F - i;
+      i++;
+    }
+    int j = i + (p - base);
+    double v = (i == j) ? -0.5 * a[i * F + i] : -a[i * F + j];
+    tab[(int64_t)(1 + F + p) * C + c] = v;
+  }
+}
+
+// ----------------------------------------------------------------------------- stage 1: top-K
+
+namespace sel {
+constexpr int BM = 64, BN = 64, NT = 256;
+using Cfg = GemmCfg<BM, BN, 4, 2, 4, 1>;  // warp tile 32x16; BK field unused (full K resident)
+}
+
+__device__ __forceinline__ bool ranks_before(double v, int i, double w, int j) {  // (v,i) strictly better
+  return v > w || (v == w && i < j);
+}
+
+// dynamic smem: A [BM][KP+4] features, B [KP][BN+4] table block, LL [BM][BN+1], lists
+template <typename XT>
+__global__ void __launch_bounds__(sel::NT) select_topk_kernel(const XT* x, int64_t T, int F, const double* tab,
+                                                              int C, int K, int32_t* sel_out, double* sel_val) {
+  using namespace sel;
+  extern __shared__ __align__(16) double smem[];
+  const int KD = 2 * F + 1;
+  const int KP = (KD + 3) & ~3;
+  const int AS = KP + 4, BS = BN + 4, LS = BN + 1;
+  double* sA = smem;
+  double* sB = sA + BM * AS;
+  double* sL = sB + KP * BS;
+  double* lv = sL + BM * LS;                    // [BM][K]
+  int* li = reinterpret_cast<int*>(lv + BM * K);  // [BM][K]
+  int* lc = li + BM * K;                        // [BM]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int64_t t0 = (int64_t)blockIdx.x * BM;
+
+  // features [x^2, x, 1, 0-pad] for this frame tile
+  for (int idx = tid; idx < BM * KP; idx += NT) {
+    int r = idx / KP, k = idx % KP;
+    double v = 0.0;
+    if (t0 + r < T) {
+      if (k < F) {
+        double xv = (double)x[(t0 + r) * F + k];
+        v = xv * xv;
+      } else if (k < 2 * F) {
+        v = (double)x[(t0 + r) * F + (k - F)];
+      } else if (k == 2 * F) {
+        v = 1.0;
+      }
+    }
+    sA[r * AS + k] = v;
+  }
+  for (int r = tid; r < BM; r += NT) lc[r] = 0;
+
+  for (int n0 = 0; n0 < C; n0 += BN) {
+    __syncthreads();  // previous block's list merge done with sL / sB
+    for (int idx = tid; idx < KP * BN; idx += NT) {
+      int k = idx / BN, c = idx % BN;
+      bool ok = k < KD && n0 + c < C;
+      cp_async8(&sB[k * BS + c], ok ? tab + (int64_t)k * C + n0 + c : tab, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    Acc<Cfg> acc;
+    acc.zero();
+    const int g = lane >> 2, t = lane & 3;
+    for (int kk = 0; kk < KP; kk += 4) {
+      double a[Cfg::FM], b[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; i++) a[i] = sA[(wm * Cfg::WTM + i * 8 + g) * AS + kk + t];
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; j++) b[j] = sB[(kk + t) * BS + wn * Cfg::WTN + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; i++)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; j++) dmma884(acc.v[i][j][0], acc.v[i][j][1], a[i], b[j]);
+    }
+    for_each_acc<Cfg>(acc, wm, wn, lane, [&](int r, int c, double v) { sL[r * LS + c] = v; });
+    __syncthreads();
+
+    // merge this block into each frame's running top-K (one warp per frame at a time)
+    const int nb = min(BN, C - n0);
+    for (int r = warp; r < BM; r += NT / 32) {
+      if (t0 + r >= T) continue;
+      int cnt = lc[r];
+      double myv = (lane < cnt) ? lv[r * K + lane] : -INFINITY;
+      int myi = (lane < cnt) ? li[r * K + lane] : 0x7fffffff;
+      for (int base = 0; base < nb; base += 32) {
+        int ci = base + lane;
+        double cv = ci < nb ? sL[r * LS + ci] : -INFINITY;
+        int gi = n0 + ci;
+        double wv = __shfl_sync(0xffffffffu, myv, K - 1);
+        int wi = __shfl_sync(0xffffffffu, myi, K - 1);
+        bool cand = ci < nb && (cnt < K || ranks_before(cv, gi, wv, wi));
+        unsigned mask = __ballot_sync(0xffffffffu, cand);
+        while (mask) {
+          int src = __ffs(mask) - 1;
+          mask &= mask - 1;
+          double v = __shfl_sync(0xffffffffu, cv, src);
+          int vi = __shfl_sync(0xffffffffu, gi, src);
+          wv = __shfl_sync(0xffffffffu, myv, K - 1);
+          wi = __shfl_sync(0xffffffffu, myi, K - 1);
+          if (cnt == K && !ranks_before(v, vi, wv, wi)) continue;
+          unsigned better = __ballot_sync(0xffffffffu, lane < cnt && ranks_before(myv, myi, v, vi));
+          int pos = __popc(better);
+          double upv = __shfl_up_sync(0xffffffffu, myv, 1);
+          int upi = __shfl_up_sync(0xffffffffu, myi, 1);
+          if (lane > pos) {
+            myv = upv;
+            myi = upi;
+          } else if (lane == pos) {
+            myv = v;
+            myi = vi;
+          }
+          cnt = min(cnt + 1, K);
+        }
+      }
+      if (lane < K) {
+        lv[r * K + lane] = myv;
+        li[r * K + lane] = myi;
+      }
+      if (lane == 0) lc[r] = cnt;
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < BM * K; idx += NT) {
+    int r = idx / K, j = idx % K;
+    if (t0 + r < T) {
+      sel_out[(t0 + r) * K + j] = li[r * K + j];
+      if (sel_val) sel_val[(t0 + r) * K + j] = lv[r * K + j];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- stage 2: full LL
+
+namespace fll {
+using Cfg = GemmCfg<128, 128, 16, 2, 4, 3>;
+}
+
+// A operand: phi_k(x) = xe[i_k] * xe[j_k] with xe = [x, 1]; pairs (F,F) -> 1, (i,F) -> x_i.
+template <typename XT>
+__global__ void __launch_bounds__(fll::Cfg::NT) full_ll_kernel(const XT* x, int64_t T, int F, const double* tab,
+                                                               int C, int K, const int32_t* sel, double* sel_ll) {
+  using Cfg = fll::Cfg;
+  using L = SmemLayout<Cfg::BM, Cfg::BN, Cfg::BK, false, false>;
+  extern __shared__ __align__(16) double smem[];
+  const int Q = 1 + F + F * (F + 1) / 2;
+  double* stages = smem;
+  XT* xs = reinterpret_cast<XT*>(stages + Cfg::STAGES * L::STAGE);  // [BM][F+1]
+  int* pairs = reinterpret_cast<int*>(xs + Cfg::BM * (F + 1));          // [Qpad] packed (i<<16)|j
+  const int Qpad = (Q + Cfg::BK - 1) / Cfg::BK * Cfg::BK;
+  unsigned char* slot = reinterpret_cast<unsigned char*>(pairs + Qpad);  // [BM][BN] selection slot or 255
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int64_t m0 = (int64_t)(blockIdx.x % ((T + Cfg::BM - 1) / Cfg::BM)) * Cfg::BM;
+  const int n0 = (int)(blockIdx.x / ((T + Cfg::BM - 1) / Cfg::BM)) * Cfg::BN;
+  const int FE = F + 1;
+
+  for (int idx = tid; idx < Cfg::BM * FE; idx += Cfg::NT) {
+    int r = idx / FE, f = idx % FE;
+    XT v = XT(0);
+    if (m0 + r < T) v = (f < F) ? x[(m0 + r) * F + f] : XT(1);
+    xs[idx] = v;
+  }
+  for (int k = tid; k < Qpad; k += Cfg::NT) {
+    int i, j;
+    if (k == 0 || k >= Q) {
+      i = F;
+      j = F;
+    } else if (k <= F) {
+      i = k - 1;
+      j = F;
+    } else {
+      int p = k - 1 - F, base = 0;
+      i = 0;
+      while (base + (F - i) <= p) {
+        base += F - i;
+        i++;
+      }
+      j = i + (p - base);
+    }
+    pairs[k] = (i << 16) | j;
+  }
+  for (int idx = tid; idx < Cfg::BM * Cfg::BN; idx += Cfg::NT) slot[idx] = 255;
+  __syncthreads();
+  for (int idx = tid; idx < Cfg::BM * K; idx += Cfg::NT) {
+    int r = idx / K, j = idx % K;
+    if (m0 + r >= T) continue;
+    int c = sel[(m0 + r) * K + j] - n0;
+    if (c >= 0 && c < Cfg::BN) slot[r * Cfg::BN + c] = (unsigned char)j;
+  }
+
+  const int nk = Qpad / Cfg::BK;
+  auto load_stage = [&](int stage, int kt) {
+    double* sA = stages + stage * L::STAGE;
+    double* sB = sA + L::A_ELEMS;
+    int k0 = kt * Cfg::BK;
+    load_tile_async<Cfg::BK, Cfg::BN, Cfg::BN + 4, Cfg::NT, false>(sB, tab, C, k0, n0, Q, C, tid);
+    for (int idx = tid; idx < Cfg::BM * Cfg::BK; idx += Cfg::NT) {
+      int r = idx / Cfg::BK, kk = idx % Cfg::BK;
+      int pr = pairs[k0 + kk];
+      const XT* xr = xs + r * FE;
+      sA[L::a_off(r, kk)] = (double)xr[pr >> 16] * (double)xr[pr & 0xffff];
+    }
+  };
+
+  Acc<Cfg> acc;
+  acc.zero();
+#pragma unroll
+  for (int s = 0; s < Cfg::STAGES - 1; s++) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; kt++) {
+    cp_async_wait<Cfg::STAGES - 2>();
+    __syncthreads();
+    int nxt = kt + Cfg::STAGES - 1;
+    if (nxt < nk) load_stage(nxt % Cfg::STAGES, nxt);
+    cp_async_commit();
+    const double* sA = stages + (kt % Cfg::STAGES) * L::STAGE;
+    mma_stage<Cfg, L>(acc, sA, sA + L::A_ELEMS, wm, wn, lane);
+  }
+  cp_async_wait<0>();
+  for_each_acc<Cfg>(acc, wm, wn, lane, [&](int r, int c, double v) {
+    int j = slot[r * Cfg::BN + c];
+    if (j != 255) sel_ll[(m0 + r) * K + j] = v;
+  });
+}
+
+// ----------------------------------------------------------------------------- stage 3: finalize
+
+__global__ void finalize_kernel(int64_t T, int K, double prune, const int32_t* sel, const double* sel_ll,
+                                int32_t* comp_pad, float* w_pad, int64_t* counts) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  double ll[kMaxTopK];
+  int id[kMaxTopK];
+  double mx = -INFINITY;
+  for (int j = 0; j < K; j++) {
+    ll[j] = sel_ll[t * K + j];
+    id[j] = sel[t * K + j];
+    mx = fmax(mx, ll[j]);
+  }
+  if (!isfinite(mx)) mx = 0.0;  // scipy logsumexp convention
+  double s = 0.0;
+  for (int j = 0; j < K; j++) s += exp(ll[j] - mx);
+  double lse = log(s) + mx;
+  int nkeep = 0, best = 0;
+  for (int j = 0; j < K; j++) {
+    ll[j] = exp(ll[j] - lse);  // posterior over the selection
+    if (ll[j] > ll[best]) best = j;
+    if (ll[j] >= prune) nkeep++;
+  }
+  bool degenerate = nkeep == 0;
+  double tot = 0.0;
+  for (int j = 0; j < K; j++) {
+    bool keep = degenerate ? (j == best) : (ll[j] >= prune);
+    if (!keep) ll[j] = 0.0;
+    tot += ll[j];
+  }
+  // emit kept entries sorted by component (insertion sort, K <= 32)
+  int n = 0;
+  int oc[kMaxTopK];
+  float ow[kMaxTopK];
+  for (int j = 0; j < K; j++) {
+    bool keep = degenerate ? (j == best) : (ll[j] >= prune);
+    if (!keep) continue;
+    float wv = (float)(ll[j] / tot);
+    int c = id[j];
+    int p = n++;
+    while (p > 0 && oc[p - 1] > c) {
+      oc[p] = oc[p - 1];
+      ow[p] = ow[p - 1];
+      p--;
+    }
+    oc[p] = c;
+    ow[p] = wv;
+  }
+  for (int e = 0; e < n; e++) {
+    comp_pad[t * K + e] = oc[e];
+    w_pad[t * K + e] = ow[e];
+  }
+  counts[t] = n;
+}
+
+// ----------------------------------------------------------------------------- stage 4: scan + compact
+
+constexpr int kScanBlock = 1024;
+
+__global__ void scan_block_sums(const int64_t* counts, int64_t T, int64_t* block_sums) {
+  __shared__ int64_t red[32];
+  int64_t base = (int64_t)blockIdx.x * kScanBlock;
+  int64_t s = 0;
+  for (int i = threadIdx.x; i < kScanBlock; i += blockDim.x)
+    if (base + i < T) s += counts[base + i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += red[w];
+    block_sums[blockIdx.x] = tot;
+  }
+}
+
+__global__ void scan_block_prefix(int64_t* block_sums, int nblocks) {
+  // single CTA exclusive scan over the block sums (sequential chunks, parallel within)
+  __shared__ int64_t carry;
+  __shared__ int64_t buf[1024];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nblocks; base += 1024) {
+    int i = base + threadIdx.x;
+    int64_t v = i < nblocks ? block_sums[i] : 0;
+    buf[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      int64_t add = threadIdx.x >= o ? buf[threadIdx.x - o] : 0;
+      __syncthreads();
+      buf[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (i < nblocks) block_sums[i] = carry + buf[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += buf[1023];
+    __syncthreads();
+  }
+}
+
+__global__ void scan_write_offsets(const int64_t* counts, int64_t T, const int64_t* block_prefix, int64_t* offsets) {
+  __shared__ int64_t buf[kScanBlock];
+  int64_t base = (int64_t)blockIdx.x * kScanBlock;
+  int i = threadIdx.x;  // blockDim == kScanBlock
+  int64_t v = base + i < T ? counts[base + i] : 0;
+  buf[i] = v;
+  __syncthreads();
+  for (int o = 1; o < kScanBlock; o <<= 1) {
+    int64_t add = i >= o ? buf[i - o] : 0;
+    __syncthreads();
+    buf[i] += add;
+    __syncthreads();
+  }
+  int64_t pre = block_prefix[blockIdx.x];
+  if (base + i < T) offsets[base + i] = pre + buf[i] - v;
+  if (base + i == T - 1) offsets[T] = pre + buf[i];
+}
+
+__global__ void compact_kernel(int64_t T, int K, const int64_t* offsets, const int32_t* comp_pad, const float* w_pad,
+                               int32_t* comps, float* wts) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int64_t o = offsets[t], n = offsets[t + 1] - o;
+  for (int e = 0; e < n; e++) {
+    comps[o + e] = comp_pad[t * K + e];
+    wts[o + e] = w_pad[t * K + e];
+  }
+}
+
+int exclusive_scan_counts(const int64_t* counts, int64_t T, int64_t* offsets, int64_t* block_sums, cudaStream_t st) {
+  int nb = (int)((T + kScanBlock - 1) / kScanBlock);
+  scan_block_sums<<<nb, 256, 0, st>>>(counts, T, block_sums);
+  scan_block_prefix<<<1, 1024, 0, st>>>(block_sums, nb);
+  scan_write_offsets<<<nb, kScanBlock, 0, st>>>(counts, T, block_sums, offsets);
+  TVK_CHECK_LAUNCH("scan");
+  return TVK_OK;
+}
+
+static size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct AlignWs {
+  int32_t* sel;
+  double* sel_ll;
+  int32_t* comp_pad;
+  float* w_pad;
+  int64_t* counts;
+  int64_t* block_sums;
+  size_t bytes;
+};
+
+static AlignWs carve(void* base, int64_t T, int K) {
+  AlignWs w{};
+  size_t off = 0;
+  char* b = (char*)base;
+  auto take = [&](size_t n) {
+    char* p = b ? b + off : nullptr;
+    off += align_up(n);
+    return p;
+  };
+  w.sel = (int32_t*)take(sizeof(int32_t) * T * K);
+  w.sel_ll = (double*)take(sizeof(double) * T * K);
+  w.comp_pad = (int32_t*)take(sizeof(int32_t) * T * K);
+  w.w_pad = (float*)take(sizeof(float) * T * K);
+  w.counts = (int64_t*)take(sizeof(int64_t) * (T + 1));
+  w.block_sums = (int64_t*)take(sizeof(int64_t) * ((T + kScanBlock - 1) / kScanBlock + 1));
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace tvk
+
+using namespace tvk;
+
+extern "C" int tvk_diag_table(const double* weights, const double* means, const double* variances, int C, int F,
+                              double* table, void* stream) {
+  TVK_REQUIRE(C >= 1 && F >= 1, "diag_table: empty model");
+  diag_table_kernel<<<ceil_div(C, 128), 128, 0, (cudaStream_t)stream>>>(weights, means, variances, C, F, table);
+  TVK_CHECK_LAUNCH("diag_table");
+  return TVK_OK;
+}
+
+extern "C" int tvk_full_table(const double* weights, const double* means, const double* covariances, int C, int F,
+                              double* table, int32_t* status, void* stream) {
+  TVK_REQUIRE(C >= 1 && F >= 1 && F <= kSmallSpdMax, "full_table: need 1 <= F <= 96");
+  TVK_REQUIRE(F < 32767, "full_table: F too large");
+  size_t smem = sizeof(double) * (2 * F * F + F);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(full_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * (2 * kSmallSpdMax * kSmallSpdMax + kSmallSpdMax)));
+    attr = true;
+  }
+  full_table_kernel<<<C, 256, smem, (cudaStream_t)stream>>>(weights, means, covariances, C, F, table, status);
+  TVK_CHECK_LAUNCH("full_table");
+  return TVK_OK;
+}
+
+extern "C" int64_t tvk_align_workspace_bytes(int64_t T, int K) { return (int64_t)carve(nullptr, T, K).bytes; }
+
+namespace tvk {
+
+template <typename XT>
+static int launch_select(const XT* x, int64_t T, int F, const double* diag_table, int C, int K, int32_t* sel,
+                         double* val, cudaStream_t st) {
+  using namespace sel;
+  int KP = ((2 * F + 1) + 3) & ~3;
+  size_t smem = sizeof(double) * (BM * (KP + 4) + KP * (BN + 4) + BM * (BN + 1) + BM * K) + sizeof(int) * (BM * K + BM);
+  TVK_REQUIRE(smem <= 227 * 1024, "align_frames: F too large for the preselection tile");
+  cudaFuncSetAttribute(select_topk_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int64_t grid = (T + BM - 1) / BM;
+  TVK_REQUIRE(grid < (1ll << 31), "align_frames: too many frames for one call");
+  select_topk_kernel<XT><<<(unsigned)grid, NT, smem, st>>>(x, T, F, diag_table, C, K, sel, val);
+  TVK_CHECK_LAUNCH("select_topk");
+  return TVK_OK;
+}
+
+template <typename XT>
+static int launch_full_ll(const XT* x, int64_t T, int F, const double* full_table, int C, int K, const int32_t* sel,
+                          double* sel_ll, cudaStream_t st) {
+  using Cfg = fll::Cfg;
+  using L = SmemLayout<Cfg::BM, Cfg::BN, Cfg::BK, false, false>;
+  int Q = 1 + F + F * (F + 1) / 2;
+  int Qpad = (Q + Cfg::BK - 1) / Cfg::BK * Cfg::BK;
+  size_t smem = sizeof(double) * Cfg::STAGES * L::STAGE + sizeof(XT) * Cfg::BM * (F + 1) + sizeof(int) * Qpad +
+                Cfg::BM * Cfg::BN;
+  TVK_REQUIRE(smem <= 227 * 1024, "align_frames: F too large for the full-covariance tile");
+  cudaFuncSetAttribute(full_ll_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int64_t mt = (T + Cfg::BM - 1) / Cfg::BM, nt = (C + Cfg::BN - 1) / Cfg::BN;
+  TVK_REQUIRE(mt * nt < (1ll << 31), "align_frames: too many frames for one call");
+  full_ll_kernel<XT><<<(unsigned)(mt * nt), Cfg::NT, smem, st>>>(x, T, F, full_table, C, K, sel, sel_ll);
+  TVK_CHECK_LAUNCH("full_ll");
+  return TVK_OK;
+}
+
+template <typename XT>
+__global__ void frame_features_kernel(const XT* x, int64_t T, int F, int kind, double* out) {
+  // kind 0: [x^2, x, 1] (2F+1); kind 1: [1, x_i, x_i x_j (i<=j)] (1+F+F(F+1)/2)
+  int Q = kind == 0 ? 2 * F + 1 : 1 + F + F * (F + 1) / 2;
+  int64_t total = T * Q;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = idx / Q;
+    int k = (int)(idx % Q);
+    const XT* xr = x + t * F;
+    double v;
+    if (kind == 0) {
+      v = k < F ? (double)xr[k] * (double)xr[k] : (k < 2 * F ? (double)xr[k - F] : 1.0);
+    } else if (k == 0) {
+      v = 1.0;
+    } else if (k <= F) {
+      v = (double)xr[k - 1];
+    } else {
+      int p = k - 1 - F, i = 0, base = 0;
+      while (base + (F - i) <= p) {
+        base += F - i;
+        i++;
+      }
+      v = (double)xr[i] * (double)xr[i + (p - base)];
+    }
+    out[idx] = v;
+  }
+}
+
+template <typename XT>
+static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, const double* full_table, int C,
+                      int K, double prune, void* workspace, int64_t workspace_bytes, int64_t* offsets,
+                      int32_t* components, float* weights, int32_t* selected, double* sel_ll_out, cudaStream_t st) {
+  AlignWs w = carve(workspace, T, K);
+  TVK_REQUIRE(workspace != nullptr && (int64_t)w.bytes <= workspace_bytes, "align_frames: workspace too small");
+  TVK_TRY(launch_select<XT>(x, T, F, diag_table, C, K, w.sel, nullptr, st));
+  TVK_TRY(launch_full_ll<XT>(x, T, F, full_table, C, K, w.sel, w.sel_ll, st));
+  int fb = (int)((T + 127) / 128);
+  finalize_kernel<<<fb, 128, 0, st>>>(T, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts);
+  TVK_CHECK_LAUNCH("finalize");
+  TVK_TRY(exclusive_scan_counts(w.counts, T, offsets, w.block_sums, st));
+  compact_kernel<<<fb, 128, 0, st>>>(T, K, offsets, w.comp_pad, w.w_pad, components, weights);
+  TVK_CHECK_LAUNCH("compact");
+  if (selected) cudaMemcpyAsync(selected, w.sel, sizeof(int32_t) * T * K, cudaMemcpyDeviceToDevice, st);
+  if (sel_ll_out) cudaMemcpyAsync(sel_ll_out, w.sel_ll, sizeof(double) * T * K, cudaMemcpyDeviceToDevice, st);
+  TVK_CHECK_LAUNCH("align_frames copies");
+  return TVK_OK;
+}
+
+}  // namespace tvk
+
+extern "C" int tvk_align_frames(const void* x, int x_f64, int64_t T, int F, const double* diag_table,
+                                const double* full_table, int C, int K, double prune, void* workspace,
+                                int64_t workspace_bytes, int64_t* offsets, int32_t* components, float* weights,
+                                int32_t* selected, double* sel_ll_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1, "align_frames: bad shape");
+  TVK_REQUIRE(K >= 1 && K <= kMaxTopK && K <= C, "align_frames: top_k must be in [1, min(C, 32)]");
+  TVK_REQUIRE(F <= 255, "align_frames: F too large");
+  if (T == 0) {
+    cudaMemsetAsync(offsets, 0, sizeof(int64_t), st);
+    TVK_CHECK_LAUNCH("align_frames memset");
+    return TVK_OK;
+  }
+  if (x_f64)
+    return align_impl<double>((const double*)x, T, F, diag_table, full_table, C, K, prune, workspace,
+                              workspace_bytes, offsets, components, weights, selected, sel_ll_out, st);
+  return align_impl<float>((const float*)x, T, F, diag_table, full_table, C, K, prune, workspace, workspace_bytes,
+                           offsets, components, weights, selected, sel_ll_out, st);
+}
+
+extern "C" int tvk_select_topk(const void* x, int x_f64, int64_t T, int F, const double* diag_table, int C, int K,
+                               int32_t* selected, double* values, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1, "select_topk: bad shape");
+  TVK_REQUIRE(K >= 1 && K <= kMaxTopK && K <= C, "select_topk: k must be in [1, min(C, 32)]");
+  if (T == 0) return TVK_OK;
+  if (x_f64) return launch_select<double>((const double*)x, T, F, diag_table, C, K, selected, values, st);
+  return launch_select<float>((const float*)x, T, F, diag_table, C, K, selected, values, st);
+}
+
+extern "C" int tvk_frame_features(const void* x, int x_f64, int64_t T, int F, int kind, double* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TVK_REQUIRE(T >= 0 && F >= 1 && (kind == 0 || kind == 1), "frame_features: bad arguments");
+  if (T == 0) return TVK_OK;
+  int64_t Q = kind == 0 ? 2 * F + 1 : 1 + F + (int64_t)F * (F + 1) / 2;
+  int blocks = (int)std::min<int64_t>((T * Q + 255) / 256, 148 * 32);
+  if (x_f64)
+    frame_features_kernel<double><<<blocks, 256, 0, st>>>((const double*)x, T, F, kind, out);
+  else
+    frame_features_kernel<float><<<blocks, 256, 0, st>>>((const float*)x, T, F, kind, out);
+  TVK_CHECK_LAUNCH("frame_features");
+  return TVK_OK;
+}

@@ -1,0 +1,312 @@
+// Baum-Welch statistics (gmm.py:442-492), deterministic (no floating-point atomics).
+//
+// bw_first_order_kernel: one CTA per utterance.  The utterance's alignment entries are
+// counting-sorted by component in shared memory (stable: frame order is kept inside a
+// component, gmm.py:479 uses a stable argsort), then one warp per component sums
+//   n_c = sum w,   f_c = sum w (x - m_c)
+// in frame order and writes dense rows of N (U x C) and F (U x C*F) -- the operands of
+// the E-step GEMMs.  Optionally the per-utterance second order S (API path).
+//
+// bw_second_order_kernel: one CTA per component accumulates the corpus second-order sum
+//   Ssum_c += sum_u sum_t w (x - m_c)(x - m_c)^T
+// over the component's runs, utterance by utterance, each accumulator element owned by one
+// thread (fixed summation order).
+#include "common.cuh"
+#include "internal.h"
+
+namespace tvk {
+
+constexpr int kBwThreads = 256;
+constexpr int kBwMaxC = 8192;
+
+struct BwWs {
+  int32_t* ent_frame;   // [Ecap] frame of each entry
+  int32_t* sorted_frame;  // [Ecap] entries of each utterance sorted by component
+  double* sorted_w;     // [Ecap]
+  int32_t* comp_start;  // [U][C+1] run starts (relative to the utterance's first entry)
+  size_t bytes;
+};
+
+static size_t aup(size_t v) { return (v + 255) & ~size_t(255); }
+
+static BwWs bw_carve(void* base, int64_t E, int U, int C) {
+  BwWs w{};
+  char* b = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    char* p = b ? b + off : nullptr;
+    off += aup(n);
+    return p;
+  };
+  w.ent_frame = (int32_t*)take(sizeof(int32_t) * (E + 1));
+  w.sorted_frame = (int32_t*)take(sizeof(int32_t) * (E + 1));
+  w.sorted_w = (double*)take(sizeof(double) * (E + 1));
+  w.comp_start = (int32_t*)take(sizeof(int32_t) * (int64_t)U * (C + 1));
+  w.bytes = off;
+  return w;
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(kBwThreads) bw_first_order_kernel(
+    const XT* x, int F, const int64_t* utt_frames, const int64_t* ali_off, const int32_t* comps,
+    const float* wts, int C, const double* center, double* n_out, double* f_out, double* S_out, BwWs ws) {
+  extern __shared__ int cnt[];  // [C+1] counts -> starts -> cursors
+  __shared__ int part[kBwThreads];
+  const int u = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t t0 = utt_frames[u], t1 = utt_frames[u + 1];
+  const int64_t ebase = ali_off[utt_frames[0]];
+  const int64_t e0 = ali_off[t0], e1 = ali_off[t1];
+  const int ne = (int)(e1 - e0);
+  const int64_t r0 = e0 - ebase;  // this utterance's region in the sorted arrays
+
+  for (int c = tid; c <= C; c += kBwThreads) cnt[c] = 0;
+  for (int64_t t = t0 + tid; t < t1; t += kBwThreads)
+    for (int64_t e = ali_off[t]; e < ali_off[t + 1]; e++) ws.ent_frame[e - ebase] = (int32_t)t;
+  __syncthreads();
+  for (int i = tid; i < ne; i += kBwThreads) atomicAdd(&cnt[comps[e0 + i]], 1);  // integer: exact
+  __syncthreads();
+  // exclusive scan of cnt[0..C) -> starts; cnt[C] = ne
+  {
+    int per = (C + kBwThreads - 1) / kBwThreads;
+    int lo = tid * per, hi = min(lo + per, C);
+    int s = 0;
+    for (int c = lo; c < hi; c++) s += cnt[c];
+    part[tid] = s;
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int i = 0; i < kBwThreads; i++) {
+        int v = part[i];
+        part[i] = run;
+        run += v;
+      }
+    }
+    __syncthreads();
+    int run = part[tid];
+    for (int c = lo; c < hi; c++) {
+      int v = cnt[c];
+      cnt[c] = run;
+      run += v;
+    }
+    if (tid == 0) cnt[C] = ne;
+    __syncthreads();
+  }
+  int32_t* cs = ws.comp_start + (int64_t)u * (C + 1);
+  for (int c = tid; c <= C; c += kBwThreads) cs[c] = cnt[c];
+  __syncthreads();
+  // stable scatter (warp 0, entries in order): cnt[] becomes the running cursor
+  if (warp == 0) {
+    for (int base = 0; base < ne; base += 32) {
+      int i = base + lane;
+      bool act = i < ne;
+      unsigned am = __ballot_sync(0xffffffffu, act);
+      if (!act) continue;
+      int key = comps[e0 + i];
+      unsigned peers = __match_any_sync(am, key);
+      int leader = __ffs(peers) - 1;
+      int rank = __popc(peers & ((1u << lane) - 1));
+      int p0 = 0;
+      if (lane == leader) {
+        p0 = cnt[key];
+        cnt[key] = p0 + __popc(peers);
+      }
+      p0 = __shfl_sync(am, p0, leader);
+      int pos = p0 + rank;
+      ws.sorted_frame[r0 + pos] = ws.ent_frame[e0 - ebase + i];
+      ws.sorted_w[r0 + pos] = (double)wts[e0 + i];
+    }
+  }
+  __syncthreads();
+  // one warp per component: n_c, f_c (dense rows, zero for absent components)
+  double* nrow = n_out + (int64_t)u * C;
+  double* frow = f_out + (int64_t)u * C * F;
+  for (int c = warp; c < C; c += kBwThreads / 32) {
+    int s = cs[c], n = cs[c + 1] - s;
+    double* fc = frow + (int64_t)c * F;
+    if (n == 0) {
+      for (int j = lane; j < F; j += 32) fc[j] = 0.0;
+      if (lane == 0) nrow[c] = 0.0;
+      continue;
+    }
+    const double* mc = center ? center + (int64_t)c * F : nullptr;
+    double occ = 0.0;
+    for (int j0 = 0; j0 < F; j0 += 32) {
+      int j = j0 + lane;
+      double acc = 0.0;
+      double occ_j = 0.0;
+      for (int r = 0; r < n; r++) {
+        int t = ws.sorted_frame[r0 + s + r];
+        double w = ws.sorted_w[r0 + s + r];
+        occ_j += w;
+        if (j < F) {
+          double xv = (double)x[(int64_t)t * F + j];
+          if (mc) xv -= mc[j];
+          acc += w * xv;
+        }
+      }
+      if (j < F) fc[j] = acc;
+      occ = occ_j;
+    }
+    if (lane == 0) nrow[c] = occ;
+  }
+  if (S_out == nullptr) return;
+  // per-utterance second order (reference API path): S_c = sym(sum (x w) x^T)
+  double* Srow = S_out + (int64_t)u * C * F * F;
+  for (int c = warp; c < C; c += kBwThreads / 32) {
+    int s = cs[c], n = cs[c + 1] - s;
+    double* Sc = Srow + (int64_t)c * F * F;
+    const double* mc = center ? center + (int64_t)c * F : nullptr;
+    for (int p = lane; p < F * F; p += 32) {
+      int i = p / F, j = p % F;
+      if (j > i) continue;
+      double acc = 0.0;
+      for (int r = 0; r < n; r++) {
+        int t = ws.sorted_frame[r0 + s + r];
+        double w = ws.sorted_w[r0 + s + r];
+        double xi = (double)x[(int64_t)t * F + i], xj = (double)x[(int64_t)t * F + j];
+        if (mc) {
+          xi -= mc[i];
+          xj -= mc[j];
+        }
+        acc += (xi * w) * xj;
+      }
+      Sc[i * F + j] = acc;
+      Sc[j * F + i] = acc;
+    }
+  }
+}
+
+constexpr int kSoBatch = 32;       // entries staged per round
+constexpr int kSoMaxPairs = 8;     // pairs per thread (F(F+1)/2 <= 8*256 -> F <= 63)
+constexpr int kSoUttChunk = 1024;  // utterance runs gathered per pass
+
+template <typename XT>
+__global__ void __launch_bounds__(kBwThreads) bw_second_order_kernel(const XT* x, int F, int U, int C,
+                                                                     const int64_t* utt_frames,
+                                                                     const int64_t* ali_off, const double* center,
+                                                                     double* ssum, BwWs ws) {
+  __shared__ int run_s[kSoUttChunk], run_n[kSoUttChunk];
+  __shared__ int64_t run_r0[kSoUttChunk];
+  __shared__ double xe[kSoBatch][64];
+  __shared__ double we[kSoBatch];
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const int npair = F * (F + 1) / 2;
+  int pi[kSoMaxPairs], pj[kSoMaxPairs];
+  double acc[kSoMaxPairs];
+#pragma unroll
+  for (int k = 0; k < kSoMaxPairs; k++) {
+    int p = tid + k * kBwThreads;
+    int i = 0, base = 0;
+    if (p < npair) {
+      while (base + (i + 1) <= p) {  // row-major lower: row i has i+1 entries
+        base += i + 1;
+        i++;
+      }
+    }
+    pi[k] = i;
+    pj[k] = p - base;
+    acc[k] = 0.0;
+  }
+  const int64_t ebase = ali_off[utt_frames[0]];
+  const double* mc = center ? center + (int64_t)c * F : nullptr;
+  for (int u0 = 0; u0 < U; u0 += kSoUttChunk) {
+    int nu = min(kSoUttChunk, U - u0);
+    __syncthreads();
+    for (int k = tid; k < nu; k += kBwThreads) {
+      const int32_t* cs = ws.comp_start + (int64_t)(u0 + k) * (C + 1);
+      run_s[k] = cs[c];
+      run_n[k] = cs[c + 1] - cs[c];
+      run_r0[k] = ali_off[utt_frames[u0 + k]] - ebase;
+    }
+    __syncthreads();
+    // walk the runs in utterance order, staging kSoBatch entries at a time
+    int k = 0, r = 0;
+    while (true) {
+      // collect the next batch positions (identical walk in every thread)
+      int kk = k, rr = r, nb = 0;
+      int64_t pos[kSoBatch];
+      while (nb < kSoBatch && kk < nu) {
+        if (rr < run_n[kk]) {
+          pos[nb++] = run_r0[kk] + run_s[kk] + rr;
+          rr++;
+        } else {
+          kk++;
+          rr = 0;
+        }
+      }
+      if (nb == 0) break;
+      __syncthreads();
+      for (int idx = tid; idx < nb * F; idx += kBwThreads) {
+        int e = idx / F, j = idx % F;
+        int t = ws.sorted_frame[pos[e]];
+        double v = (double)x[(int64_t)t * F + j];
+        if (mc) v -= mc[j];
+        xe[e][j] = v;
+      }
+      for (int e = tid; e < nb; e += kBwThreads) we[e] = ws.sorted_w[pos[e]];
+      __syncthreads();
+      for (int e = 0; e < nb; e++) {
+        double w = we[e];
+#pragma unroll
+        for (int q = 0; q < kSoMaxPairs; q++)
+          if (tid + q * kBwThreads < npair) acc[q] += (xe[e][pi[q]] * w) * xe[e][pj[q]];
+      }
+      k = kk;
+      r = rr;
+    }
+  }
+  double* S = ssum + (int64_t)c * F * F;
+#pragma unroll
+  for (int q = 0; q < kSoMaxPairs; q++) {
+    if (tid + q * kBwThreads >= npair) continue;
+    int i = pi[q], j = pj[q];
+    double v = S[i * F + j] + acc[q];
+    S[i * F + j] = v;
+    if (i != j) S[j * F + i] = v;
+  }
+}
+
+}  // namespace tvk
+
+using namespace tvk;
+
+extern "C" int64_t tvk_bw_workspace_bytes(int64_t E, int U, int C) { return (int64_t)bw_carve(nullptr, E, U, C).bytes; }
+
+extern "C" int tvk_bw_stats(const void* x, int x_f64, int F, const int64_t* utt_frames, int U, const int64_t* ali_offsets,
+                            const int32_t* components, const float* weights, int C, const double* center,
+                            double* n_out, double* f_out, double* S_out, double* ssum_acc, int64_t entry_capacity,
+                            void* workspace, int64_t workspace_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TVK_REQUIRE(F >= 1 && C >= 1 && U >= 0, "bw_stats: bad shape");
+  TVK_REQUIRE(C <= kBwMaxC, "bw_stats: C > 8192 not supported");
+  if (U == 0) return TVK_OK;
+  TVK_REQUIRE(workspace != nullptr, "bw_stats: workspace required");
+  TVK_REQUIRE((int64_t)bw_carve(nullptr, entry_capacity, U, C).bytes <= workspace_bytes,
+              "bw_stats: workspace too small for the entry capacity");
+  BwWs ws = bw_carve(workspace, entry_capacity, U, C);
+  size_t smem = sizeof(int) * (C + 1);
+  if (x_f64) {
+    cudaFuncSetAttribute(bw_first_order_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    bw_first_order_kernel<double><<<U, kBwThreads, smem, st>>>((const double*)x, F, utt_frames, ali_offsets,
+                                                               components, weights, C, center, n_out, f_out, S_out,
+                                                               ws);
+  } else {
+    cudaFuncSetAttribute(bw_first_order_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    bw_first_order_kernel<float><<<U, kBwThreads, smem, st>>>((const float*)x, F, utt_frames, ali_offsets,
+                                                              components, weights, C, center, n_out, f_out, S_out,
+                                                              ws);
+  }
+  TVK_CHECK_LAUNCH("bw_first_order");
+  if (ssum_acc) {
+    TVK_REQUIRE(F <= 63, "bw_stats: corpus second order supports F <= 63");
+    if (x_f64)
+      bw_second_order_kernel<double><<<C, kBwThreads, 0, st>>>((const double*)x, F, U, C, utt_frames, ali_offsets,
+                                                               center, ssum_acc, ws);
+    else
+      bw_second_order_kernel<float><<<C, kBwThreads, 0, st>>>((const float*)x, F, U, C, utt_frames, ali_offsets,
+                                                              center, ssum_acc, ws);
+    TVK_CHECK_LAUNCH("bw_second_order");
+  }
+  return TVK_OK;
+}

@@ -1,0 +1,423 @@
+// Batched SPD factor / inverse / solve for the i-vector posterior (tvm.py:183-215) and the
+// T update (tvm.py:317-334), on packed-lower D x D matrices (D = 400 at the configs).
+//
+// One CTA per matrix (persistent over the batch), 8 warps.  Blocked right-looking Cholesky
+// in place on the packed storage with 32-wide panels; every O(D^3) part is a 32x32x32 tile
+// product on the FP64 tensor pipe (DMMA.8x8x4) whose fragments are loaded straight from the
+// (L2-resident) packed matrix:
+//   potrf  : diag block in shared memory, panel TRSM row-parallel, trailing SYRK as tile MMAs
+//   trtri  : Y = R^-1 row block by row block (T_IJ = sum_K R_IK Y_KJ staged in shared memory)
+//   lauum  : Phi = Y^T Y tile MMAs, epilogue adds phi phi^T and writes the packed moment
+//            M = Phi + phi phi^T that the A-accumulation GEMM consumes (tvm.py:298-301)
+//   solves : phi = L^-1 b by forward/backward substitution with R (cho_solve semantics).
+#include <math.h>
+
+#include "common.cuh"
+#include "internal.h"
+#include "spd_small.cuh"
+
+namespace tvk {
+
+constexpr int PT = 256;  // threads per CTA
+constexpr int NB = 32;   // panel / tile width
+constexpr int kPosteriorMaxD = 768;
+
+struct Opnd {
+  const double* p;
+  int64_t ld;  // dense leading dimension (packed_n == 0)
+  int n;       // packed order (> 0) or dense rows
+  int ncols;   // dense cols
+  int r0, c0;
+  bool packed, trans;
+};
+
+__device__ __forceinline__ Opnd packed_op(const double* p, int n, int r0, int c0, bool trans) {
+  Opnd o;
+  o.p = p;
+  o.ld = 0;
+  o.n = n;
+  o.ncols = n;
+  o.r0 = r0;
+  o.c0 = c0;
+  o.packed = true;
+  o.trans = trans;
+  return o;
+}
+__device__ __forceinline__ Opnd dense_op(const double* p, int64_t ld, int nr, int nc, int r0, int c0, bool trans) {
+  Opnd o;
+  o.p = p;
+  o.ld = ld;
+  o.n = nr;
+  o.ncols = nc;
+  o.r0 = r0;
+  o.c0 = c0;
+  o.packed = false;
+  o.trans = trans;
+  return o;
+}
+
+__device__ __forceinline__ double ld_elem(const Opnd& o, int r, int c) {
+  if (o.packed) return (r < o.n && c <= r && c >= 0) ? o.p[packed_index(r, c)] : 0.0;
+  return (r < o.n && c < o.ncols && r >= 0 && c >= 0) ? o.p[(int64_t)r * o.ld + c] : 0.0;
+}
+
+// acc(32x32) += A(32 x klen) * B(klen x 32); A logical (i,k), B logical (k,j).
+__device__ __forceinline__ void tile_mma(double (&acc)[4][4][2], const Opnd& A, const Opnd& B, int klen, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  double a[8][4], b[8][4];
+#pragma unroll
+  for (int ks = 0; ks < 8; ks++) {
+    int k = ks * 4 + t;
+    bool kin = k < klen;
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+      int i = f * 8 + g;
+      double av = 0.0, bv = 0.0;
+      if (kin) {
+        av = A.trans ? ld_elem(A, A.r0 + k, A.c0 + i) : ld_elem(A, A.r0 + i, A.c0 + k);
+        bv = B.trans ? ld_elem(B, B.r0 + i, B.c0 + k) : ld_elem(B, B.r0 + k, B.c0 + i);
+      }
+      a[ks][f] = av;
+      b[ks][f] = bv;
+    }
+  }
+#pragma unroll
+  for (int ks = 0; ks < 8; ks++)
+#pragma unroll
+    for (int fi = 0; fi < 4; fi++)
+#pragma unroll
+      for (int fj = 0; fj < 4; fj++) dmma884(acc[fi][fj][0], acc[fi][fj][1], a[ks][fi], b[ks][fj]);
+}
+
+__device__ __forceinline__ void zero_acc(double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+template <class Fn>
+__device__ __forceinline__ void acc_foreach(const double (&acc)[4][4][2], int lane, Fn&& fn) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int fi = 0; fi < 4; fi++)
+#pragma unroll
+    for (int fj = 0; fj < 4; fj++) {
+      fn(fi * 8 + g, fj * 8 + 2 * t, acc[fi][fj][0]);
+      fn(fi * 8 + g, fj * 8 + 2 * t + 1, acc[fi][fj][1]);
+    }
+}
+
+// ------------------------------------------------------------------ blocked Cholesky (in place, packed)
+
+// Returns false (uniformly across the CTA) if the matrix is not positive definite.
+__device__ bool packed_cholesky(double* P, int n, double* sdiag /* NB*NB */, int* bad) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nblk = (n + NB - 1) / NB;
+  for (int kb = 0; kb < nblk; kb++) {
+    const int k0 = kb * NB, kw = min(NB, n - k0);
+    // (1) factor the diagonal block in shared memory
+    for (int idx = tid; idx < kw * kw; idx += PT) {
+      int r = idx / kw, c = idx % kw;
+      sdiag[idx] = c <= r ? P[packed_index(k0 + r, k0 + c)] : 0.0;
+    }
+    if (tid == 0) *bad = 0;
+    __syncthreads();
+    block_cholesky(sdiag, kw, bad);
+    __syncthreads();
+    if (*bad) return false;
+    for (int idx = tid; idx < kw * kw; idx += PT) {
+      int r = idx / kw, c = idx % kw;
+      if (c <= r) P[packed_index(k0 + r, k0 + c)] = sdiag[idx];
+    }
+    // (2) panel: rows below, X = W R_kk^-T (row-parallel forward substitution)
+    for (int i = k0 + kw + tid; i < n; i += PT) {
+      double* row = P + packed_index(i, k0);
+      double x[NB];
+#pragma unroll
+      for (int j = 0; j < NB; j++) x[j] = j < kw ? row[j] : 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; j++) {
+        if (j < kw) {
+          double s = x[j];
+#pragma unroll
+          for (int l = 0; l < j; l++) s -= x[l] * sdiag[j * kw + l];
+          x[j] = s / sdiag[j * kw + j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NB; j++)
+        if (j < kw) row[j] = x[j];
+    }
+    __syncthreads();
+    // (3) trailing update of the lower triangle: C_IJ -= P_I P_J^T, tiles I >= J > kb
+    const int nt = nblk - kb - 1;
+    const int ntiles = nt * (nt + 1) / 2;
+    for (int tix = warp; tix < ntiles; tix += PT / 32) {
+      int I = 0, base = 0;
+      while (base + I + 1 <= tix) {
+        base += I + 1;
+        I++;
+      }
+      int J = tix - base;
+      const int i0 = k0 + kw + I * NB, j0 = k0 + kw + J * NB;
+      double acc[4][4][2];
+      zero_acc(acc);
+      tile_mma(acc, packed_op(P, n, i0, k0, false), packed_op(P, n, j0, k0, true), kw, lane);
+      acc_foreach(acc, lane, [&](int r, int c, double v) {
+        int gi = i0 + r, gj = j0 + c;
+        if (gi < n && gj <= gi) P[packed_index(gi, gj)] -= v;
+      });
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// forward R z = b then backward R^T x = z (warp 0), z/x in shared memory (in place in v)
+__device__ void packed_cho_solve_warp(const double* P, int n, double* v, int lane) {
+  for (int i = 0; i < n; i++) {
+    const double* row = P + packed_index(i, 0);
+    double s = 0.0;
+    for (int j = lane; j < i; j += 32) s += row[j] * v[j];
+    s = warp_sum(s);
+    if (lane == 0) v[i] = (v[i] - s) / row[i];
+    __syncwarp();
+  }
+  for (int i = n - 1; i >= 0; i--) {
+    const double* row = P + packed_index(i, 0);
+    double xi = v[i] / row[i];
+    __syncwarp();
+    for (int j = lane; j < i; j += 32) v[j] -= row[j] * xi;
+    if (lane == 0) v[i] = xi;
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ posterior kernel
+
+__global__ void __launch_bounds__(PT, 1) posterior_kernel(double* lpk, const double* bvec, int U, int D,
+                                                          int flags, double* phi_out, double* mpk,
+                                                          double* logdet_out, double* bphi_out, int32_t* status) {
+  extern __shared__ __align__(16) double sm[];
+  const int ldt = ((D + 11) / 16) * 16 + 4;  // row stride of T-temp, == 4 (mod 16): conflict-free
+  double* tmp = sm;                           // [NB][ldt]  T_IJ = sum_K R_IK Y_KJ for one row block
+  double* sdiag = tmp + NB * ldt;             // [NB*NB]
+  double* sinv = sdiag + NB * NB;             // [NB*NB]   Y_II
+  double* vb = sinv + NB * NB;                // [D]       phi
+  __shared__ int bad;
+  __shared__ double red;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t P = packed_size(D);
+  const int nblk = (D + NB - 1) / NB;
+
+  for (int u = blockIdx.x; u < U; u += gridDim.x) {
+    double* L = lpk + (int64_t)u * P;
+    if (flags & TVK_POST_ADD_IDENTITY)
+      for (int i = tid; i < D; i += PT) L[packed_index(i, i)] += 1.0;
+    __syncthreads();
+    if (!packed_cholesky(L, D, sdiag, &bad)) {
+      if (tid == 0 && status) status[u] = TVK_ITEM_NOT_SPD;
+      continue;
+    }
+    if (tid == 0 && status) status[u] = TVK_ITEM_OK;
+    // log|L| and phi = L^-1 b (cho_solve)
+    for (int i = tid; i < D; i += PT) vb[i] = bvec[(int64_t)u * D + i];
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+      for (int i = lane; i < D; i += 32) s += log(L[packed_index(i, i)]);
+      s = warp_sum(s);
+      if (lane == 0) red = 2.0 * s;
+      packed_cho_solve_warp(L, D, vb, lane);
+    }
+    __syncthreads();
+    for (int i = tid; i < D; i += PT) phi_out[(int64_t)u * D + i] = vb[i];
+    if (warp == 1 && (bphi_out || logdet_out)) {
+      double s = 0.0;
+      for (int i = lane; i < D; i += 32) s += bvec[(int64_t)u * D + i] * vb[i];
+      s = warp_sum(s);
+      if (lane == 0) {
+        if (bphi_out) bphi_out[u] = s;
+        if (logdet_out) logdet_out[u] = red;
+      }
+    }
+    if (mpk == nullptr) continue;
+    // Y = R^-1 in place, row block by row block
+    for (int I = 0; I < nblk; I++) {
+      const int i0 = I * NB, iw = min(NB, D - i0);
+      // Y_II = R_II^-1 into sinv (lower), via the whole block
+      for (int idx = tid; idx < NB * NB; idx += PT) {
+        int r = idx / NB, c = idx % NB;
+        sdiag[idx] = (r < iw && c <= r) ? L[packed_index(i0 + r, i0 + c)] : (r == c ? 1.0 : 0.0);
+      }
+      __syncthreads();
+      for (int j = tid; j < NB; j += PT) {  // column j of the inverse (forward substitution)
+        for (int r = 0; r < j; r++) sinv[r * NB + j] = 0.0;
+        sinv[j * NB + j] = 1.0 / sdiag[j * NB + j];
+        for (int r = j + 1; r < NB; r++) {
+          double s = 0.0;
+          for (int k = j; k < r; k++) s += sdiag[r * NB + k] * sinv[k * NB + j];
+          sinv[r * NB + j] = -s / sdiag[r * NB + r];
+        }
+      }
+      // T_IJ = sum_{K=J}^{I-1} R_IK Y_KJ for J < I (one warp per J), into tmp[:, J*NB..]
+      for (int J = warp; J < I; J += PT / 32) {
+        double acc[4][4][2];
+        zero_acc(acc);
+        for (int K = J; K < I; K++)
+          tile_mma(acc, packed_op(L, D, i0, K * NB, false), packed_op(L, D, K * NB, J * NB, false), NB, lane);
+        acc_foreach(acc, lane, [&](int r, int c, double v) { tmp[r * ldt + J * NB + c] = v; });
+      }
+      __syncthreads();
+      // Y_IJ = -Y_II T_IJ (overwrites R_IJ), then Y_II
+      for (int J = warp; J < I; J += PT / 32) {
+        double acc[4][4][2];
+        zero_acc(acc);
+        tile_mma(acc, dense_op(sinv, NB, NB, NB, 0, 0, false), dense_op(tmp, ldt, NB, ldt, 0, J * NB, false), NB,
+                 lane);
+        acc_foreach(acc, lane, [&](int r, int c, double v) {
+          if (r < iw) L[packed_index(i0 + r, J * NB + c)] = -v;
+        });
+      }
+      for (int idx = tid; idx < iw * iw; idx += PT) {
+        int r = idx / iw, c = idx % iw;
+        if (c <= r) L[packed_index(i0 + r, i0 + c)] = sinv[r * NB + c];
+      }
+      __syncthreads();
+    }
+    // M = Y^T Y + phi phi^T, lower tiles I >= J:  Phi_IJ = sum_{K>=I} Y_KI^T Y_KJ
+    double* M = mpk + (int64_t)u * P;
+    const int ntiles = nblk * (nblk + 1) / 2;
+    for (int tix = warp; tix < ntiles; tix += PT / 32) {
+      int I = 0, base = 0;
+      while (base + I + 1 <= tix) {
+        base += I + 1;
+        I++;
+      }
+      int J = tix - base;
+      double acc[4][4][2];
+      zero_acc(acc);
+      for (int K = I; K < nblk; K++)
+        tile_mma(acc, packed_op(L, D, K * NB, I * NB, true), packed_op(L, D, K * NB, J * NB, false),
+                 min(NB, D - K * NB), lane);
+      acc_foreach(acc, lane, [&](int r, int c, double v) {
+        int gi = I * NB + r, gj = J * NB + c;
+        if (gi < D && gj <= gi) M[packed_index(gi, gj)] = (flags & TVK_POST_MOMENT) ? v + vb[gi] * vb[gj] : v;
+      });
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ row solve (update_T)
+
+__global__ void __launch_bounds__(PT, 1) spd_solve_rows_kernel(const double* apk, const double* bmat, int batch, int D,
+                                                               int R, const int32_t* skip, double* x,
+                                                               int32_t* status, double* scratch) {
+  extern __shared__ __align__(16) double sm[];
+  double* sdiag = sm;          // [NB*NB]
+  double* vec = sdiag + NB * NB;  // [8][D] one solve vector per warp
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t P = packed_size(D);
+  double* W = scratch + (int64_t)blockIdx.x * P;
+  for (int c = blockIdx.x; c < batch; c += gridDim.x) {
+    if (skip && skip[c]) {
+      if (tid == 0 && status) status[c] = TVK_ITEM_SKIPPED;
+      continue;
+    }
+    const double* A = apk + (int64_t)c * P;
+    for (int64_t i = tid; i < P; i += PT) W[i] = A[i];
+    __syncthreads();
+    if (!packed_cholesky(W, D, sdiag, &bad)) {
+      if (tid == 0 && status) status[c] = TVK_ITEM_NOT_SPD;
+      continue;
+    }
+    if (tid == 0 && status) status[c] = TVK_ITEM_OK;
+    double* v = vec + warp * D;
+    for (int r = warp; r < R; r += PT / 32) {
+      const double* brow = bmat + ((int64_t)c * R + r) * D;
+      for (int i = lane; i < D; i += 32) v[i] = brow[i];
+      __syncwarp();
+      packed_cho_solve_warp(W, D, v, lane);
+      double* xrow = x + ((int64_t)c * R + r) * D;
+      for (int i = lane; i < D; i += 32) xrow[i] = v[i];
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+static int resident_ctas(const void* kern, size_t smem, int items) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, PT, smem);
+  if (per < 1) per = 1;
+  int g = sms * per;
+  return items < g ? items : g;
+}
+
+static size_t posterior_smem(int D) {
+  int ldt = ((D + 11) / 16) * 16 + 4;
+  return sizeof(double) * ((size_t)NB * ldt + 2 * NB * NB + D);
+}
+
+}  // namespace tvk
+
+using namespace tvk;
+
+extern "C" int64_t tvk_posterior_workspace_bytes(int D, int batch) {
+  // only tvk_spd_solve_rows needs scratch: one packed matrix per resident CTA
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t n = batch < sms ? batch : sms;
+  return n * packed_size(D) * (int64_t)sizeof(double);
+}
+
+extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, int flags, double* phi,
+                             double* mpk, double* logdet, double* bphi, int32_t* status, void* workspace,
+                             int64_t workspace_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TVK_REQUIRE(D >= 0 && D <= kPosteriorMaxD && U >= 0, "posterior: D must be in [0, 768]");
+  TVK_REQUIRE(phi != nullptr || D == 0, "posterior: phi output required");
+  TVK_REQUIRE(mpk == nullptr || mpk != lpk, "posterior: Mpk must not alias Lpk (the factor is used in place)");
+  if (U == 0) return TVK_OK;
+  if (D == 0) {  // no latent space: prior == posterior, log|I_0| = 0
+    if (logdet) cudaMemsetAsync(logdet, 0, sizeof(double) * U, st);
+    if (bphi) cudaMemsetAsync(bphi, 0, sizeof(double) * U, st);
+    if (status) cudaMemsetAsync(status, 0, sizeof(int32_t) * U, st);
+    TVK_CHECK_LAUNCH("posterior D=0");
+    return TVK_OK;
+  }
+  size_t smem = posterior_smem(D);
+  cudaFuncSetAttribute(posterior_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int grid = resident_ctas((const void*)posterior_kernel, smem, U);
+  posterior_kernel<<<grid, PT, smem, st>>>(const_cast<double*>(lpk), b, U, D, flags, phi, mpk, logdet, bphi,
+                                           status);
+  TVK_CHECK_LAUNCH("posterior");
+  return TVK_OK;
+}
+
+extern "C" int tvk_spd_solve_rows(const double* apk, const double* b, int batch, int D, int R, const int32_t* skip,
+                                  double* x, int32_t* status, void* workspace, int64_t workspace_bytes,
+                                  void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TVK_REQUIRE(D >= 0 && D <= kPosteriorMaxD && R >= 0 && batch >= 0, "spd_solve_rows: bad shape");
+  if (batch == 0) return TVK_OK;
+  if (D == 0) {
+    if (status) cudaMemsetAsync(status, 0, sizeof(int32_t) * batch, st);
+    TVK_CHECK_LAUNCH("spd_solve_rows D=0");
+    return TVK_OK;
+  }
+  size_t smem = sizeof(double) * ((size_t)NB * NB + 8 * (size_t)D);
+  cudaFuncSetAttribute(spd_solve_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int grid = resident_ctas((const void*)spd_solve_rows_kernel, smem, batch);
+  int64_t cap = workspace ? workspace_bytes / (packed_size(D) * (int64_t)sizeof(double)) : 0;
+  TVK_REQUIRE(cap >= 1, "spd_solve_rows: workspace too small");
+  if (grid > cap) grid = (int)cap;
+  spd_solve_rows_kernel<<<grid, PT, smem, st>>>(apk, b, batch, D, R, skip, x, status, (double*)workspace);
+  TVK_CHECK_LAUNCH("spd_solve_rows");
+  return TVK_OK;
+}

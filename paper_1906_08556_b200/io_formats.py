@@ -1,0 +1,220 @@
+"""Binary containers used by the drivers: FMX1 matrices, TVM1 models, ALN1 alignments.
+
+Byte-compatible with the reference ``io_formats.py`` (layouts at io_formats.py:1-15,
+59-98, 104-233, 240-295) so checkpoints and alignment caches interoperate with it.
+The ALN1 encoder is vectorized (one numpy scatter per utterance instead of a per-frame
+``struct.pack`` loop); the decoder walks the frame records with
+numpy cumulative sums over the u32 stream.
+"""
+
+from __future__ import annotations
+
+import os
+import struct
+
+import numpy as np
+
+MATRIX_MAGIC = b"FMX1"
+ALIGNMENT_MAGIC = b"ALN1"
+MODEL_MAGIC = b"TVM1"
+_CODES = {"f32": 0, "f64": 1}
+_DTYPES = {0: np.dtype("<f4"), 1: np.dtype("<f8")}
+
+
+class FormatError(ValueError):
+    """A file does not conform to its declared container layout."""
+
+
+def _need(fh, n, what):
+    b = fh.read(n)
+    if len(b) != n:
+        raise FormatError(f"truncated file while reading {what}")
+    return b
+
+
+def _fits(fh, n, what):
+    left = os.fstat(fh.fileno()).st_size - fh.tell()
+    if n > left:
+        raise FormatError(f"declared {what} size {n} exceeds remaining {left} bytes")
+
+
+def write_matrix(matrix, dtype, path):
+    """2-D array -> FMX1 file with dtype "f32" or "f64"."""
+    m = np.asarray(matrix)
+    if m.ndim != 2:
+        raise ValueError("matrix files hold 2-D arrays")
+    if m.shape[0] < 1 or m.shape[1] < 1:
+        raise ValueError("matrix must have at least one row and column")
+    if dtype not in _CODES:
+        raise ValueError(f"unknown dtype {dtype!r}, expected 'f32' or 'f64'")
+    code = _CODES[dtype]
+    with open(path, "wb") as fh:
+        fh.write(MATRIX_MAGIC + struct.pack("<BQQ", code, m.shape[0], m.shape[1]))
+        fh.write(np.ascontiguousarray(m, dtype=_DTYPES[code]).tobytes())
+
+
+def read_matrix(path):
+    with open(path, "rb") as fh:
+        if _need(fh, 4, "magic") != MATRIX_MAGIC:
+            raise FormatError("bad magic, expected b'FMX1'")
+        code, rows, cols = struct.unpack("<BQQ", _need(fh, 17, "header"))
+        if code not in _DTYPES:
+            raise FormatError(f"unknown dtype code {code}")
+        dt = _DTYPES[code]
+        _fits(fh, rows * cols * dt.itemsize, "matrix payload")
+        raw = _need(fh, rows * cols * dt.itemsize, "payload")
+        if fh.read(1):
+            raise FormatError("trailing bytes after matrix payload")
+    return np.frombuffer(raw, dtype=dt).reshape(rows, cols).copy()
+
+
+# ------------------------------------------------------------------------ models
+
+
+def save_model(model, path):
+    """TVM1: tag, C, F, D, prior offset, then weights, means, T, Sigma[, bias] as <f8."""
+    model.validate()
+    c, f, d = model.T.shape
+    tag = 0 if model.formulation == "standard" else 1
+    with open(path, "wb") as fh:
+        fh.write(MODEL_MAGIC + struct.pack("<BQQQd", tag, c, f, d, model.prior_offset))
+        parts = [model.ubm_weights, model.ubm_means, model.T, model.Sigma]
+        if tag == 0:
+            parts.append(model.bias)
+        for p in parts:
+            fh.write(np.ascontiguousarray(p, dtype="<f8").tobytes())
+
+
+def load_model(path):
+    from .tvm import TvModel
+
+    with open(path, "rb") as fh:
+        if _need(fh, 4, "magic") != MODEL_MAGIC:
+            raise FormatError("bad magic, expected b'TVM1'")
+        tag, c, f, d, p = struct.unpack("<BQQQd", _need(fh, 33, "header"))
+        if tag not in (0, 1):
+            raise FormatError(f"unknown formulation tag {tag}")
+
+        def take(shape, what):
+            k = int(np.prod(shape))
+            _fits(fh, 8 * k, what)
+            return np.frombuffer(_need(fh, 8 * k, what), dtype="<f8").reshape(shape).copy()
+
+        w = take((c,), "weights")
+        mu = take((c, f), "means")
+        T = take((c, f, d), "T")
+        S = take((c, f, f), "Sigma")
+        bias = take((c, f), "bias") if tag == 0 else None
+        if fh.read(1):
+            raise FormatError("trailing bytes after model tensors")
+    model = TvModel("standard" if tag == 0 else "augmented", T, S, w, mu, bias=bias, prior_offset=p)
+    model.validate()
+    return model
+
+
+# ------------------------------------------------------------------------ alignments
+
+
+def _encode_frames(ali):
+    """u32 stream [count_t, (comp, weight bits) * count_t] for every frame, vectorized."""
+    counts = np.diff(ali.offsets).astype(np.int64)
+    T = counts.shape[0]
+    E = int(ali.offsets[-1] - ali.offsets[0]) if T else 0
+    out = np.empty(T + 2 * E, dtype="<u4")
+    start = np.arange(T, dtype=np.int64) + 2 * (ali.offsets[:-1] - ali.offsets[0])
+    out[start] = counts
+    if E:
+        frame_of = np.repeat(np.arange(T, dtype=np.int64), counts)
+        pos = frame_of + 1 + 2 * np.arange(E, dtype=np.int64)
+        out[pos] = ali.components.astype("<u4")
+        out[pos + 1] = np.ascontiguousarray(ali.weights, dtype="<f4").view("<u4")
+    return out
+
+
+def write_alignment(path, alignments, top_k):
+    """Per-utterance sparse alignments -> one ALN1 corpus file (given order)."""
+    items = list(alignments.items()) if hasattr(alignments, "items") else list(alignments)
+    index = []
+    with open(path, "wb") as fh:
+        fh.write(ALIGNMENT_MAGIC + struct.pack("<IQQ", top_k, len(items), 0))
+        for utt, ali in items:
+            ali.validate(top_k=top_k)
+            index.append((utt, fh.tell()))
+            uid = utt.encode("utf-8")
+            fh.write(struct.pack("<I", len(uid)) + uid + struct.pack("<Q", ali.n_frames))
+            fh.write(_encode_frames(ali).tobytes())
+        index_offset = fh.tell()
+        for utt, off in index:
+            uid = utt.encode("utf-8")
+            fh.write(struct.pack("<I", len(uid)) + uid + struct.pack("<Q", off))
+        fh.seek(4 + 4 + 8)
+        fh.write(struct.pack("<Q", index_offset))
+
+
+def _decode_frames(words, n_frames):
+    """Inverse of _encode_frames; frame starts found by walking the count words."""
+    from .gmm import SparseAlignment
+
+    starts = np.empty(n_frames, dtype=np.int64)
+    counts = np.empty(n_frames, dtype=np.int64)
+    pos = 0
+    # chunked walk: each step advances by 1 + 2*count; vectorize over the known prefix
+    for t in range(n_frames):
+        if pos >= words.shape[0]:
+            raise FormatError("frame record shorter than declared (entry count)")
+        k = int(words[pos])
+        starts[t], counts[t] = pos, k
+        pos += 1 + 2 * k
+    if pos > words.shape[0]:
+        raise FormatError("frame record shorter than declared (frame entries)")
+    E = int(counts.sum())
+    offsets = np.zeros(n_frames + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    if E:
+        frame_of = np.repeat(np.arange(n_frames), counts)
+        within = np.arange(E) - offsets[:-1][frame_of]
+        idx = starts[frame_of] + 1 + 2 * within
+        comps = words[idx].astype(np.int32)
+        wts = words[idx + 1].view("<f4").astype(np.float32)
+    else:
+        comps, wts = np.zeros(0, np.int32), np.zeros(0, np.float32)
+    return SparseAlignment(offsets, comps, wts), pos
+
+
+def read_alignment(path):
+    """Whole ALN1 file -> {utterance id: SparseAlignment}."""
+    with open(path, "rb") as fh:
+        if _need(fh, 4, "magic") != ALIGNMENT_MAGIC:
+            raise FormatError("bad magic, expected b'ALN1'")
+        top_k, n_utts, index_offset = struct.unpack("<IQQ", _need(fh, 20, "header"))
+        size = os.fstat(fh.fileno()).st_size
+        if index_offset > size:
+            raise FormatError("index offset beyond end of file")
+        fh.seek(index_offset)
+        index = []
+        for _ in range(n_utts):
+            (n,) = struct.unpack("<I", _need(fh, 4, "index"))
+            _fits(fh, n, "index id")
+            uid = _need(fh, n, "index id").decode("utf-8")
+            (off,) = struct.unpack("<Q", _need(fh, 8, "index offset"))
+            index.append((uid, off))
+        out = {}
+        bounds = [off for _, off in index] + [index_offset]
+        order = np.argsort([off for _, off in index], kind="stable")
+        nxt = {}
+        sorted_offs = sorted(bounds)
+        for off in bounds[:-1]:
+            nxt[off] = sorted_offs[sorted_offs.index(off) + 1]
+        del order
+        for uid, off in index:
+            fh.seek(off)
+            (n,) = struct.unpack("<I", _need(fh, 4, "utterance id"))
+            stored = _need(fh, n, "utterance id").decode("utf-8")
+            if stored != uid:
+                raise FormatError("alignment index does not match record")
+            (n_frames,) = struct.unpack("<Q", _need(fh, 8, "frame count"))
+            body = nxt[off] - fh.tell()
+            words = np.frombuffer(_need(fh, body, "frame entries"), dtype="<u4")
+            ali, used = _decode_frames(words, n_frames)
+            out[uid] = ali
+    return out

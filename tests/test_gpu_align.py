@@ -1,0 +1,294 @@
+"""GPU parity of the frame-posterior and Baum-Welch path (libtvk) against the reference.
+
+Compares the CUDA path with (a) the golden fixtures produced by the reference
+package and (b) the oracle on the same seeded inputs; also ports the
+reference's own alignment/BW tests (pkg/tests/test_gmm.py:159-367).
+Tolerances (north star): pruning indices bit-exact except documented ties,
+posteriors within 1e-5 relative (weights are float32 on output).
+"""
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import tvkit_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+ALIGN = cases.load("align")
+TIE_REL = 1e-9  # documented tie: diag log-likelihood gap < 1e-9 * max(1, |ll|)
+
+
+def _pkg():
+    import paper_1906_08556_b200 as pkg
+    return pkg
+
+
+def _models(diag, full):
+    g = _pkg().gmm
+    return g.GmmDiag(*diag), g.GmmFull(*full)
+
+
+def _assert_alignment_matches(got, off, comp, w, tie_frames=()):
+    skip = set(int(t) for t in tie_frames)
+    cnt_ref = np.diff(off)
+    cnt_got = got.entry_counts()
+    for t in range(len(cnt_ref)):
+        if t in skip:
+            continue
+        a0, a1 = off[t], off[t + 1]
+        b0, b1 = got.offsets[t], got.offsets[t + 1]
+        assert cnt_ref[t] == cnt_got[t], f"frame {t}: entry count {cnt_got[t]} != {cnt_ref[t]}"
+        np.testing.assert_array_equal(got.components[b0:b1], comp[a0:a1], err_msg=f"frame {t}")
+        np.testing.assert_allclose(got.weights[b0:b1], w[a0:a1], rtol=1e-5, atol=1e-7, err_msg=f"frame {t}")
+
+
+@pytest.mark.parametrize("case", cases.ALIGN_CASES, ids=[c[0] for c in cases.ALIGN_CASES])
+def test_align_matches_reference_golden(gpu, case):
+    g = ALIGN[case[0]]
+    diag, full, x, k, prune, _ = cases.align_inputs(case)
+    dm, fm = _models(diag, full)
+    got = gpu.gmm.align_frames(dm, fm, x, top_k=k, prune=prune)
+    ties = np.flatnonzero(g["boundary_gap"] < TIE_REL * np.maximum(1.0, np.abs(g["sel_full_ll"][:, 0])))
+    assert ties.size <= max(1, x.shape[0] // 1000), f"too many documented ties: {ties.size}"
+    _assert_alignment_matches(got, g["offsets"], g["components"], g["weights"], ties)
+    got.validate(top_k=k, prune=prune)
+
+
+@pytest.mark.parametrize("case", cases.ALIGN_CASES, ids=[c[0] for c in cases.ALIGN_CASES])
+def test_selection_and_full_ll_match_reference(gpu, case):
+    g = ALIGN[case[0]]
+    diag, full, x, k, prune, _ = cases.align_inputs(case)
+    from paper_1906_08556_b200 import _device, _lib
+    dm, fm = _models(diag, full)
+    xd = _device.frames_to_device(x)
+    res = _device.align(xd, dm.device_table(), fm.device_table(), k, prune, debug=True)
+    sel = _lib.to_host(res.selected)
+    ties = g["boundary_gap"] < TIE_REL * np.maximum(1.0, np.abs(g["sel_full_ll"][:, 0]))
+    mism = np.flatnonzero(np.any(sel != g["selected"], axis=1) & ~ties)
+    assert mism.size == 0, f"selection differs on frames {mism[:10]}"
+    ok = ~ties
+    sll = _lib.to_host(res.sel_ll)
+    np.testing.assert_allclose(sll[ok], g["sel_full_ll"][ok], rtol=1e-10, atol=1e-9)
+
+
+@pytest.mark.parametrize("case", cases.ALIGN_CASES, ids=[c[0] for c in cases.ALIGN_CASES])
+def test_bw_stats_match_reference_golden(gpu, case):
+    g = ALIGN[case[0]]
+    diag, full, x, k, prune, center = cases.align_inputs(case)
+    ali = gpu.gmm.SparseAlignment(g["offsets"], g["components"], g["weights"])
+    c = diag[0].shape[0]
+    st = gpu.gmm.accumulate_bw_stats(x, ali, c)
+    np.testing.assert_allclose(st.n, g["n"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(st.f, g["f"], rtol=1e-12, atol=1e-10)
+    if g["S"].size:
+        np.testing.assert_allclose(st.S, g["S"], rtol=1e-12, atol=1e-10)
+    stc = gpu.gmm.accumulate_bw_stats(x, ali, c, center_with=center)
+    assert stc.centered
+    np.testing.assert_allclose(stc.f, g["fc"], rtol=1e-12, atol=1e-10)
+    if g["Sc"].size:
+        np.testing.assert_allclose(stc.S, g["Sc"], rtol=1e-12, atol=1e-10)
+
+
+def test_dense_loglik_match_oracle(gpu):
+    diag, full, x, k, prune, _ = cases.align_inputs(cases.ALIGN_CASES[3])
+    dm, fm = _models(diag, full)
+    np.testing.assert_allclose(dm.log_likelihoods(x), orc.diag_loglik(*diag, x), rtol=1e-12, atol=1e-10)
+    np.testing.assert_allclose(fm.log_likelihoods(x), orc.full_loglik(*full, x), rtol=1e-10, atol=1e-9)
+
+
+# ---------------------------------------------------------------- ported reference tests (test_gmm.py)
+
+
+def _random_model_pair(rng, c=8, f=3):
+    weights = rng.dirichlet(np.full(c, 5.0))
+    means = rng.normal(0, 3, (c, f))
+    variances = rng.uniform(0.5, 1.5, (c, f))
+    covs = np.zeros((c, f, f))
+    for i in range(c):
+        a = rng.normal(0, 0.3, (f, f))
+        covs[i] = np.diag(variances[i]) + a @ a.T
+    g = _pkg().gmm
+    return g.GmmDiag(weights, means, variances), g.GmmFull(weights, means, covs)
+
+
+class TestSelectTopK:
+    def test_frame_at_component_mean(self, gpu):
+        g = gpu.gmm
+        model = g.GmmDiag(np.array([1 / 3, 1 / 3, 1 / 3]), np.array([[0.0, 0.0], [5.0, 5.0], [-5.0, 5.0]]),
+                          np.ones((3, 2)))
+        assert g.select_top_k(model, model.means[0], 1).tolist() == [0]
+
+    def test_matches_dense_posterior_oracle(self, gpu):
+        rng = np.random.default_rng(21)
+        c, f = 16, 4
+        model = gpu.gmm.GmmDiag(rng.dirichlet(np.full(c, 2.0)), rng.normal(0, 2, (c, f)),
+                                rng.uniform(0.5, 2.0, (c, f)))
+        for _ in range(20):
+            frame = rng.normal(0, 2, f)
+            got = gpu.gmm.select_top_k(model, frame, 5)
+            log_post = model.log_posteriors(frame[None, :])[0]
+            want = np.argsort(-log_post, kind="stable")[:5]
+            np.testing.assert_array_equal(np.sort(got), np.sort(want))
+            np.testing.assert_array_equal(
+                got, orc.top_k_single(model.weights, model.means, model.variances, frame, 5))
+
+    def test_k_equals_c_returns_everything(self, gpu):
+        model = gpu.gmm.GmmDiag(np.full(4, 0.25), np.zeros((4, 2)), np.ones((4, 2)))
+        assert sorted(gpu.gmm.select_top_k(model, np.zeros(2), 4).tolist()) == [0, 1, 2, 3]
+
+    def test_tie_breaks_toward_lower_index(self, gpu):
+        model = gpu.gmm.GmmDiag(np.full(3, 1 / 3), np.zeros((3, 2)), np.ones((3, 2)))
+        assert gpu.gmm.select_top_k(model, np.ones(2), 2).tolist() == [0, 1]
+
+    def test_k_too_large_rejected(self, gpu):
+        model = gpu.gmm.GmmDiag(np.full(2, 0.5), np.zeros((2, 2)), np.ones((2, 2)))
+        with pytest.raises(ValueError):
+            gpu.gmm.select_top_k(model, np.zeros(2), 3)
+
+
+class TestAlignFrames:
+    def test_invariants_on_random_frames(self, gpu):
+        rng = np.random.default_rng(30)
+        diag, full = _random_model_pair(rng)
+        frames = rng.normal(0, 3, (1000, 3))
+        alignment = gpu.gmm.align_frames(diag, full, frames, top_k=5, prune=0.025)
+        alignment.validate(top_k=5, prune=0.025)
+        sums = np.add.reduceat(alignment.weights.astype(np.float64), alignment.offsets[:-1])
+        assert np.max(np.abs(sums - 1.0)) < 1e-5
+        assert alignment.weights.min() >= 0.025 - 1e-7
+        assert alignment.entry_counts().max() <= 5
+        off, comp, w = orc.align((diag.weights, diag.means, diag.variances),
+                                 (full.weights, full.means, full.covariances), frames, 5, 0.025)
+        _assert_alignment_matches(alignment, off, comp, w)
+
+    def test_symmetric_frame_splits_evenly(self, gpu):
+        g = gpu.gmm
+        weights = np.array([0.5, 0.5])
+        means = np.array([[-1.0, 0.0], [1.0, 0.0]])
+        diag = g.GmmDiag(weights, means, np.ones((2, 2)))
+        full = g.GmmFull(weights, means, np.stack([np.eye(2), np.eye(2)]))
+        alignment = g.align_frames(diag, full, np.zeros((1, 2)), top_k=2, prune=0.025)
+        comps, wts = alignment.frame(0)
+        np.testing.assert_array_equal(comps, [0, 1])
+        np.testing.assert_allclose(wts, [0.5, 0.5], atol=1e-6)
+
+    def test_posteriors_renormalized_over_selection_only(self, gpu):
+        from scipy.special import logsumexp
+        rng = np.random.default_rng(31)
+        diag, full = _random_model_pair(rng, c=6)
+        frames = rng.normal(0, 3, (50, 3))
+        k = 3
+        alignment = gpu.gmm.align_frames(diag, full, frames, top_k=k, prune=0.0)
+        full_ll = full.log_likelihoods(frames)
+        diag_ll = diag.log_likelihoods(frames)
+        for t in range(50):
+            sel = np.argsort(-diag_ll[t], kind="stable")[:k]
+            expect = np.exp(full_ll[t, sel] - logsumexp(full_ll[t, sel]))
+            comps, wts = alignment.frame(t)
+            order = np.argsort(sel, kind="stable")
+            np.testing.assert_array_equal(comps, np.sort(sel))
+            np.testing.assert_allclose(wts, expect[order], atol=1e-6)
+
+    def test_degenerate_frame_keeps_argmax(self, gpu):
+        rng = np.random.default_rng(32)
+        diag, full = _random_model_pair(rng, c=4)
+        frames = rng.normal(0, 3, (200, 3))
+        alignment = gpu.gmm.align_frames(diag, full, frames, top_k=4, prune=0.9999)
+        assert np.all(alignment.entry_counts() == 1)
+        np.testing.assert_allclose(alignment.weights, 1.0)
+
+    def test_model_mismatch_rejected(self, gpu):
+        rng = np.random.default_rng(33)
+        diag, _ = _random_model_pair(rng, c=4)
+        _, full = _random_model_pair(rng, c=5)
+        with pytest.raises(ValueError, match="share"):
+            gpu.gmm.align_frames(diag, full, np.zeros((1, 3)))
+
+    def test_empty_utterance(self, gpu):
+        rng = np.random.default_rng(34)
+        diag, full = _random_model_pair(rng)
+        assert gpu.gmm.align_frames(diag, full, np.zeros((0, 3))).n_frames == 0
+
+
+class TestBaumWelchStats:
+    def test_empty_utterance_zeros(self, gpu):
+        g = gpu.gmm
+        stats = g.accumulate_bw_stats(np.zeros((0, 2)), g.SparseAlignment.from_frames([]), 3)
+        assert stats.n.sum() == 0 and np.all(stats.f == 0) and np.all(stats.S == 0)
+        assert not stats.centered
+
+    def test_single_frame_centered_at_mean(self, gpu):
+        g = gpu.gmm
+        x = np.array([[1.5, -2.0]])
+        ali = g.SparseAlignment.from_frames([(np.array([0]), np.array([1.0], dtype=np.float32))])
+        means = np.array([[1.5, -2.0], [0.0, 0.0]])
+        stats = g.accumulate_bw_stats(x, ali, 2, center_with=means)
+        assert stats.centered
+        np.testing.assert_allclose(stats.n, [1.0, 0.0])
+        np.testing.assert_allclose(stats.f, 0.0, atol=1e-12)
+        np.testing.assert_allclose(stats.S, 0.0, atol=1e-12)
+
+    def test_matches_dense_brute_force(self, gpu):
+        rng = np.random.default_rng(40)
+        c, f, t = 6, 3, 5
+        x = rng.normal(0, 2, (t, f))
+        diag, full = _random_model_pair(rng, c=c, f=f)
+        alignment = gpu.gmm.align_frames(diag, full, x, top_k=4, prune=0.0)
+        stats = gpu.gmm.accumulate_bw_stats(x, alignment, c)
+        gamma = np.zeros((t, c))
+        for i in range(t):
+            comps, wts = alignment.frame(i)
+            gamma[i, comps] = wts.astype(np.float64)
+        np.testing.assert_allclose(stats.n, gamma.sum(axis=0), atol=1e-9)
+        np.testing.assert_allclose(stats.f, gamma.T @ x, atol=1e-9)
+        for ci in range(c):
+            np.testing.assert_allclose(stats.S[ci], (x * gamma[:, ci, None]).T @ x, atol=1e-9)
+
+    def test_occupancy_sums_to_frame_count(self, gpu):
+        rng = np.random.default_rng(41)
+        diag, full = _random_model_pair(rng)
+        x = rng.normal(0, 3, (321, 3))
+        alignment = gpu.gmm.align_frames(diag, full, x, top_k=5, prune=0.025)
+        stats = gpu.gmm.accumulate_bw_stats(x, alignment, 8)
+        assert abs(stats.n.sum() - 321) < 1e-6
+        stats.validate(frame_count=321)
+
+    def test_out_of_range_component_rejected(self, gpu):
+        g = gpu.gmm
+        ali = g.SparseAlignment.from_frames([(np.array([5]), np.array([1.0], dtype=np.float32))])
+        with pytest.raises(ValueError, match="out of range"):
+            g.accumulate_bw_stats(np.zeros((1, 2)), ali, 3)
+
+    def test_frame_count_mismatch_rejected(self, gpu):
+        g = gpu.gmm
+        ali = g.SparseAlignment.from_frames([(np.array([0]), np.array([1.0], dtype=np.float32))])
+        with pytest.raises(ValueError, match="frame count"):
+            g.accumulate_bw_stats(np.zeros((2, 2)), ali, 3)
+
+
+def test_dgemm_matches_torch_fp64(gpu):
+    import torch
+    from paper_1906_08556_b200 import _lib
+    rng = np.random.default_rng(0)
+    for (m, n, k, ta, tb) in [(1, 1, 1, 0, 0), (5, 7, 3, 0, 0), (130, 70, 33, 1, 0), (200, 300, 129, 0, 1),
+                              (257, 129, 64, 1, 1), (1024, 1024, 96, 0, 0)]:
+        a = rng.normal(size=(k, m) if ta else (m, k))
+        b = rng.normal(size=(n, k) if tb else (k, n))
+        want = (a.T if ta else a) @ (b.T if tb else b)
+        c = _lib.empty((m, n))
+        _lib.dgemm(_lib.to_dev(a), _lib.to_dev(b), c, m, n, k, trans_a=bool(ta), trans_b=bool(tb))
+        np.testing.assert_allclose(_lib.to_host(c), want, rtol=1e-12, atol=1e-12 * k)
+    # packed-lower output and split-K
+    m, k = 200, 1000
+    a = rng.normal(size=(m, k))
+    want = a @ a.T
+    c = _lib.zeros((m * (m + 1) // 2,))
+    _lib.dgemm(_lib.to_dev(a), _lib.to_dev(a), c, m, m, k, trans_b=True, out_mode=_lib.TVK_OUT_PACKED_LOWER)
+    il = np.tril_indices(m)
+    np.testing.assert_allclose(_lib.to_host(c), want[il], rtol=1e-12, atol=1e-10)
+    work = _lib.empty((8 * m * m,))
+    c2 = _lib.empty((m, m))
+    _lib.dgemm(_lib.to_dev(a), _lib.to_dev(a), c2, m, m, k, trans_b=True, splits=8, work=work)
+    np.testing.assert_allclose(_lib.to_host(c2), want, rtol=1e-12, atol=1e-10)
+    del torch

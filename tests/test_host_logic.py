@@ -1,0 +1,149 @@
+"""CPU tests of the host side: C-ABI exports, config files, sharding, the multi-process merge,
+and the ALN1/TVM1/FMX1 containers (byte compatibility with the reference layouts)."""
+
+import ctypes
+import os
+import re
+import struct
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1906_08556_b200 import _lib
+    header = open(os.path.join(REPO, "include", "tvk.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|int64_t)\s+(tvk_\w+)\s*\(", header, re.M))
+    assert declared, "no declarations parsed"
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in sorted(declared) if not hasattr(lib, s)]
+    assert not missing, f"libtvk.so lacks {missing}"
+    assert declared == set(_lib.SIGNATURES), "ctypes table and header disagree"
+    assert _lib.load().tvk_version() >= 100
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_1906_08556_b200 import _lib
+    with pytest.raises(_lib.TvkError, match="CUDA device"):
+        _lib.device()
+
+
+def test_train_config_round_trip_and_validation(tmp_path):
+    from paper_1906_08556_b200.pipeline import TrainConfig
+    cfg = TrainConfig(seeds=(3, 1, 4), workers=2, prune=0.05, latent_dim=4)
+    path = tmp_path / "train.cfg"
+    cfg.save(path)
+    back = TrainConfig.load(path)
+    assert back == cfg and back.config_hash() == cfg.config_hash()
+    with pytest.raises(ValueError, match="unknown config key"):
+        TrainConfig.from_text("latent_dim = 4\nturbo = on\n")
+    c2 = TrainConfig.from_text("# c\nlatent_dim = 6\n\niterations = 2  # inline\n")
+    assert c2.latent_dim == 6 and c2.iterations == 2
+    for bad in (dict(iterations=0), dict(seeds=()), dict(realign_interval=-1),
+                dict(formulation="augmented", update_mean=True)):
+        with pytest.raises(ValueError):
+            TrainConfig(**bad).validate()
+    with pytest.warns(RuntimeWarning, match="poorly"):
+        TrainConfig(formulation="standard", update_mean=True, sigma_update=True).validate()
+    d = TrainConfig()
+    assert (d.latent_dim, d.iterations, d.top_k, d.prune, d.prior_offset, len(d.seeds)) == (400, 22, 20, 0.025,
+                                                                                             100.0, 5)
+    assert TrainConfig().config_hash() != TrainConfig(iterations=4).config_hash()
+
+
+def test_shard_ranges_partition_the_corpus():
+    from paper_1906_08556_b200._dist import shard, shard_range
+    for n in (0, 1, 7, 20000):
+        for ws in (1, 2, 3, 8):
+            spans = [shard_range(n, r, ws) for r in range(ws)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+    ids = [f"u{i}" for i in range(10)]
+    assert sum((shard(ids, r, 3) for r in range(3)), []) == ids
+
+
+def _merge_worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1906_08556_b200 import _dist
+    rng = np.random.default_rng(rank)
+    flat = torch.from_numpy(rng.normal(size=1000))
+    local = flat.clone()
+    _dist.allreduce_sum_(flat)
+    results[rank] = (local.numpy(), flat.numpy(), _dist.world())
+    gathered = _dist.gather_rows(torch.full((rank + 1, 2), float(rank), dtype=torch.float64), [1, 2])
+    results[rank] = results[rank] + (gathered.numpy(),)
+    dist.destroy_process_group()
+
+
+def test_gloo_two_rank_accumulator_merge_is_a_sum():
+    """The multi-GPU merge (one all-reduce of the flat accumulator) equals EmAccumulators.merge."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_merge_worker, args=(2, port, results), nprocs=2, join=True)
+    total = results[0][0] + results[1][0]
+    for r in range(2):
+        np.testing.assert_allclose(results[r][1], total, rtol=1e-15)
+        assert results[r][2] == (r, 2)
+        np.testing.assert_array_equal(results[r][3], [[0, 0], [1, 1], [1, 1]])
+
+
+def test_aln1_layout_and_round_trip(tmp_path):
+    from paper_1906_08556_b200.gmm import SparseAlignment
+    from paper_1906_08556_b200.io_formats import read_alignment, write_alignment
+    rng = np.random.default_rng(0)
+    alis = {}
+    for u in ("a", "bb", "c"):
+        frames = []
+        for _ in range(int(rng.integers(0, 6))):
+            k = int(rng.integers(1, 4))
+            w = rng.dirichlet(np.ones(k)).astype(np.float32)
+            frames.append((np.sort(rng.choice(20, k, replace=False)), w))
+        alis[u] = SparseAlignment.from_frames(frames)
+    path = str(tmp_path / "x.aln")
+    write_alignment(path, alis, top_k=4)
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"ALN1"
+    top_k, n, idx = struct.unpack("<IQQ", raw[4:24])
+    assert (top_k, n) == (4, 3) and idx < len(raw)
+    # first record written by hand from the layout at io_formats.py:104-148
+    a = alis["a"]
+    rec = struct.pack("<I", 1) + b"a" + struct.pack("<Q", a.n_frames)
+    for t in range(a.n_frames):
+        c, w = a.frame(t)
+        rec += struct.pack("<I", len(c))
+        for ci, wi in zip(c, w):
+            rec += struct.pack("<I", int(ci)) + struct.pack("<f", float(wi))
+    assert raw[24:24 + len(rec)] == rec
+    back = read_alignment(path)
+    for u, ali in alis.items():
+        np.testing.assert_array_equal(back[u].offsets, ali.offsets)
+        np.testing.assert_array_equal(back[u].components, ali.components)
+        assert back[u].weights.tobytes() == ali.weights.tobytes()
+
+
+def test_fmx1_round_trip(tmp_path):
+    from paper_1906_08556_b200.io_formats import FormatError, read_matrix, write_matrix
+    m = np.arange(12.0).reshape(3, 4)
+    p = str(tmp_path / "m.fmx")
+    write_matrix(m, "f32", p)
+    raw = open(p, "rb").read()
+    assert raw[:4] == b"FMX1" and struct.unpack("<BQQ", raw[4:21]) == (0, 3, 4)
+    np.testing.assert_array_equal(read_matrix(p), m.astype(np.float32))
+    open(p, "ab").write(b"x")
+    with pytest.raises(FormatError):
+        read_matrix(p)
