@@ -1,0 +1,421 @@
+"""Benchmark of the GPU i-vector hot path (BASELINE.json metric).
+
+Headline (``value``): UBM frame posteriors (BASELINE config 2): 2048-component full-covariance
+UBM, 60-dim frames, 1e7 synthetic frames per GPU per step, top-20 preselection + prune 0.025,
+frames resident in HBM (2.4 GB per GPU, larger than L2).  ``e2e``: the same through the public
+``align_frames`` API from pinned host frames to a host SparseAlignment.  A second object
+(``em_iteration``) reports seconds per EM iteration of the Kaldi augmented-bias extractor at
+2048 x 60, R=400 (BASELINE config 3 shape) on ``--em-utts`` synthetic utterances per GPU.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--no-em]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU)
+
+``--impl reference`` times the reference algorithm on the host cores (the CPU oracle restating
+tvkit.gmm.align_frames, since the reference tree does not exist on the GPU box) on a bounded
+frame sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = json.load(open(os.path.join(REPO, "BASELINE.json")))["metric"]
+C, F, K_TOP, PRUNE = 2048, 60, 20, 0.025
+FRAMES_PER_GPU = 10_000_000
+Q = 1 + F + F * (F + 1) // 2
+FLOP_FULL_PER_FRAME = 2 * C * Q            # dominant kernel (quadratic-feature GEMM)
+FLOP_PER_FRAME = 2 * C * (2 * F + 1) + FLOP_FULL_PER_FRAME   # 8,241,152
+FP64_PEAK_FILE = os.path.join(REPO, "profiles", "r01_fp64_pipe_peak.txt")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def fp64_peak():
+    """Measured FP64 tensor-pipe (DMMA.8x8x4) issue ceiling on this pool's B200 (tools/fp64_peak.cu)."""
+    try:
+        vals = [float(l.split()[-2]) for l in open(FP64_PEAK_FILE) if l.startswith("DMMA")]
+        return max(vals), "measured DMMA.8x8x4 issue ceiling (profiles/r01_fp64_pipe_peak.txt)"
+    except Exception:
+        return 37.2, "nominal 148 SM x 64 FP64 FMA/clk x 1.965 GHz"
+
+
+def make_ubm(seed=0):
+    """SURVEY §8(d) config 2 recipe: w ~ Dir(10), mu ~ N(0, 0.3^2), Sigma = A A'/2F + 0.5 I."""
+    rng = np.random.default_rng(seed)
+    w = rng.dirichlet(np.full(C, 10.0))
+    mu = rng.normal(0.0, 0.3, (C, F))
+    a = rng.normal(0.0, 1.0, (C, F, 2 * F))
+    cov = np.einsum("cik,cjk->cij", a, a) / (2 * F) + 0.5 * np.eye(F)
+    return w, mu, cov
+
+
+def sample_frames(w, mu, cov, n, seed, device):
+    """n frames from the full GMM, generated on the device (not timed), returned as f32."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    wt = torch.from_numpy(w).to(device)
+    counts = torch.bincount(torch.multinomial(wt, n, replacement=True, generator=g), minlength=C).cpu().numpy()
+    chol = torch.linalg.cholesky(torch.from_numpy(cov).to(device))
+    mut = torch.from_numpy(mu).to(device)
+    out = torch.empty((n, F), dtype=torch.float32, device=device)
+    pos = 0
+    for c0 in range(0, C, 256):
+        c1 = min(C, c0 + 256)
+        mx = int(counts[c0:c1].max())
+        z = torch.randn((c1 - c0, mx, F), dtype=torch.float64, device=device, generator=g)
+        x = torch.bmm(z, chol[c0:c1].transpose(1, 2)) + mut[c0:c1, None, :]
+        for i, c in enumerate(range(c0, c1)):
+            k = int(counts[c])
+            out[pos:pos + k] = x[i, :k].to(torch.float32)
+            pos += k
+    perm = torch.randperm(n, device=device, generator=g)
+    return out[perm].contiguous()
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (the recipe's clocks line)."""
+
+    def __init__(self, index):
+        self.proc = None
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        load = [r[0] for r in rows]
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": rows[0][1], "reasons": reasons,
+                "samples": len(rows)}
+
+
+def bench_reference(args):
+    """CPU reference arm: the reference align_frames algorithm (oracle port) on host cores."""
+    from oracle import tvkit_oracle as orc
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    w, mu, cov = make_ubm(0)
+    rng = np.random.default_rng(1)
+    comp = rng.choice(C, p=w, size=args.ref_frames)
+    L = np.linalg.cholesky(cov)
+    x = (mu[comp] + np.einsum("tij,tj->ti", L[comp], rng.standard_normal((args.ref_frames, F)))).astype(np.float32)
+    diag = (w, mu, np.ascontiguousarray(np.diagonal(cov, axis1=1, axis2=2)))
+    full = (w, mu, cov)
+    for _ in range(args.warmup):
+        orc.align(diag, full, x, K_TOP, PRUNE)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        orc.align(diag, full, x, K_TOP, PRUNE)
+    dt = (time.perf_counter() - t0) / args.steps
+    fps = args.ref_frames / dt
+    cores = len(os.sched_getaffinity(0))
+    sample = f"{args.ref_frames} frames of the config-2 workload per step (one align_frames chunk)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2 frame posteriors: 2048-comp full-cov UBM, 60-dim, top-20, prune 0.025",
+                   "frames_per_step": args.ref_frames},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "x_realtime": fps / 100.0,
+    }), flush=True)
+
+
+def cpu_baseline_sample(n_frames=4000):
+    """Oracle timing on rank 0 (reported baseline, not the target)."""
+    from oracle import tvkit_oracle as orc
+    w, mu, cov = make_ubm(0)
+    rng = np.random.default_rng(2)
+    comp = rng.choice(C, p=w, size=n_frames)
+    L = np.linalg.cholesky(cov)
+    x = (mu[comp] + np.einsum("tij,tj->ti", L[comp], rng.standard_normal((n_frames, F)))).astype(np.float32)
+    diag = (w, mu, np.ascontiguousarray(np.diagonal(cov, axis1=1, axis2=2)))
+    t0 = time.perf_counter()
+    orc.align(diag, (w, mu, cov), x, K_TOP, PRUNE)
+    dt = time.perf_counter() - t0
+    return {"value": n_frames / dt, "unit": "frames/s", "cores": len(os.sched_getaffinity(0)), "kind": "port",
+            "sample": f"{n_frames} frames (one chunk) of the config-2 workload, oracle restatement of "
+                      f"tvkit.gmm.align_frames, numpy/OpenBLAS on all host cores"}
+
+
+def bench_ours(args):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    import paper_1906_08556_b200 as pkg
+    from paper_1906_08556_b200 import _device, _lib
+
+    w, mu, cov = make_ubm(0)
+    diag_m = pkg.GmmDiag(w, mu, np.ascontiguousarray(np.diagonal(cov, axis1=1, axis2=2)))
+    full_m = pkg.GmmFull(w, mu, cov)
+    n = args.frames
+    x = sample_frames(w, mu, cov, n, 1000 + rank, dev)
+    dtab, ftab = diag_m.device_table(), full_m.device_table()
+    k = K_TOP
+    offsets = _lib.empty((n + 1,), torch.int64)
+    comps = _lib.empty((n * k,), torch.int32)
+    wts = _lib.empty((n * k,), torch.float32)
+    ws_bytes = int(_lib.load().tvk_align_workspace_bytes(n, k))
+    ws = _lib.empty((ws_bytes,), torch.uint8)
+
+    def step():
+        _lib.call("tvk_align_frames", _lib.ptr(x), 0, n, F, _lib.ptr(dtab.table), _lib.ptr(ftab.table), C, k,
+                  PRUNE, _lib.ptr(ws), ws_bytes, _lib.ptr(offsets), _lib.ptr(comps), _lib.ptr(wts), None, None,
+                  _lib.stream())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = Clocks(local)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    entries = int(offsets[n].item())
+    value = world * n / (ms / 1e3)
+
+    # dominant kernel alone (stage 2: quadratic-feature GEMM + selection gather), CUDA events
+    sel = _lib.empty((n, k), torch.int32)
+    _lib.call("tvk_select_topk", _lib.ptr(x), 0, n, F, _lib.ptr(dtab.table), C, k, _lib.ptr(sel), None,
+              _lib.stream())
+    sll = _lib.empty((n, k))
+    reps = 3
+    for _ in range(1):
+        _lib.call("tvk_full_loglik_selected", _lib.ptr(x), 0, n, F, _lib.ptr(ftab.table), C, k, _lib.ptr(sel),
+                  _lib.ptr(sll), _lib.stream())
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(reps):
+        _lib.call("tvk_full_loglik_selected", _lib.ptr(x), 0, n, F, _lib.ptr(ftab.table), C, k, _lib.ptr(sel),
+                  _lib.ptr(sll), _lib.stream())
+    e3.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = e2.elapsed_time(e3) / reps
+    peak, peak_src = fp64_peak()
+    achieved = FLOP_FULL_PER_FRAME * n / (kern_ms / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(REPO, "profiles", "r01_ncu_full_ll.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch_per_frame")
+            traffic = traffic * n if traffic is not None else None
+        except Exception:
+            traffic = None
+    del sel, sll
+
+    # e2e through the public API: pinned host frames -> align_frames -> host SparseAlignment
+    host = torch.empty((n, F), dtype=torch.float32, pin_memory=True)
+    host.copy_(x)
+    del x, ws, comps, wts
+    torch.cuda.empty_cache()
+    e2e_steps = max(1, min(args.steps, 3))
+    pkg.align_frames(diag_m, full_m, host, top_k=k, prune=PRUNE)
+    barrier()
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(e2e_steps):
+        ali = pkg.align_frames(diag_m, full_m, host, top_k=k, prune=PRUNE)
+        d2h = ali.offsets.nbytes + ali.components.nbytes + ali.weights.nbytes
+    barrier()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    e2e_value = world * n / e2e_s
+    del host, ali
+
+    em = None
+    if args.em_utts > 0:
+        em = bench_em(args, pkg, dev, rank, world, barrier, max_over_ranks)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2 frame posteriors: 2048-comp full-cov UBM, 60-dim MFCC-shaped "
+                                   "frames, top-20 diag preselection, prune 0.025",
+                       "frames_per_gpu_per_step": n, "global_frames_per_step": world * n,
+                       "parallelism": f"dp{world} (frames sharded, no collective)",
+                       "l2": "inputs (2.4 GB/GPU) larger than L2"},
+            "x_realtime": value / 100.0,
+            "entries_per_frame": entries / n,
+            "gpu_launches": 7 * args.steps,
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": n * F * 4,
+                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                    "path": "paper_1906_08556_b200.align_frames(pinned host f32 frames) -> SparseAlignment"},
+            "roofline": {"bound": "tensor", "kernel": "full_ll_kernel (quadratic-feature DMMA GEMM)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "peak_source": peak_src, "flop_per_frame": FLOP_FULL_PER_FRAME, "launch_ms": kern_ms,
+                         "share_of_step": kern_ms / ms, "traffic": traffic},
+            "clocks": clk,
+        }
+        if em is not None:
+            line["em_iteration"] = em
+        if not args.no_cpu:
+            try:
+                line["cpu_baseline"] = cpu_baseline_sample(args.cpu_frames)
+            except Exception as exc:  # never let the reported baseline kill the bench line
+                line["cpu_baseline"] = {"error": str(exc)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_em(args, pkg, dev, rank, world, barrier, max_over_ranks):
+    """Seconds per EM iteration, augmented formulation, 2048 x 60, R=400 (config 3 shape)."""
+    import torch
+    from paper_1906_08556_b200 import _estep, _lib, pipeline as P
+    D, p = 400, 100.0
+    n_utt, n_fr = args.em_utts, 300
+    rng = np.random.default_rng(7)
+    w = rng.dirichlet(np.full(C, 10.0))
+    mu = rng.normal(0.0, 8.0, (C, F))
+    a = rng.normal(0.0, 1.0, (C, F, 2 * F))
+    sig = np.einsum("cik,cjk->cij", a, a) / (2 * F) + 0.5 * np.eye(F)
+    Tg = rng.normal(0.0, 1.0, (C, F, D))
+    Tg[:, :, 0] = mu / p
+    gen = pkg.TvModel("augmented", Tg, sig, w, mu, None, p)
+    # utterances: latent z = p e1 + N(0, I); frames x = T_c z + Sigma_c^(1/2) e (generated on device)
+    g = torch.Generator(device=dev).manual_seed(11 + rank)
+    Td = torch.from_numpy(Tg).to(dev).view(C * F, D)
+    L = torch.linalg.cholesky(torch.from_numpy(sig).to(dev))
+    z = torch.randn((n_utt, D), dtype=torch.float64, device=dev, generator=g)
+    z[:, 0] += p
+    comp = torch.multinomial(torch.from_numpy(w).to(dev), n_utt * n_fr, replacement=True, generator=g)
+    x = torch.empty((n_utt * n_fr, F), dtype=torch.float32, device=dev)
+    for u0 in range(0, n_utt, 64):
+        u1 = min(n_utt, u0 + 64)
+        M = (Td @ z[u0:u1].T).T.reshape(u1 - u0, C, F)  # mean supervectors
+        cu = comp[u0 * n_fr:u1 * n_fr].view(u1 - u0, n_fr)
+        means = torch.gather(M, 1, cu[:, :, None].expand(-1, -1, F))
+        e = torch.randn((u1 - u0, n_fr, F), dtype=torch.float64, device=dev, generator=g)
+        noise = torch.einsum("utij,utj->uti", L[cu], e)
+        x[u0 * n_fr:u1 * n_fr] = (means + noise).reshape(-1, F).to(torch.float32)
+    del Td, M, means, noise, e
+    ids = [f"u{rank:02d}_{i:07d}" for i in range(n_utt)]
+    corpus = P.DeviceCorpus.from_device(x, np.arange(0, (n_utt + 1) * n_fr, n_fr), ids)
+    ubm_full = gen.alignment_ubm_full()
+    ubm_diag = gen.alignment_ubm_diag()
+    model = pkg.init_model(ubm_full, D, "augmented", seed=0, prior_offset=p)
+    cfg = P.TrainConfig(formulation="augmented", latent_dim=D, iterations=10 ** 6, min_div=True,
+                        sigma_update=True, top_k=K_TOP, prune=PRUNE, seeds=(0,))
+    tr = P.DeviceTrainer(model, corpus, cfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tr.align(ubm_diag, ubm_full.covariances)
+    barrier()
+    align_s = max_over_ranks(time.perf_counter() - t0)
+    for _ in range(args.em_warmup):
+        tr.iteration()
+    barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    auxes = []
+    for _ in range(args.em_steps):
+        auxes.append(tr.iteration())
+    e1.record(stream)
+    barrier()
+    sec = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.em_steps)
+    flop_utt = C * D * (D + 1) * 2 + 4 * C * F * D + D ** 3
+    return {"value": sec, "unit": "s/iter", "higher_is_better": False, "utts_per_gpu": n_utt,
+            "frames_per_utt": n_fr, "global_utts": world * n_utt, "steps": args.em_steps,
+            "warmup": args.em_warmup, "alignment_s": align_s,
+            "config": "augmented TVM, C=2048, F=60, R=400, min-div + Sigma update, realign 0 (config 3 shape)",
+            "achieved_tflops": world * n_utt * flop_utt / sec / 1e12, "aux_last": auxes[-1]}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=FRAMES_PER_GPU)
+    ap.add_argument("--em-utts", type=int, default=20000)
+    ap.add_argument("--em-steps", type=int, default=3)
+    ap.add_argument("--em-warmup", type=int, default=1)
+    ap.add_argument("--no-em", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-frames", type=int, default=4000)
+    ap.add_argument("--ref-frames", type=int, default=2000)
+    args = ap.parse_args()
+    if args.no_em:
+        args.em_utts = 0
+    if args.warmup < 3 and args.impl == "ours":
+        log("note: fewer than 3 warm-up steps")
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

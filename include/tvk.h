@@ -101,6 +101,11 @@ int tvk_align_frames(const void* x, int x_f64, int64_t T, int F, const double* d
 int tvk_select_topk(const void* x, int x_f64, int64_t T, int F, const double* diag_table, int C, int K,
                     int32_t* selected, double* values, void* stream);
 
+/* Full-covariance log-likelihoods of preselected components only (stage 2 of tvk_align_frames:
+ * the quadratic-feature DMMA GEMM with the selection-gather epilogue).  sel_ll is T*K f64. */
+int tvk_full_loglik_selected(const void* x, int x_f64, int64_t T, int F, const double* full_table, int C, int K,
+                             const int32_t* selected, double* sel_ll, void* stream);
+
 /* Frame feature expansion used by the dense log-likelihood API (GmmDiag/GmmFull.log_likelihoods):
  * kind 0 -> [x*x, x, 1] (T x (2F+1)); kind 1 -> [1, x_i, x_i x_j (i<=j)] (T x Q).  The dense T x C
  * log-likelihoods are then tvk_dgemm(features, table). */

@@ -49,7 +49,7 @@ def frames_to_device(features):
         x = features
         if x.dtype not in (torch.float32, torch.float64):
             x = x.to(torch.float64)
-        return x.to(_lib.device()).contiguous()
+        return x.to(_lib.device(), non_blocking=True).contiguous()
     arr = np.asarray(features)
     if arr.dtype != np.float32:
         arr = arr.astype(np.float64, copy=False)

@@ -44,6 +44,7 @@ SIGNATURES = {
     "tvk_align_frames": (_i, [_p, _i, _i64, _i, _p, _p, _i, _i, _d, _p, _i64, _p, _p, _p, _p, _p, _p]),
     "tvk_select_topk": (_i, [_p, _i, _i64, _i, _p, _i, _i, _p, _p, _p]),
     "tvk_frame_features": (_i, [_p, _i, _i64, _i, _i, _p, _p]),
+    "tvk_full_loglik_selected": (_i, [_p, _i, _i64, _i, _p, _i, _i, _p, _p, _p]),
     "tvk_bw_workspace_bytes": (_i64, [_i64, _i, _i]),
     "tvk_bw_stats": (_i, [_p, _i, _i, _p, _i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i64, _p, _i64, _p]),
     "tvk_posterior_workspace_bytes": (_i64, [_i, _i]),

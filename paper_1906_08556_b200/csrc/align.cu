@@ -652,3 +652,15 @@ extern "C" int tvk_frame_features(const void* x, int x_f64, int64_t T, int F, in
   TVK_CHECK_LAUNCH("frame_features");
   return TVK_OK;
 }
+
+/* Stage 2 alone (the dominant kernel of the frame-posterior path), for roofline timing and
+ * for callers that already hold a preselection: sel_ll[t*K+j] = full log-likelihood of
+ * component selected[t*K+j] for frame t. */
+extern "C" int tvk_full_loglik_selected(const void* x, int x_f64, int64_t T, int F, const double* full_table, int C,
+                                        int K, const int32_t* selected, double* sel_ll, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1 && K >= 1 && K <= kMaxTopK && K <= C, "full_loglik_selected: bad shape");
+  if (T == 0) return TVK_OK;
+  if (x_f64) return launch_full_ll<double>((const double*)x, T, F, full_table, C, K, selected, sel_ll, st);
+  return launch_full_ll<float>((const float*)x, T, F, full_table, C, K, selected, sel_ll, st);
+}
