@@ -34,7 +34,9 @@ C, F, K_TOP, PRUNE = 2048, 60, 20, 0.025
 FRAMES_PER_GPU = 10_000_000
 Q = 1 + F + F * (F + 1) // 2
 FLOP_FULL_PER_FRAME = 2 * C * Q            # dominant kernel (quadratic-feature GEMM)
-FLOP_PER_FRAME = 2 * C * (2 * F + 1) + FLOP_FULL_PER_FRAME   # 8,241,152
+FLOP_DIAG_PER_FRAME = 2 * C * (2 * F + 1)   # preselection GEMM [x^2, x, 1] . Wdiag
+FLOP_PER_FRAME = FLOP_DIAG_PER_FRAME + FLOP_FULL_PER_FRAME   # 8,241,152 (dense)
+FLOP_GROUPED_PER_FRAME = 2 * K_TOP * F * F                   # (x-mu)' P (x-mu) for the K selected
 FP64_PEAK_FILE = os.path.join(REPO, "profiles", "r01_fp64_pipe_peak.txt")
 
 
@@ -206,13 +208,17 @@ def bench_ours(args):
     offsets = _lib.empty((n + 1,), torch.int64)
     comps = _lib.empty((n * k,), torch.int32)
     wts = _lib.empty((n * k,), torch.float32)
-    ws_bytes = int(_lib.load().tvk_align_workspace_bytes(n, k))
+    ws_bytes = int(_lib.load().tvk_align_workspace_bytes(n, k, C))
     ws = _lib.empty((ws_bytes,), torch.uint8)
+    quad = None
 
-    def step():
-        _lib.call("tvk_align_frames", _lib.ptr(x), 0, n, F, _lib.ptr(dtab.table), _lib.ptr(ftab.table), C, k,
-                  PRUNE, _lib.ptr(ws), ws_bytes, _lib.ptr(offsets), _lib.ptr(comps), _lib.ptr(wts), None, None,
-                  _lib.stream())
+    def step(dense=False):
+        nonlocal quad
+        if dense and quad is None:
+            quad = ftab.table
+        _lib.call("tvk_align_frames", _lib.ptr(x), 0, n, F, _lib.ptr(dtab.table), _lib.ptr(quad) if dense else None,
+                  _lib.ptr(ftab.prec), C, k, PRUNE, 1 if dense else 0, _lib.ptr(ws), ws_bytes, _lib.ptr(offsets),
+                  _lib.ptr(comps), _lib.ptr(wts), None, None, _lib.stream())
 
     def barrier():
         if world > 1:
@@ -226,11 +232,21 @@ def bench_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, reps):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(reps):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / reps
+
     for _ in range(args.warmup):
         step()
     barrier()
     clocks = Clocks(local)
-    stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -241,36 +257,55 @@ def bench_ours(args):
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     entries = int(offsets[n].item())
     value = world * n / (ms / 1e3)
+    ref_offsets = offsets.clone()
+    ref_comps = comps[:entries].clone()
 
-    # dominant kernel alone (stage 2: quadratic-feature GEMM + selection gather), CUDA events
+    # per-stage kernel times (CUDA events on the launching stream)
     sel = _lib.empty((n, k), torch.int32)
-    _lib.call("tvk_select_topk", _lib.ptr(x), 0, n, F, _lib.ptr(dtab.table), C, k, _lib.ptr(sel), None,
-              _lib.stream())
     sll = _lib.empty((n, k))
-    reps = 3
-    for _ in range(1):
-        _lib.call("tvk_full_loglik_selected", _lib.ptr(x), 0, n, F, _lib.ptr(ftab.table), C, k, _lib.ptr(sel),
-                  _lib.ptr(sll), _lib.stream())
-    torch.cuda.synchronize()
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record(stream)
-    for _ in range(reps):
-        _lib.call("tvk_full_loglik_selected", _lib.ptr(x), 0, n, F, _lib.ptr(ftab.table), C, k, _lib.ptr(sel),
-                  _lib.ptr(sll), _lib.stream())
-    e3.record(stream)
-    torch.cuda.synchronize()
-    kern_ms = e2.elapsed_time(e3) / reps
+    gws_bytes = int(_lib.load().tvk_full_loglik_workspace_bytes(n, k, C))
+    gws = _lib.empty((gws_bytes,), torch.uint8)
+
+    def stage1():
+        _lib.call("tvk_select_topk", _lib.ptr(x), 0, n, F, _lib.ptr(dtab.table), C, k, _lib.ptr(sel), None,
+                  _lib.stream())
+
+    def stage2(dense=False):
+        _lib.call("tvk_full_loglik_selected", _lib.ptr(x), 0, n, F, _lib.ptr(quad) if dense else None,
+                  _lib.ptr(ftab.prec), C, k, 1 if dense else 0, _lib.ptr(sel), _lib.ptr(sll), _lib.ptr(gws),
+                  gws_bytes, _lib.stream())
+
+    stage1()
+    s1_ms = timed(stage1, 3)
+    stage2()
+    s2_ms = timed(stage2, 3)
     peak, peak_src = fp64_peak()
-    achieved = FLOP_FULL_PER_FRAME * n / (kern_ms / 1e3) / 1e12
+    s1_tf = FLOP_DIAG_PER_FRAME * n / (s1_ms / 1e3) / 1e12
+    s2_tf = FLOP_GROUPED_PER_FRAME * n / (s2_ms / 1e3) / 1e12
+    # dense north-star variant: quadratic-feature GEMM over all C components (the reference's own work)
+    dense = None
+    if args.dense_steps > 0:
+        step(dense=True)
+        torch.cuda.synchronize()
+        dense_ms = timed(lambda: step(dense=True), args.dense_steps)
+        same = bool(torch.equal(offsets, ref_offsets)) and bool(torch.equal(comps[:entries], ref_comps))
+        stage2(dense=True)
+        d2_ms = timed(lambda: stage2(dense=True), 1)
+        dense = {"value": world * n / (max_over_ranks(dense_ms) / 1e3), "unit": "frames/s",
+                 "ms_per_step": dense_ms, "steps": args.dense_steps,
+                 "alignment_identical_to_grouped": same,
+                 "full_ll_kernel": {"launch_ms": d2_ms, "flop_per_frame": FLOP_FULL_PER_FRAME,
+                                    "achieved_tflops": FLOP_FULL_PER_FRAME * n / (d2_ms / 1e3) / 1e12,
+                                    "frac_of_peak": FLOP_FULL_PER_FRAME * n / (d2_ms / 1e3) / 1e12 / peak}}
+    prof = os.path.join(REPO, "profiles", "r01_ncu_summary.json")
     traffic = None
-    prof = os.path.join(REPO, "profiles", "r01_ncu_full_ll.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch_per_frame")
-            traffic = traffic * n if traffic is not None else None
+            per_frame = json.load(open(prof))["select_topk"]["dram_bytes_per_frame"]
+            traffic = per_frame * n
         except Exception:
             traffic = None
-    del sel, sll
+    del sel, sll, gws
 
     # e2e through the public API: pinned host frames -> align_frames -> host SparseAlignment
     host = torch.empty((n, F), dtype=torch.float32, pin_memory=True)
@@ -306,14 +341,18 @@ def bench_ours(args):
                        "l2": "inputs (2.4 GB/GPU) larger than L2"},
             "x_realtime": value / 100.0,
             "entries_per_frame": entries / n,
-            "gpu_launches": 7 * args.steps,
+            "gpu_launches": 10 * args.steps,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": n * F * 4,
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                     "path": "paper_1906_08556_b200.align_frames(pinned host f32 frames) -> SparseAlignment"},
-            "roofline": {"bound": "tensor", "kernel": "full_ll_kernel (quadratic-feature DMMA GEMM)",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "peak_source": peak_src, "flop_per_frame": FLOP_FULL_PER_FRAME, "launch_ms": kern_ms,
-                         "share_of_step": kern_ms / ms, "traffic": traffic},
+            "roofline": {"bound": "tensor", "kernel": "select_topk_kernel (diag LL DMMA GEMM + stable top-20)",
+                         "achieved": s1_tf, "peak": peak, "unit": "TFLOP/s", "frac": s1_tf / peak,
+                         "peak_source": peak_src, "flop_per_frame": FLOP_DIAG_PER_FRAME, "launch_ms": s1_ms,
+                         "share_of_step": s1_ms / ms, "traffic": traffic},
+            "stages": {"select_topk_ms": s1_ms, "grouped_full_ll_ms": s2_ms,
+                       "grouped_full_ll_tflops": s2_tf, "grouped_full_ll_flop_per_frame": FLOP_GROUPED_PER_FRAME,
+                       "rest_ms": ms - s1_ms - s2_ms},
+            "dense_variant": dense,
             "clocks": clk,
         }
         if em is not None:
@@ -403,6 +442,7 @@ def main():
     ap.add_argument("--em-steps", type=int, default=3)
     ap.add_argument("--em-warmup", type=int, default=1)
     ap.add_argument("--no-em", action="store_true")
+    ap.add_argument("--dense-steps", type=int, default=1, help="steps of the dense quadratic-feature variant")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=4000)
     ap.add_argument("--ref-frames", type=int, default=2000)

@@ -83,28 +83,43 @@ int tvk_diag_table(const double* weights, const double* means, const double* var
 int tvk_full_table(const double* weights, const double* means, const double* covariances, int C, int F,
                    double* table, int32_t* status, void* stream);
 
-/* Scratch bytes tvk_align_frames needs for T frames and top-K K. */
-int64_t tvk_align_workspace_bytes(int64_t T, int K);
+/* Per-component precision table for the grouped path, stride tvk_precision_table_stride(F):
+ * [Sigma_c^-1 (F x F) | mu_c (F) | log w_c - (F log 2pi + log|Sigma_c|)/2 | 0].  status as above. */
+int tvk_precision_table(const double* weights, const double* means, const double* covariances, int C, int F,
+                        double* table, int32_t* status, void* stream);
+int64_t tvk_precision_table_stride(int F);
 
-/* Sparse frame alignment (gmm.py:389-439): diagonal top-K preselection (stable, lower index
- * wins ties), full-covariance log-likelihoods of the selected components, softmax over the
- * selection, prune (post >= prune), degenerate rule (argmax in selection order), renormalize,
- * entries sorted by component within a frame.  Outputs CSR: offsets (T+1, int64, offsets[T]
- * is the entry count E), components/weights with capacity T*K.  Optional debugging outputs:
- * selected (T*K int32, selection order) and sel_ll (T*K f64 full log-likelihoods). */
+#define TVK_ALIGN_DENSE 1 /* full LLs by the dense quadratic-feature GEMM over all C (else grouped) */
+
+/* Scratch bytes tvk_align_frames needs for T frames, top-K K and C components (either mode). */
+int64_t tvk_align_workspace_bytes(int64_t T, int K, int C);
+
+/* Sparse frame alignment (gmm.py:389-439) of frames x (T x F, f32 or f64 if x_f64): diagonal top-K
+ * preselection (stable, lower index wins ties), full-covariance log-likelihoods of the selected
+ * components, softmax over the selection, prune (post >= prune), degenerate rule (argmax in
+ * selection order), renormalize, entries sorted by component within a frame.
+ * Full log-likelihoods: default (grouped) mode evaluates only the T*K selected pairs, bucketed by
+ * component, from prec_table; flags & TVK_ALIGN_DENSE evaluates the quadratic-feature GEMM over
+ * all C from full_table and gathers the selected ones (the reference's own work, gmm.py:412).
+ * Outputs CSR: offsets (T+1, int64, offsets[T] is the entry count E), components/weights with
+ * capacity T*K.  Optional debugging outputs: selected (T*K int32, selection order) and sel_ll
+ * (T*K f64 full log-likelihoods). */
 int tvk_align_frames(const void* x, int x_f64, int64_t T, int F, const double* diag_table, const double* full_table,
-                     int C, int K, double prune, void* workspace, int64_t workspace_bytes, int64_t* offsets,
-                     int32_t* components, float* weights, int32_t* selected, double* sel_ll, void* stream);
+                     const double* prec_table, int C, int K, double prune, int flags, void* workspace,
+                     int64_t workspace_bytes, int64_t* offsets, int32_t* components, float* weights,
+                     int32_t* selected, double* sel_ll, void* stream);
 
 /* Stable top-K of the diagonal log-likelihoods (select_top_k, gmm.py:376-386 and gmm.py:409-410):
  * selected (T*K int32) in descending order, lower index first on ties; values (T*K f64, may be NULL). */
 int tvk_select_topk(const void* x, int x_f64, int64_t T, int F, const double* diag_table, int C, int K,
                     int32_t* selected, double* values, void* stream);
 
-/* Full-covariance log-likelihoods of preselected components only (stage 2 of tvk_align_frames:
- * the quadratic-feature DMMA GEMM with the selection-gather epilogue).  sel_ll is T*K f64. */
-int tvk_full_loglik_selected(const void* x, int x_f64, int64_t T, int F, const double* full_table, int C, int K,
-                             const int32_t* selected, double* sel_ll, void* stream);
+/* Full-covariance log-likelihoods of preselected components only (stage 2 of tvk_align_frames,
+ * either mode; grouped mode needs tvk_full_loglik_workspace_bytes of scratch).  sel_ll is T*K f64. */
+int64_t tvk_full_loglik_workspace_bytes(int64_t T, int K, int C);
+int tvk_full_loglik_selected(const void* x, int x_f64, int64_t T, int F, const double* full_table,
+                             const double* prec_table, int C, int K, int flags, const int32_t* selected,
+                             double* sel_ll, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Frame feature expansion used by the dense log-likelihood API (GmmDiag/GmmFull.log_likelihoods):
  * kind 0 -> [x*x, x, 1] (T x (2F+1)); kind 1 -> [1, x_i, x_i x_j (i<=j)] (T x Q).  The dense T x C

@@ -6,6 +6,8 @@ follow the reference (C components, F feature dims, D latent dims).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -28,16 +30,30 @@ class DiagTable:
 
 
 class FullTable:
-    """Q x C quadratic-feature table of a full-covariance GMM (gmm.py:106-119)."""
+    """Device tables of a full-covariance GMM (gmm.py:106-119): the per-component precision table
+    used by the grouped (default) path and, on demand, the Q x C quadratic-feature table used by
+    the dense path and the dense T x C log-likelihood API."""
 
     def __init__(self, weights, means, covariances):
-        w, mu, cov = _f64(weights), _f64(means), _f64(covariances)
-        self.C, self.F = mu.shape
-        q = 1 + self.F + self.F * (self.F + 1) // 2
-        self.table = _lib.empty((q, self.C))
+        self._w, self._mu, self._cov = _f64(weights), _f64(means), _f64(covariances)
+        self.C, self.F = self._mu.shape
+        stride = int(_lib.load().tvk_precision_table_stride(self.F))
+        self.prec = _lib.empty((self.C, stride))
         self.status = _lib.empty((self.C,), torch.int32)
-        call("tvk_full_table", ptr(w), ptr(mu), ptr(cov), self.C, self.F, ptr(self.table), ptr(self.status),
-             stream())
+        call("tvk_precision_table", ptr(self._w), ptr(self._mu), ptr(self._cov), self.C, self.F, ptr(self.prec),
+             ptr(self.status), stream())
+        self._quad = None
+
+    @property
+    def table(self):
+        """Q x C quadratic-feature table (built on first use)."""
+        if self._quad is None:
+            q = 1 + self.F + self.F * (self.F + 1) // 2
+            self._quad = _lib.empty((q, self.C))
+            st = _lib.empty((self.C,), torch.int32)
+            call("tvk_full_table", ptr(self._w), ptr(self._mu), ptr(self._cov), self.C, self.F, ptr(self._quad),
+                 ptr(st), stream())
+        return self._quad
 
     def bad_components(self):
         return np.flatnonzero(_lib.to_host(self.status) != _lib.ITEM_OK)
@@ -87,21 +103,34 @@ class AlignResult:
         self.n_entries = n_entries
 
 
-def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True):
-    """Frame posteriors for a device frame matrix (gmm.py:389-439), all on device."""
+ALIGN_DENSE = 1  # TVK_ALIGN_DENSE
+DEFAULT_DENSE = os.environ.get("TVK_ALIGN_MODE", "grouped") == "dense"
+
+
+def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True, dense=None):
+    """Frame posteriors for a device frame matrix (gmm.py:389-439), all on device.
+
+    ``dense`` selects the dense quadratic-feature GEMM over all C components (the reference's
+    own work, gmm.py:412) instead of the grouped evaluation of the K selected ones; both give
+    the same alignment (see tests/test_gpu_align.py).
+    """
+    if dense is None:
+        dense = DEFAULT_DENSE
     T, F = x.shape
     C = diag_tab.C
     k = min(top_k, C)
     offsets = _lib.empty((T + 1,), torch.int64)
     comps = _lib.empty((max(T * k, 1),), torch.int32)
     wts = _lib.empty((max(T * k, 1),), torch.float32)
-    ws_bytes = int(_lib.load().tvk_align_workspace_bytes(T, k))
+    ws_bytes = int(_lib.load().tvk_align_workspace_bytes(T, k, C))
     ws = _lib.empty((max(ws_bytes, 1),), torch.uint8)
     sel = _lib.empty((T, k), torch.int32) if debug else None
     sll = _lib.empty((T, k)) if debug else None
     xp, xf = _lib.x_args(x)
-    call("tvk_align_frames", xp, xf, T, F, ptr(diag_tab.table), ptr(full_tab.table), C, k, float(prune), ptr(ws),
-         ws_bytes, ptr(offsets), ptr(comps), ptr(wts), ptr(sel), ptr(sll), stream())
+    quad = ptr(full_tab.table) if dense else None
+    call("tvk_align_frames", xp, xf, T, F, ptr(diag_tab.table), quad, ptr(full_tab.prec), C, k, float(prune),
+         ALIGN_DENSE if dense else 0, ptr(ws), ws_bytes, ptr(offsets), ptr(comps), ptr(wts), ptr(sel), ptr(sll),
+         stream())
     n = int(offsets[T].item()) if sync_count else None
     res = AlignResult(offsets, comps, wts, n)
     if debug:

@@ -40,11 +40,14 @@ SIGNATURES = {
     "tvk_spd_small": (_i, [_p, _i, _i, _p, _p, _p, _p, _p]),
     "tvk_diag_table": (_i, [_p, _p, _p, _i, _i, _p, _p]),
     "tvk_full_table": (_i, [_p, _p, _p, _i, _i, _p, _p, _p]),
-    "tvk_align_workspace_bytes": (_i64, [_i64, _i]),
-    "tvk_align_frames": (_i, [_p, _i, _i64, _i, _p, _p, _i, _i, _d, _p, _i64, _p, _p, _p, _p, _p, _p]),
+    "tvk_precision_table": (_i, [_p, _p, _p, _i, _i, _p, _p, _p]),
+    "tvk_precision_table_stride": (_i64, [_i]),
+    "tvk_align_workspace_bytes": (_i64, [_i64, _i, _i]),
+    "tvk_align_frames": (_i, [_p, _i, _i64, _i, _p, _p, _p, _i, _i, _d, _i, _p, _i64, _p, _p, _p, _p, _p, _p]),
     "tvk_select_topk": (_i, [_p, _i, _i64, _i, _p, _i, _i, _p, _p, _p]),
     "tvk_frame_features": (_i, [_p, _i, _i64, _i, _i, _p, _p]),
-    "tvk_full_loglik_selected": (_i, [_p, _i, _i64, _i, _p, _i, _i, _p, _p, _p]),
+    "tvk_full_loglik_workspace_bytes": (_i64, [_i64, _i, _i]),
+    "tvk_full_loglik_selected": (_i, [_p, _i, _i64, _i, _p, _p, _i, _i, _i, _p, _p, _p, _i64, _p]),
     "tvk_bw_workspace_bytes": (_i64, [_i64, _i, _i]),
     "tvk_bw_stats": (_i, [_p, _i, _i, _p, _i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i64, _p, _i64, _p]),
     "tvk_posterior_workspace_bytes": (_i64, [_i, _i]),

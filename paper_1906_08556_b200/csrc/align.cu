@@ -471,10 +471,12 @@ struct AlignWs {
   float* w_pad;
   int64_t* counts;
   int64_t* block_sums;
+  void* group;  // grouped-path scratch (pair sort)
+  int64_t group_bytes;
   size_t bytes;
 };
 
-static AlignWs carve(void* base, int64_t T, int K) {
+static AlignWs carve(void* base, int64_t T, int K, int C) {
   AlignWs w{};
   size_t off = 0;
   char* b = (char*)base;
@@ -489,6 +491,8 @@ static AlignWs carve(void* base, int64_t T, int K) {
   w.w_pad = (float*)take(sizeof(float) * T * K);
   w.counts = (int64_t*)take(sizeof(int64_t) * (T + 1));
   w.block_sums = (int64_t*)take(sizeof(int64_t) * ((T + kScanBlock - 1) / kScanBlock + 1));
+  w.group_bytes = grouped_workspace_bytes(T * K, C);
+  w.group = take((size_t)w.group_bytes);
   w.bytes = off;
   return w;
 }
@@ -508,20 +512,15 @@ extern "C" int tvk_diag_table(const double* weights, const double* means, const 
 extern "C" int tvk_full_table(const double* weights, const double* means, const double* covariances, int C, int F,
                               double* table, int32_t* status, void* stream) {
   TVK_REQUIRE(C >= 1 && F >= 1 && F <= kSmallSpdMax, "full_table: need 1 <= F <= 96");
-  TVK_REQUIRE(F < 32767, "full_table: F too large");
   size_t smem = sizeof(double) * (2 * F * F + F);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(full_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (2 * kSmallSpdMax * kSmallSpdMax + kSmallSpdMax)));
-    attr = true;
-  }
+  cudaFuncSetAttribute(full_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double) * (2 * kSmallSpdMax * kSmallSpdMax + kSmallSpdMax)));
   full_table_kernel<<<C, 256, smem, (cudaStream_t)stream>>>(weights, means, covariances, C, F, table, status);
   TVK_CHECK_LAUNCH("full_table");
   return TVK_OK;
 }
 
-extern "C" int64_t tvk_align_workspace_bytes(int64_t T, int K) { return (int64_t)carve(nullptr, T, K).bytes; }
+extern "C" int64_t tvk_align_workspace_bytes(int64_t T, int K, int C) { return (int64_t)carve(nullptr, T, K, C).bytes; }
 
 namespace tvk {
 
@@ -559,6 +558,18 @@ static int launch_full_ll(const XT* x, int64_t T, int F, const double* full_tabl
 }
 
 template <typename XT>
+static int full_ll_dispatch(const XT* x, int64_t T, int F, const double* full_table, const double* prec_table,
+                            int C, int K, int flags, const int32_t* sel, double* sel_ll, void* group_ws,
+                            int64_t group_bytes, cudaStream_t st) {
+  if (flags & TVK_ALIGN_DENSE) {
+    TVK_REQUIRE(full_table != nullptr, "align_frames: dense mode needs the quadratic-feature table");
+    return launch_full_ll<XT>(x, T, F, full_table, C, K, sel, sel_ll, st);
+  }
+  TVK_REQUIRE(prec_table != nullptr, "align_frames: grouped mode needs the precision table");
+  return grouped_full_ll<XT>(x, T, F, prec_table, C, K, sel, sel_ll, group_ws, group_bytes, st);
+}
+
+template <typename XT>
 __global__ void frame_features_kernel(const XT* x, int64_t T, int F, int kind, double* out) {
   // kind 0: [x^2, x, 1] (2F+1); kind 1: [1, x_i, x_i x_j (i<=j)] (1+F+F(F+1)/2)
   int Q = kind == 0 ? 2 * F + 1 : 1 + F + F * (F + 1) / 2;
@@ -588,13 +599,15 @@ __global__ void frame_features_kernel(const XT* x, int64_t T, int F, int kind, d
 }
 
 template <typename XT>
-static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, const double* full_table, int C,
-                      int K, double prune, void* workspace, int64_t workspace_bytes, int64_t* offsets,
-                      int32_t* components, float* weights, int32_t* selected, double* sel_ll_out, cudaStream_t st) {
-  AlignWs w = carve(workspace, T, K);
+static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, const double* full_table,
+                      const double* prec_table, int C, int K, double prune, int flags, void* workspace,
+                      int64_t workspace_bytes, int64_t* offsets, int32_t* components, float* weights,
+                      int32_t* selected, double* sel_ll_out, cudaStream_t st) {
+  AlignWs w = carve(workspace, T, K, C);
   TVK_REQUIRE(workspace != nullptr && (int64_t)w.bytes <= workspace_bytes, "align_frames: workspace too small");
   TVK_TRY(launch_select<XT>(x, T, F, diag_table, C, K, w.sel, nullptr, st));
-  TVK_TRY(launch_full_ll<XT>(x, T, F, full_table, C, K, w.sel, w.sel_ll, st));
+  TVK_TRY(full_ll_dispatch<XT>(x, T, F, full_table, prec_table, C, K, flags, w.sel, w.sel_ll, w.group,
+                               w.group_bytes, st));
   int fb = (int)((T + 127) / 128);
   finalize_kernel<<<fb, 128, 0, st>>>(T, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts);
   TVK_CHECK_LAUNCH("finalize");
@@ -610,9 +623,10 @@ static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, c
 }  // namespace tvk
 
 extern "C" int tvk_align_frames(const void* x, int x_f64, int64_t T, int F, const double* diag_table,
-                                const double* full_table, int C, int K, double prune, void* workspace,
-                                int64_t workspace_bytes, int64_t* offsets, int32_t* components, float* weights,
-                                int32_t* selected, double* sel_ll_out, void* stream) {
+                                const double* full_table, const double* prec_table, int C, int K, double prune,
+                                int flags, void* workspace, int64_t workspace_bytes, int64_t* offsets,
+                                int32_t* components, float* weights, int32_t* selected, double* sel_ll_out,
+                                void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1, "align_frames: bad shape");
   TVK_REQUIRE(K >= 1 && K <= kMaxTopK && K <= C, "align_frames: top_k must be in [1, min(C, 32)]");
@@ -623,10 +637,10 @@ extern "C" int tvk_align_frames(const void* x, int x_f64, int64_t T, int F, cons
     return TVK_OK;
   }
   if (x_f64)
-    return align_impl<double>((const double*)x, T, F, diag_table, full_table, C, K, prune, workspace,
-                              workspace_bytes, offsets, components, weights, selected, sel_ll_out, st);
-  return align_impl<float>((const float*)x, T, F, diag_table, full_table, C, K, prune, workspace, workspace_bytes,
-                           offsets, components, weights, selected, sel_ll_out, st);
+    return align_impl<double>((const double*)x, T, F, diag_table, full_table, prec_table, C, K, prune, flags,
+                              workspace, workspace_bytes, offsets, components, weights, selected, sel_ll_out, st);
+  return align_impl<float>((const float*)x, T, F, diag_table, full_table, prec_table, C, K, prune, flags, workspace,
+                           workspace_bytes, offsets, components, weights, selected, sel_ll_out, st);
 }
 
 extern "C" int tvk_select_topk(const void* x, int x_f64, int64_t T, int F, const double* diag_table, int C, int K,
@@ -653,14 +667,19 @@ extern "C" int tvk_frame_features(const void* x, int x_f64, int64_t T, int F, in
   return TVK_OK;
 }
 
-/* Stage 2 alone (the dominant kernel of the frame-posterior path), for roofline timing and
- * for callers that already hold a preselection: sel_ll[t*K+j] = full log-likelihood of
- * component selected[t*K+j] for frame t. */
-extern "C" int tvk_full_loglik_selected(const void* x, int x_f64, int64_t T, int F, const double* full_table, int C,
-                                        int K, const int32_t* selected, double* sel_ll, void* stream) {
+extern "C" int64_t tvk_full_loglik_workspace_bytes(int64_t T, int K, int C) {
+  return grouped_workspace_bytes(T * K, C);
+}
+
+extern "C" int tvk_full_loglik_selected(const void* x, int x_f64, int64_t T, int F, const double* full_table,
+                                        const double* prec_table, int C, int K, int flags, const int32_t* selected,
+                                        double* sel_ll, void* workspace, int64_t workspace_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1 && K >= 1 && K <= kMaxTopK && K <= C, "full_loglik_selected: bad shape");
   if (T == 0) return TVK_OK;
-  if (x_f64) return launch_full_ll<double>((const double*)x, T, F, full_table, C, K, selected, sel_ll, st);
-  return launch_full_ll<float>((const float*)x, T, F, full_table, C, K, selected, sel_ll, st);
+  if (x_f64)
+    return full_ll_dispatch<double>((const double*)x, T, F, full_table, prec_table, C, K, flags, selected, sel_ll,
+                                    workspace, workspace_bytes, st);
+  return full_ll_dispatch<float>((const float*)x, T, F, full_table, prec_table, C, K, flags, selected, sel_ll,
+                                 workspace, workspace_bytes, st);
 }

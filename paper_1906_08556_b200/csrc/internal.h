@@ -29,3 +29,12 @@ int spd_small(const double* A, int batch, int n, double* chol, double* inv, doub
               cudaStream_t st);
 
 }  // namespace tvk
+
+namespace tvk {
+// grouped (selected-only) full-covariance log-likelihoods, align_grouped.cu
+__host__ __device__ inline int64_t precision_stride(int F) { return (int64_t)F * F + F + 2; }
+int64_t grouped_workspace_bytes(int64_t n_pairs, int C);
+template <typename XT>
+int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, int K, const int32_t* sel,
+                    double* sel_ll, void* ws_base, int64_t ws_bytes, cudaStream_t st);
+}  // namespace tvk

@@ -55,14 +55,19 @@ def test_align_matches_reference_golden(gpu, case):
     got.validate(top_k=k, prune=prune)
 
 
+@pytest.mark.parametrize("dense", [False, True], ids=["grouped", "dense"])
 @pytest.mark.parametrize("case", cases.ALIGN_CASES, ids=[c[0] for c in cases.ALIGN_CASES])
-def test_selection_and_full_ll_match_reference(gpu, case):
+def test_selection_and_full_ll_match_reference(gpu, case, dense):
     g = ALIGN[case[0]]
     diag, full, x, k, prune, _ = cases.align_inputs(case)
     from paper_1906_08556_b200 import _device, _lib
     dm, fm = _models(diag, full)
     xd = _device.frames_to_device(x)
-    res = _device.align(xd, dm.device_table(), fm.device_table(), k, prune, debug=True)
+    res = _device.align(xd, dm.device_table(), fm.device_table(), k, prune, debug=True, dense=dense)
+    ties0 = np.flatnonzero(g["boundary_gap"] < TIE_REL * np.maximum(1.0, np.abs(g["sel_full_ll"][:, 0])))
+    got = gpu.gmm.SparseAlignment(_lib.to_host(res.offsets), _lib.to_host(res.components[:res.n_entries]),
+                                  _lib.to_host(res.weights[:res.n_entries]))
+    _assert_alignment_matches(got, g["offsets"], g["components"], g["weights"], ties0)
     sel = _lib.to_host(res.selected)
     ties = g["boundary_gap"] < TIE_REL * np.maximum(1.0, np.abs(g["sel_full_ll"][:, 0]))
     mism = np.flatnonzero(np.any(sel != g["selected"], axis=1) & ~ties)
