@@ -61,6 +61,16 @@ int tvk_dgemm(int trans_a, int trans_b, int m, int n, int k, double alpha, const
               int64_t stride_a, const double* b, int64_t ldb, int64_t stride_b, double beta, double* c,
               int64_t ldc, int64_t stride_c, int batch, int out_mode, int splits, double* work, void* stream);
 
+/* Fixed-order reductions (bit-reproducible, no atomics):
+ *   tvk_colsum: out[j] = beta*out[j] + alpha * sum_r a[r*lda + j]   (rows x cols)
+ *   tvk_ddot:   out[0] = beta*out[0] + alpha * sum_i x_i y_i (y may be NULL: plain sum);
+ *               workspace of tvk_ddot_workspace_bytes(). */
+int tvk_colsum(const double* a, int64_t rows, int64_t cols, int64_t lda, double alpha, double beta, double* out,
+               void* stream);
+int64_t tvk_ddot_workspace_bytes(void);
+int tvk_ddot(const double* x, const double* y, int64_t n, double alpha, double beta, double* out, double* workspace,
+             void* stream);
+
 /* Batched SPD factorization of n x n matrices (n <= 96): lower Cholesky factor (optional),
  * inverse (optional, full symmetric), log-determinant (optional).  status[i] = TVK_ITEM_NOT_SPD
  * when the factorization of matrix i fails (outputs for it are then undefined).

@@ -58,14 +58,22 @@ def ones(n):
     return torch.ones(n, dtype=torch.float64, device=_lib.device())
 
 
-def col_sum_into(out_row, mat, rows, cols, beta=1.0):
-    """out (1 x cols) = beta*out + ones(1 x rows) @ mat (rows x cols)  [fixed-order reduction]."""
-    if rows == 0:
-        if beta == 0.0:
-            out_row.zero_()
-        return out_row
-    dgemm(ones(rows), mat, out_row, 1, cols, rows, beta=beta)
+def col_sum_into(out_row, mat, rows, cols, beta=1.0, alpha=1.0):
+    """out (cols) = beta*out + alpha * sum over the rows of mat (rows x cols)  [fixed order]."""
+    call("tvk_colsum", ptr(mat), rows, cols, cols, alpha, beta, ptr(out_row), stream())
     return out_row
+
+
+_DOT_WS = {}
+
+
+def dot_into(out, x, y, n, alpha=1.0, beta=1.0):
+    """out[0] = beta*out[0] + alpha * x.y over n elements (fixed-order reduction; y None: sum)."""
+    dev = _lib.device()
+    if dev not in _DOT_WS:
+        _DOT_WS[dev] = _lib.empty((int(_lib.load().tvk_ddot_workspace_bytes()) // 8,))
+    call("tvk_ddot", ptr(x), ptr(y), n, alpha, beta, ptr(out), ptr(_DOT_WS[dev]), stream())
+    return out
 
 
 class DeviceModel:
@@ -197,8 +205,8 @@ def accumulate_batch(dm: DeviceModel, ws: Workspace, acc: DeviceAcc, n, fm, S=No
     if S is not None:
         col_sum_into(acc.Ssum.view(1, C * F * F), S, Ub, C * F * F)
     # sum_u (0.5 b.phi - 0.5 log|L|)
-    dgemm(ones(Ub), bphi, acc.aux_post, 1, 1, Ub, alpha=0.5, beta=1.0)
-    dgemm(ones(Ub), logdet, acc.aux_post, 1, 1, Ub, alpha=-0.5, beta=1.0)
+    dot_into(acc.aux_post, bphi, None, Ub, alpha=0.5)
+    dot_into(acc.aux_post, logdet, None, Ub, alpha=-0.5)
     acc.count += Ub
 
 
@@ -207,10 +215,9 @@ def finalize_aux(dm: DeviceModel, ws: Workspace, acc: DeviceAcc):
     C, F = dm.C, dm.F
     out = acc.aux_post.clone()
     # -0.5 sum_c N_c (F log 2pi + log|Sigma_c|)
-    dgemm(acc.N.view(1, C), ws.const.view(C, 1), out, 1, 1, C, alpha=-0.5, beta=1.0)
+    dot_into(out, acc.N, ws.const, C, alpha=-0.5)
     # -0.5 <Sinv, Ssum>
-    K = C * F * F
-    dgemm(ws.Sinv.view(1, K), acc.Ssum.view(K, 1), out, 1, 1, K, alpha=-0.5, beta=1.0)
+    dot_into(out, ws.Sinv, acc.Ssum, C * F * F, alpha=-0.5)
     mu0 = dm.prior_mean
     return float(out.item()) - 0.5 * float(mu0 @ mu0) * acc.U
 

@@ -37,6 +37,9 @@ SIGNATURES = {
     "tvk_last_error": (_i, [ctypes.c_char_p, _i64]),
     "tvk_dgemm": (_i, [_i, _i, _i, _i, _i, _d, _p, _i64, _i64, _p, _i64, _i64, _d, _p, _i64, _i64, _i, _i, _i,
                        _p, _p]),
+    "tvk_colsum": (_i, [_p, _i64, _i64, _i64, _d, _d, _p, _p]),
+    "tvk_ddot_workspace_bytes": (_i64, []),
+    "tvk_ddot": (_i, [_p, _p, _i64, _d, _d, _p, _p, _p]),
     "tvk_spd_small": (_i, [_p, _i, _i, _p, _p, _p, _p, _p]),
     "tvk_diag_table": (_i, [_p, _p, _p, _i, _i, _p, _p]),
     "tvk_full_table": (_i, [_p, _p, _p, _i, _i, _p, _p, _p]),

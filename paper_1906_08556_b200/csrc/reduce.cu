@@ -1,0 +1,80 @@
+// Fixed-order (bit-reproducible) reductions used by the E-step accumulators:
+//   tvk_colsum: out[j] = beta*out[j] + alpha * sum_r a[r, j]   (N_c, phi_sum, moment sums over a batch)
+//   tvk_ddot:   out    = beta*out    + alpha * sum_i x_i y_i   (aux terms <Sigma^-1, Ssum>, N . const)
+// No floating-point atomics: every partial sum has a fixed owner and a fixed combination order that
+// does not depend on the device, so results match across runs and GPUs.
+#include "common.cuh"
+
+namespace tvk {
+
+constexpr int kDotBlocks = 1024;  // fixed partition (device-independent)
+constexpr int kDotThreads = 256;
+
+__global__ void colsum_kernel(const double* a, int64_t rows, int64_t cols, int64_t lda, double alpha, double beta,
+                              double* out) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t r = 0;
+  for (; r + 4 <= rows; r += 4) {
+    s0 += a[r * lda + j];
+    s1 += a[(r + 1) * lda + j];
+    s2 += a[(r + 2) * lda + j];
+    s3 += a[(r + 3) * lda + j];
+  }
+  for (; r < rows; r++) s0 += a[r * lda + j];
+  double s = (s0 + s1) + (s2 + s3);
+  out[j] = (beta != 0.0 ? beta * out[j] : 0.0) + alpha * s;
+}
+
+__global__ void dot_partial_kernel(const double* x, const double* y, int64_t n, double* partial) {
+  __shared__ double red[kDotThreads];
+  int64_t per = (n + kDotBlocks - 1) / kDotBlocks;
+  int64_t lo = blockIdx.x * per, hi = lo + per < n ? lo + per : n;
+  double s = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) s += x[i] * (y ? y[i] : 1.0);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kDotThreads / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void dot_final_kernel(const double* partial, double alpha, double beta, double* out) {
+  __shared__ double red[kDotThreads];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < kDotBlocks; i += kDotThreads) s += partial[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kDotThreads / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = (beta != 0.0 ? beta * out[0] : 0.0) + alpha * red[0];
+}
+
+}  // namespace tvk
+
+extern "C" int tvk_colsum(const double* a, int64_t rows, int64_t cols, int64_t lda, double alpha, double beta,
+                          double* out, void* stream) {
+  TVK_REQUIRE(rows >= 0 && cols >= 0 && lda >= cols, "colsum: bad shape");
+  if (cols == 0) return TVK_OK;
+  int64_t blocks = (cols + 255) / 256;
+  tvk::colsum_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a, rows, cols, lda, alpha, beta, out);
+  TVK_CHECK_LAUNCH("colsum");
+  return TVK_OK;
+}
+
+extern "C" int64_t tvk_ddot_workspace_bytes(void) { return tvk::kDotBlocks * (int64_t)sizeof(double); }
+
+extern "C" int tvk_ddot(const double* x, const double* y, int64_t n, double alpha, double beta, double* out,
+                        double* workspace, void* stream) {
+  TVK_REQUIRE(n >= 0 && workspace != nullptr, "ddot: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  tvk::dot_partial_kernel<<<tvk::kDotBlocks, tvk::kDotThreads, 0, st>>>(x, y, n, workspace);
+  tvk::dot_final_kernel<<<1, tvk::kDotThreads, 0, st>>>(workspace, alpha, beta, out);
+  TVK_CHECK_LAUNCH("ddot");
+  return TVK_OK;
+}
