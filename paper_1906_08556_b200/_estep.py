@@ -172,8 +172,10 @@ def posterior_batch(dm: DeviceModel, ws: Workspace, n, fm, want_moment=True, sta
     bphi = _lib.empty((Ub,))
     status = status_out if status_out is not None else _lib.empty((Ub,), torch.int32)
     flags = POST_ADD_IDENTITY | (0 if covariance else POST_MOMENT)
+    ws_bytes = int(_lib.load().tvk_posterior_workspace_bytes(D, Ub))
+    scratch = _lib.empty((max(ws_bytes // 8, 1),))
     call("tvk_posterior", ptr(Lpk), ptr(b), Ub, D, flags, ptr(phi), ptr(Mpk), ptr(logdet), ptr(bphi), ptr(status),
-         None, 0, stream())
+         ptr(scratch), ws_bytes, stream())
     return phi, Mpk, logdet, bphi, status, b
 
 

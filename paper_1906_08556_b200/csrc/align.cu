@@ -101,35 +101,50 @@ __global__ void full_table_kernel(const double* w, const double* mu, const doubl
 // ----------------------------------------------------------------------------- stage 1: top-K
 
 namespace sel {
-constexpr int BM = 64, BN = 64, NT = 256;
-using Cfg = GemmCfg<BM, BN, 4, 2, 4, 1>;  // warp tile 32x16; BK field unused (full K resident)
+// Warp-specialized: warps 0-3 run the DMMA GEMM (64 frames x 64 components per block, K streamed
+// through a 3-stage cp.async ring of 16-deep table chunks), warps 4-7 merge the finished block into
+// the per-frame top-K lists.  Two LL tile buffers let the merge of block n overlap the MMA of
+// block n+1 (named barriers FULL/EMPTY per buffer).
+constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 3;
+constexpr int NMMA = 128, NMERGE = 128, NT = NMMA + NMERGE;
+constexpr int BS = BN + 4;  // == 4 (mod 16): conflict-free B fragments
+constexpr int LS = BN + 1;
+using Cfg = GemmCfg<BM, BN, BK, 2, 2, NSTAGE>;  // 4 MMA warps of 32x32
+__host__ __device__ inline int kpad(int F) { return ((2 * F + 1) + BK - 1) / BK * BK; }
+__host__ __device__ inline int astride(int F) { int kp = kpad(F); return kp + ((4 - kp % 16) + 16) % 16; }
+__host__ inline size_t smem_bytes(int F, int K) {
+  return sizeof(double) * ((size_t)BM * astride(F) + NSTAGE * BK * BS + 2 * BM * LS + (size_t)BM * K) +
+         sizeof(int) * ((size_t)BM * K + BM);
 }
+}  // namespace sel
 
 __device__ __forceinline__ bool ranks_before(double v, int i, double w, int j) {  // (v,i) strictly better
   return v > w || (v == w && i < j);
 }
 
-// dynamic smem: A [BM][KP+4] features, B [KP][BN+4] table block, LL [BM][BN+1], lists
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n));
+}
+
 template <typename XT>
-__global__ void __launch_bounds__(sel::NT) select_topk_kernel(const XT* x, int64_t T, int F, const double* tab,
-                                                              int C, int K, int32_t* sel_out, double* sel_val) {
+__global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, int64_t T, int F, const double* tab,
+                                                                 int C, int K, int32_t* sel_out, double* sel_val) {
   using namespace sel;
   extern __shared__ __align__(16) double smem[];
   const int KD = 2 * F + 1;
-  const int KP = (KD + 3) & ~3;
-  const int AS = KP + 4, BS = BN + 4, LS = BN + 1;
-  double* sA = smem;
-  double* sB = sA + BM * AS;
-  double* sL = sB + KP * BS;
-  double* lv = sL + BM * LS;                    // [BM][K]
+  const int KP = kpad(F), AS = astride(F);
+  double* sA = smem;                          // [BM][AS]
+  double* sB = sA + BM * AS;                  // [NSTAGE][BK][BS]
+  double* sL = sB + NSTAGE * BK * BS;         // [2][BM][LS]
+  double* lv = sL + 2 * BM * LS;              // [BM][K]
   int* li = reinterpret_cast<int*>(lv + BM * K);  // [BM][K]
-  int* lc = li + BM * K;                        // [BM]
+  int* lc = li + BM * K;                      // [BM]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
   const int64_t t0 = (int64_t)blockIdx.x * BM;
+  const int nblocks = (C + BN - 1) / BN, nk = KP / BK;
 
-  // features [x^2, x, 1, 0-pad] for this frame tile
-  for (int idx = tid; idx < BM * KP; idx += NT) {
+  for (int idx = tid; idx < BM * KP; idx += NT) {  // features [x^2, x, 1, 0-pad]
     int r = idx / KP, k = idx % KP;
     double v = 0.0;
     if (t0 + r < T) {
@@ -138,83 +153,126 @@ __global__ void __launch_bounds__(sel::NT) select_topk_kernel(const XT* x, int64
         v = xv * xv;
       } else if (k < 2 * F) {
         v = (double)x[(t0 + r) * F + (k - F)];
-      } else if (k == 2 * F) {
+      } else if (k == KD - 1) {
         v = 1.0;
       }
     }
     sA[r * AS + k] = v;
   }
   for (int r = tid; r < BM; r += NT) lc[r] = 0;
+  __syncthreads();
 
-  for (int n0 = 0; n0 < C; n0 += BN) {
-    __syncthreads();  // previous block's list merge done with sL / sB
-    for (int idx = tid; idx < KP * BN; idx += NT) {
-      int k = idx / BN, c = idx % BN;
-      bool ok = k < KD && n0 + c < C;
-      cp_async8(&sB[k * BS + c], ok ? tab + (int64_t)k * C + n0 + c : tab, ok);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    Acc<Cfg> acc;
-    acc.zero();
+  if (warp < NMMA / 32) {
+    // ------------------------------------------------------------ MMA warps
+    const int wm = warp >> 1, wn = warp & 1;
     const int g = lane >> 2, t = lane & 3;
-    for (int kk = 0; kk < KP; kk += 4) {
-      double a[Cfg::FM], b[Cfg::FN];
-#pragma unroll
-      for (int i = 0; i < Cfg::FM; i++) a[i] = sA[(wm * Cfg::WTM + i * 8 + g) * AS + kk + t];
-#pragma unroll
-      for (int j = 0; j < Cfg::FN; j++) b[j] = sB[(kk + t) * BS + wn * Cfg::WTN + j * 8 + g];
-#pragma unroll
-      for (int i = 0; i < Cfg::FM; i++)
-#pragma unroll
-        for (int j = 0; j < Cfg::FN; j++) dmma884(acc.v[i][j][0], acc.v[i][j][1], a[i], b[j]);
+    const int total = nblocks * nk;
+    auto load = [&](int chunk) {
+      int blk = chunk / nk, kc = chunk % nk;
+      double* dst = sB + (chunk % NSTAGE) * BK * BS;
+      for (int idx = tid; idx < BK * BN; idx += NMMA) {
+        int k = idx / BN, c = idx % BN;
+        int gk = kc * BK + k, gc = blk * BN + c;
+        bool ok = gk < KD && gc < C;
+        cp_async8(&dst[k * BS + c], ok ? tab + (int64_t)gk * C + gc : tab, ok);
+      }
+    };
+    for (int s = 0; s < NSTAGE - 1; s++) {
+      if (s < total) load(s);
+      cp_async_commit();
     }
-    for_each_acc<Cfg>(acc, wm, wn, lane, [&](int r, int c, double v) { sL[r * LS + c] = v; });
-    __syncthreads();
-
-    // merge this block into each frame's running top-K (one warp per frame at a time)
-    const int nb = min(BN, C - n0);
-    for (int r = warp; r < BM; r += NT / 32) {
-      if (t0 + r >= T) continue;
-      int cnt = lc[r];
-      double myv = (lane < cnt) ? lv[r * K + lane] : -INFINITY;
-      int myi = (lane < cnt) ? li[r * K + lane] : 0x7fffffff;
-      for (int base = 0; base < nb; base += 32) {
-        int ci = base + lane;
-        double cv = ci < nb ? sL[r * LS + ci] : -INFINITY;
-        int gi = n0 + ci;
-        double wv = __shfl_sync(0xffffffffu, myv, K - 1);
-        int wi = __shfl_sync(0xffffffffu, myi, K - 1);
-        bool cand = ci < nb && (cnt < K || ranks_before(cv, gi, wv, wi));
-        unsigned mask = __ballot_sync(0xffffffffu, cand);
-        while (mask) {
-          int src = __ffs(mask) - 1;
-          mask &= mask - 1;
-          double v = __shfl_sync(0xffffffffu, cv, src);
-          int vi = __shfl_sync(0xffffffffu, gi, src);
-          wv = __shfl_sync(0xffffffffu, myv, K - 1);
-          wi = __shfl_sync(0xffffffffu, myi, K - 1);
-          if (cnt == K && !ranks_before(v, vi, wv, wi)) continue;
-          unsigned better = __ballot_sync(0xffffffffu, lane < cnt && ranks_before(myv, myi, v, vi));
-          int pos = __popc(better);
-          double upv = __shfl_up_sync(0xffffffffu, myv, 1);
-          int upi = __shfl_up_sync(0xffffffffu, myi, 1);
-          if (lane > pos) {
-            myv = upv;
-            myi = upi;
-          } else if (lane == pos) {
-            myv = v;
-            myi = vi;
-          }
-          cnt = min(cnt + 1, K);
+    int chunk = 0;
+    for (int blk = 0; blk < nblocks; blk++) {
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int kc = 0; kc < nk; kc++, chunk++) {
+        cp_async_wait<NSTAGE - 2>();
+        named_sync(1, NMMA);
+        if (chunk + NSTAGE - 1 < total) load(chunk + NSTAGE - 1);
+        cp_async_commit();
+        const double* b_s = sB + (chunk % NSTAGE) * BK * BS;
+        const double* a_s = sA + kc * BK;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+          double a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; i++) a[i] = a_s[(wm * 32 + i * 8 + g) * AS + kk + t];
+#pragma unroll
+          for (int j = 0; j < 4; j++) b[j] = b_s[(kk + t) * BS + wn * 32 + j * 8 + g];
+#pragma unroll
+          for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
       }
-      if (lane < K) {
-        lv[r * K + lane] = myv;
-        li[r * K + lane] = myi;
+      const int buf = blk & 1;
+      if (blk >= 2) named_sync(4 + buf, NT);  // wait until the merge warps released this buffer
+      double* L = sL + buf * BM * LS;
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          int r = wm * 32 + i * 8 + g, c = wn * 32 + j * 8 + 2 * t;
+          L[r * LS + c] = acc[i][j][0];
+          L[r * LS + c + 1] = acc[i][j][1];
+        }
+      __threadfence_block();
+      named_arrive(2 + buf, NT);  // FULL[buf]
+    }
+    cp_async_wait<0>();
+  } else {
+    // ------------------------------------------------------------ merge warps
+    const int mw = warp - NMMA / 32;
+    for (int blk = 0; blk < nblocks; blk++) {
+      const int buf = blk & 1;
+      named_sync(2 + buf, NT);  // FULL[buf]
+      const double* L = sL + buf * BM * LS;
+      const int n0 = blk * BN, nb = min(BN, C - n0);
+      for (int r = mw; r < BM; r += NMERGE / 32) {
+        if (t0 + r >= T) continue;
+        int cnt = lc[r];
+        double myv = (lane < cnt) ? lv[r * K + lane] : -INFINITY;
+        int myi = (lane < cnt) ? li[r * K + lane] : 0x7fffffff;
+        for (int base = 0; base < nb; base += 32) {
+          int ci = base + lane;
+          double cv = ci < nb ? L[r * LS + ci] : -INFINITY;
+          int gi = n0 + ci;
+          double wv = __shfl_sync(0xffffffffu, myv, K - 1);
+          int wi = __shfl_sync(0xffffffffu, myi, K - 1);
+          bool cand = ci < nb && (cnt < K || ranks_before(cv, gi, wv, wi));
+          unsigned mask = __ballot_sync(0xffffffffu, cand);
+          while (mask) {
+            int src = __ffs(mask) - 1;
+            mask &= mask - 1;
+            double v = __shfl_sync(0xffffffffu, cv, src);
+            int vi = __shfl_sync(0xffffffffu, gi, src);
+            wv = __shfl_sync(0xffffffffu, myv, K - 1);
+            wi = __shfl_sync(0xffffffffu, myi, K - 1);
+            if (cnt == K && !ranks_before(v, vi, wv, wi)) continue;
+            unsigned better = __ballot_sync(0xffffffffu, lane < cnt && ranks_before(myv, myi, v, vi));
+            int pos = __popc(better);
+            double upv = __shfl_up_sync(0xffffffffu, myv, 1);
+            int upi = __shfl_up_sync(0xffffffffu, myi, 1);
+            if (lane > pos) {
+              myv = upv;
+              myi = upi;
+            } else if (lane == pos) {
+              myv = v;
+              myi = vi;
+            }
+            cnt = min(cnt + 1, K);
+          }
+        }
+        if (lane < K) {
+          lv[r * K + lane] = myv;
+          li[r * K + lane] = myi;
+        }
+        if (lane == 0) lc[r] = cnt;
       }
-      if (lane == 0) lc[r] = cnt;
+      if (blk + 2 < nblocks) named_arrive(4 + buf, NT);  // EMPTY[buf]
     }
   }
   __syncthreads();
@@ -527,14 +585,12 @@ namespace tvk {
 template <typename XT>
 static int launch_select(const XT* x, int64_t T, int F, const double* diag_table, int C, int K, int32_t* sel,
                          double* val, cudaStream_t st) {
-  using namespace sel;
-  int KP = ((2 * F + 1) + 3) & ~3;
-  size_t smem = sizeof(double) * (BM * (KP + 4) + KP * (BN + 4) + BM * (BN + 1) + BM * K) + sizeof(int) * (BM * K + BM);
+  size_t smem = sel::smem_bytes(F, K);
   TVK_REQUIRE(smem <= 227 * 1024, "align_frames: F too large for the preselection tile");
   cudaFuncSetAttribute(select_topk_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int64_t grid = (T + BM - 1) / BM;
+  int64_t grid = (T + sel::BM - 1) / sel::BM;
   TVK_REQUIRE(grid < (1ll << 31), "align_frames: too many frames for one call");
-  select_topk_kernel<XT><<<(unsigned)grid, NT, smem, st>>>(x, T, F, diag_table, C, K, sel, val);
+  select_topk_kernel<XT><<<(unsigned)grid, sel::NT, smem, st>>>(x, T, F, diag_table, C, K, sel, val);
   TVK_CHECK_LAUNCH("select_topk");
   return TVK_OK;
 }

@@ -18,8 +18,9 @@
 
 namespace tvk {
 
-constexpr int PT = 256;  // threads per CTA
+constexpr int PT = 128;  // threads per CTA (4 warps; 4 CTAs per SM overlap the serial panel phases)
 constexpr int NB = 32;   // panel / tile width
+constexpr int kCtasPerSm = 4;
 constexpr int kPosteriorMaxD = 768;
 
 struct Opnd {
@@ -29,6 +30,7 @@ struct Opnd {
   int ncols;   // dense cols
   int r0, c0;
   bool packed, trans;
+  bool sym;  // packed symmetric: (r, c) with c > r reads (c, r)
 };
 
 __device__ __forceinline__ Opnd packed_op(const double* p, int n, int r0, int c0, bool trans) {
@@ -41,6 +43,7 @@ __device__ __forceinline__ Opnd packed_op(const double* p, int n, int r0, int c0
   o.c0 = c0;
   o.packed = true;
   o.trans = trans;
+  o.sym = false;
   return o;
 }
 __device__ __forceinline__ Opnd dense_op(const double* p, int64_t ld, int nr, int nc, int r0, int c0, bool trans) {
@@ -53,40 +56,52 @@ __device__ __forceinline__ Opnd dense_op(const double* p, int64_t ld, int nr, in
   o.c0 = c0;
   o.packed = false;
   o.trans = trans;
+  o.sym = false;
   return o;
 }
 
 __device__ __forceinline__ double ld_elem(const Opnd& o, int r, int c) {
-  if (o.packed) return (r < o.n && c <= r && c >= 0) ? o.p[packed_index(r, c)] : 0.0;
+  if (o.packed) {
+    if (o.sym && c > r) {
+      int t = r;
+      r = c;
+      c = t;
+    }
+    return (r < o.n && c <= r && c >= 0) ? o.p[packed_index(r, c)] : 0.0;
+  }
   return (r < o.n && c < o.ncols && r >= 0 && c >= 0) ? o.p[(int64_t)r * o.ld + c] : 0.0;
 }
 
 // acc(32x32) += A(32 x klen) * B(klen x 32); A logical (i,k), B logical (k,j).
 __device__ __forceinline__ void tile_mma(double (&acc)[4][4][2], const Opnd& A, const Opnd& B, int klen, int lane) {
   const int g = lane >> 2, t = lane & 3;
-  double a[8][4], b[8][4];
+  // two k-steps of fragments in flight (16 loads) per 32 MMAs: bounded registers, 4 CTAs/SM
+#pragma unroll 1
+  for (int ks0 = 0; ks0 < 8; ks0 += 2) {
+    double a[2][4], b[2][4];
 #pragma unroll
-  for (int ks = 0; ks < 8; ks++) {
-    int k = ks * 4 + t;
-    bool kin = k < klen;
+    for (int h = 0; h < 2; h++) {
+      int k = (ks0 + h) * 4 + t;
+      bool kin = k < klen;
 #pragma unroll
-    for (int f = 0; f < 4; f++) {
-      int i = f * 8 + g;
-      double av = 0.0, bv = 0.0;
-      if (kin) {
-        av = A.trans ? ld_elem(A, A.r0 + k, A.c0 + i) : ld_elem(A, A.r0 + i, A.c0 + k);
-        bv = B.trans ? ld_elem(B, B.r0 + i, B.c0 + k) : ld_elem(B, B.r0 + k, B.c0 + i);
+      for (int f = 0; f < 4; f++) {
+        int i = f * 8 + g;
+        double av = 0.0, bv = 0.0;
+        if (kin) {
+          av = A.trans ? ld_elem(A, A.r0 + k, A.c0 + i) : ld_elem(A, A.r0 + i, A.c0 + k);
+          bv = B.trans ? ld_elem(B, B.r0 + i, B.c0 + k) : ld_elem(B, B.r0 + k, B.c0 + i);
+        }
+        a[h][f] = av;
+        b[h][f] = bv;
       }
-      a[ks][f] = av;
-      b[ks][f] = bv;
     }
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int fi = 0; fi < 4; fi++)
+#pragma unroll
+        for (int fj = 0; fj < 4; fj++) dmma884(acc[fi][fj][0], acc[fi][fj][1], a[h][fi], b[h][fj]);
   }
-#pragma unroll
-  for (int ks = 0; ks < 8; ks++)
-#pragma unroll
-    for (int fi = 0; fi < 4; fi++)
-#pragma unroll
-      for (int fj = 0; fj < 4; fj++) dmma884(acc[fi][fj][0], acc[fi][fj][1], a[ks][fi], b[ks][fj]);
 }
 
 __device__ __forceinline__ void zero_acc(double (&acc)[4][4][2]) {
@@ -194,22 +209,93 @@ __device__ void packed_cho_solve_warp(const double* P, int n, double* v, int lan
   }
 }
 
+// ------------------------------------------------------------------ SPD inverse (trtri + lauum)
+
+// After packed_cholesky: L holds R (lower).  Overwrites L with Y = R^-1 (row block by row block:
+// Y_IJ = -Y_II sum_{K=J}^{I-1} R_IK Y_KJ, staged through the per-CTA scratch `tmp` [NB][ldt]) and
+// writes M = Y^T Y (= (R R^T)^-1) (+ v v^T if v != NULL) packed into M.
+__device__ void packed_inverse_from_chol(double* L, int D, double* M, const double* v, double* tmp, int ldt,
+                                        double* sdiag, double* sinv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nblk = (D + NB - 1) / NB;
+  for (int I = 0; I < nblk; I++) {
+    const int i0 = I * NB, iw = min(NB, D - i0);
+    for (int idx = tid; idx < NB * NB; idx += PT) {
+      int r = idx / NB, c = idx % NB;
+      sdiag[idx] = (r < iw && c <= r) ? L[packed_index(i0 + r, i0 + c)] : (r == c ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    for (int j = tid; j < NB; j += PT) {  // column j of Y_II (forward substitution)
+      for (int r = 0; r < j; r++) sinv[r * NB + j] = 0.0;
+      sinv[j * NB + j] = 1.0 / sdiag[j * NB + j];
+      for (int r = j + 1; r < NB; r++) {
+        double s = 0.0;
+        for (int k = j; k < r; k++) s += sdiag[r * NB + k] * sinv[k * NB + j];
+        sinv[r * NB + j] = -s / sdiag[r * NB + r];
+      }
+    }
+    for (int J = warp; J < I; J += PT / 32) {  // T_IJ = sum_{K=J}^{I-1} R_IK Y_KJ
+      double acc[4][4][2];
+      zero_acc(acc);
+      for (int K = J; K < I; K++)
+        tile_mma(acc, packed_op(L, D, i0, K * NB, false), packed_op(L, D, K * NB, J * NB, false), NB, lane);
+      acc_foreach(acc, lane, [&](int r, int c, double val) { tmp[r * ldt + J * NB + c] = val; });
+    }
+    __syncthreads();
+    for (int J = warp; J < I; J += PT / 32) {  // Y_IJ = -Y_II T_IJ (overwrites R_IJ)
+      double acc[4][4][2];
+      zero_acc(acc);
+      tile_mma(acc, dense_op(sinv, NB, NB, NB, 0, 0, false), dense_op(tmp, ldt, NB, ldt, 0, J * NB, false), NB, lane);
+      acc_foreach(acc, lane, [&](int r, int c, double val) {
+        if (r < iw) L[packed_index(i0 + r, J * NB + c)] = -val;
+      });
+    }
+    for (int idx = tid; idx < iw * iw; idx += PT) {
+      int r = idx / iw, c = idx % iw;
+      if (c <= r) L[packed_index(i0 + r, i0 + c)] = sinv[r * NB + c];
+    }
+    __syncthreads();
+  }
+  // M_IJ = sum_{K>=I} Y_KI^T Y_KJ (+ v_i v_j), lower tiles I >= J
+  const int ntiles = nblk * (nblk + 1) / 2;
+  for (int tix = warp; tix < ntiles; tix += PT / 32) {
+    int I = 0, base = 0;
+    while (base + I + 1 <= tix) {
+      base += I + 1;
+      I++;
+    }
+    int J = tix - base;
+    double acc[4][4][2];
+    zero_acc(acc);
+    for (int K = I; K < nblk; K++)
+      tile_mma(acc, packed_op(L, D, K * NB, I * NB, true), packed_op(L, D, K * NB, J * NB, false),
+               min(NB, D - K * NB), lane);
+    acc_foreach(acc, lane, [&](int r, int c, double val) {
+      int gi = I * NB + r, gj = J * NB + c;
+      if (gi < D && gj <= gi) M[packed_index(gi, gj)] = v ? val + v[gi] * v[gj] : val;
+    });
+  }
+  __syncthreads();
+}
+
+__host__ __device__ inline int tmp_ld(int D) { return ((D + 11) / 16) * 16 + 4; }  // == 4 (mod 16)
+
 // ------------------------------------------------------------------ posterior kernel
 
-__global__ void __launch_bounds__(PT, 1) posterior_kernel(double* lpk, const double* bvec, int U, int D,
-                                                          int flags, double* phi_out, double* mpk,
-                                                          double* logdet_out, double* bphi_out, int32_t* status) {
+__global__ void __launch_bounds__(PT, kCtasPerSm) posterior_kernel(double* lpk, const double* bvec, int U, int D,
+                                                                   int flags, double* phi_out, double* mpk,
+                                                                   double* logdet_out, double* bphi_out,
+                                                                   int32_t* status, double* scratch) {
   extern __shared__ __align__(16) double sm[];
-  const int ldt = ((D + 11) / 16) * 16 + 4;  // row stride of T-temp, == 4 (mod 16): conflict-free
-  double* tmp = sm;                           // [NB][ldt]  T_IJ = sum_K R_IK Y_KJ for one row block
-  double* sdiag = tmp + NB * ldt;             // [NB*NB]
-  double* sinv = sdiag + NB * NB;             // [NB*NB]   Y_II
-  double* vb = sinv + NB * NB;                // [D]       phi
+  const int ldt = tmp_ld(D);
+  double* tmp = scratch + (int64_t)blockIdx.x * NB * ldt;  // [NB][ldt] (L2-resident)
+  double* sdiag = sm;                                      // [NB*NB]
+  double* sinv = sdiag + NB * NB;                          // [NB*NB]
+  double* vb = sinv + NB * NB;                             // [D]  phi
   __shared__ int bad;
   __shared__ double red;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t P = packed_size(D);
-  const int nblk = (D + NB - 1) / NB;
 
   for (int u = blockIdx.x; u < U; u += gridDim.x) {
     double* L = lpk + (int64_t)u * P;
@@ -222,20 +308,25 @@ __global__ void __launch_bounds__(PT, 1) posterior_kernel(double* lpk, const dou
     }
     if (tid == 0 && status) status[u] = TVK_ITEM_OK;
     // log|L| and phi = L^-1 b (cho_solve)
-    for (int i = tid; i < D; i += PT) vb[i] = bvec[(int64_t)u * D + i];
-    __syncthreads();
     if (warp == 0) {
       double s = 0.0;
       for (int i = lane; i < D; i += 32) s += log(L[packed_index(i, i)]);
       s = warp_sum(s);
       if (lane == 0) red = 2.0 * s;
-      packed_cho_solve_warp(L, D, vb, lane);
+    }
+    if (bvec) {
+      for (int i = tid; i < D; i += PT) vb[i] = bvec[(int64_t)u * D + i];
+      __syncthreads();
+      if (warp == 0) packed_cho_solve_warp(L, D, vb, lane);
+      __syncthreads();
+      if (phi_out)
+        for (int i = tid; i < D; i += PT) phi_out[(int64_t)u * D + i] = vb[i];
     }
     __syncthreads();
-    for (int i = tid; i < D; i += PT) phi_out[(int64_t)u * D + i] = vb[i];
     if (warp == 1 && (bphi_out || logdet_out)) {
       double s = 0.0;
-      for (int i = lane; i < D; i += 32) s += bvec[(int64_t)u * D + i] * vb[i];
+      if (bvec)
+        for (int i = lane; i < D; i += 32) s += bvec[(int64_t)u * D + i] * vb[i];
       s = warp_sum(s);
       if (lane == 0) {
         if (bphi_out) bphi_out[u] = s;
@@ -243,85 +334,30 @@ __global__ void __launch_bounds__(PT, 1) posterior_kernel(double* lpk, const dou
       }
     }
     if (mpk == nullptr) continue;
-    // Y = R^-1 in place, row block by row block
-    for (int I = 0; I < nblk; I++) {
-      const int i0 = I * NB, iw = min(NB, D - i0);
-      // Y_II = R_II^-1 into sinv (lower), via the whole block
-      for (int idx = tid; idx < NB * NB; idx += PT) {
-        int r = idx / NB, c = idx % NB;
-        sdiag[idx] = (r < iw && c <= r) ? L[packed_index(i0 + r, i0 + c)] : (r == c ? 1.0 : 0.0);
-      }
-      __syncthreads();
-      for (int j = tid; j < NB; j += PT) {  // column j of the inverse (forward substitution)
-        for (int r = 0; r < j; r++) sinv[r * NB + j] = 0.0;
-        sinv[j * NB + j] = 1.0 / sdiag[j * NB + j];
-        for (int r = j + 1; r < NB; r++) {
-          double s = 0.0;
-          for (int k = j; k < r; k++) s += sdiag[r * NB + k] * sinv[k * NB + j];
-          sinv[r * NB + j] = -s / sdiag[r * NB + r];
-        }
-      }
-      // T_IJ = sum_{K=J}^{I-1} R_IK Y_KJ for J < I (one warp per J), into tmp[:, J*NB..]
-      for (int J = warp; J < I; J += PT / 32) {
-        double acc[4][4][2];
-        zero_acc(acc);
-        for (int K = J; K < I; K++)
-          tile_mma(acc, packed_op(L, D, i0, K * NB, false), packed_op(L, D, K * NB, J * NB, false), NB, lane);
-        acc_foreach(acc, lane, [&](int r, int c, double v) { tmp[r * ldt + J * NB + c] = v; });
-      }
-      __syncthreads();
-      // Y_IJ = -Y_II T_IJ (overwrites R_IJ), then Y_II
-      for (int J = warp; J < I; J += PT / 32) {
-        double acc[4][4][2];
-        zero_acc(acc);
-        tile_mma(acc, dense_op(sinv, NB, NB, NB, 0, 0, false), dense_op(tmp, ldt, NB, ldt, 0, J * NB, false), NB,
-                 lane);
-        acc_foreach(acc, lane, [&](int r, int c, double v) {
-          if (r < iw) L[packed_index(i0 + r, J * NB + c)] = -v;
-        });
-      }
-      for (int idx = tid; idx < iw * iw; idx += PT) {
-        int r = idx / iw, c = idx % iw;
-        if (c <= r) L[packed_index(i0 + r, i0 + c)] = sinv[r * NB + c];
-      }
-      __syncthreads();
-    }
-    // M = Y^T Y + phi phi^T, lower tiles I >= J:  Phi_IJ = sum_{K>=I} Y_KI^T Y_KJ
-    double* M = mpk + (int64_t)u * P;
-    const int ntiles = nblk * (nblk + 1) / 2;
-    for (int tix = warp; tix < ntiles; tix += PT / 32) {
-      int I = 0, base = 0;
-      while (base + I + 1 <= tix) {
-        base += I + 1;
-        I++;
-      }
-      int J = tix - base;
-      double acc[4][4][2];
-      zero_acc(acc);
-      for (int K = I; K < nblk; K++)
-        tile_mma(acc, packed_op(L, D, K * NB, I * NB, true), packed_op(L, D, K * NB, J * NB, false),
-                 min(NB, D - K * NB), lane);
-      acc_foreach(acc, lane, [&](int r, int c, double v) {
-        int gi = I * NB + r, gj = J * NB + c;
-        if (gi < D && gj <= gi) M[packed_index(gi, gj)] = (flags & TVK_POST_MOMENT) ? v + vb[gi] * vb[gj] : v;
-      });
-    }
-    __syncthreads();
+    const bool moment = (flags & TVK_POST_MOMENT) && bvec;
+    packed_inverse_from_chol(L, D, mpk + (int64_t)u * P, moment ? vb : nullptr, tmp, ldt, sdiag, sinv);
   }
 }
 
 // ------------------------------------------------------------------ row solve (update_T)
 
-__global__ void __launch_bounds__(PT, 1) spd_solve_rows_kernel(const double* apk, const double* bmat, int batch, int D,
-                                                               int R, const int32_t* skip, double* x,
-                                                               int32_t* status, double* scratch) {
+// X_c = B_c A_c^-1 via the explicit SPD inverse (Cholesky, trtri, lauum) and a tile GEMM against
+// the symmetric packed inverse: all O(D^3) work on the tensor pipe.
+__global__ void __launch_bounds__(PT, kCtasPerSm) spd_solve_rows_kernel(const double* apk, const double* bmat,
+                                                                        int batch, int D, int R,
+                                                                        const int32_t* skip, double* x,
+                                                                        int32_t* status, double* scratch) {
   extern __shared__ __align__(16) double sm[];
-  double* sdiag = sm;          // [NB*NB]
-  double* vec = sdiag + NB * NB;  // [8][D] one solve vector per warp
+  double* sdiag = sm;
+  double* sinv = sdiag + NB * NB;
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t P = packed_size(D);
-  double* W = scratch + (int64_t)blockIdx.x * P;
+  const int ldt = tmp_ld(D);
+  double* W = scratch + (int64_t)blockIdx.x * (2 * P + NB * ldt);
+  double* Winv = W + P;
+  double* tmp = Winv + P;
+  const int nblk = (D + NB - 1) / NB, rblk = (R + NB - 1) / NB;
   for (int c = blockIdx.x; c < batch; c += gridDim.x) {
     if (skip && skip[c]) {
       if (tid == 0 && status) status[c] = TVK_ITEM_SKIPPED;
@@ -335,15 +371,24 @@ __global__ void __launch_bounds__(PT, 1) spd_solve_rows_kernel(const double* apk
       continue;
     }
     if (tid == 0 && status) status[c] = TVK_ITEM_OK;
-    double* v = vec + warp * D;
-    for (int r = warp; r < R; r += PT / 32) {
-      const double* brow = bmat + ((int64_t)c * R + r) * D;
-      for (int i = lane; i < D; i += 32) v[i] = brow[i];
-      __syncwarp();
-      packed_cho_solve_warp(W, D, v, lane);
-      double* xrow = x + ((int64_t)c * R + r) * D;
-      for (int i = lane; i < D; i += 32) xrow[i] = v[i];
-      __syncwarp();
+    packed_inverse_from_chol(W, D, Winv, nullptr, tmp, ldt, sdiag, sinv);
+    // X (R x D) = B (R x D) A^-1 (D x D symmetric, packed lower)
+    const double* B = bmat + (int64_t)c * R * D;
+    double* X = x + (int64_t)c * R * D;
+    for (int tix = warp; tix < rblk * nblk; tix += PT / 32) {
+      const int I = tix / nblk, J = tix % nblk;
+      double acc[4][4][2];
+      zero_acc(acc);
+      for (int K = 0; K < nblk; K++) {
+        Opnd Bo = dense_op(B, D, R, D, I * NB, K * NB, false);
+        Opnd Ao = packed_op(Winv, D, K * NB, J * NB, false);
+        Ao.sym = true;
+        tile_mma(acc, Bo, Ao, min(NB, D - K * NB), lane);
+      }
+      acc_foreach(acc, lane, [&](int r, int cc, double val) {
+        int gi = I * NB + r, gj = J * NB + cc;
+        if (gi < R && gj < D) X[(int64_t)gi * D + gj] = val;
+      });
     }
     __syncthreads();
   }
@@ -359,21 +404,20 @@ static int resident_ctas(const void* kern, size_t smem, int items) {
   return items < g ? items : g;
 }
 
-static size_t posterior_smem(int D) {
-  int ldt = ((D + 11) / 16) * 16 + 4;
-  return sizeof(double) * ((size_t)NB * ldt + 2 * NB * NB + D);
-}
+static size_t posterior_smem(int D) { return sizeof(double) * ((size_t)2 * NB * NB + D); }
+
+static int64_t per_cta_scratch(int D) { return 2 * packed_size(D) + (int64_t)NB * tmp_ld(D); }
 
 }  // namespace tvk
 
 using namespace tvk;
 
 extern "C" int64_t tvk_posterior_workspace_bytes(int D, int batch) {
-  // only tvk_spd_solve_rows needs scratch: one packed matrix per resident CTA
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t n = batch < sms ? batch : sms;
-  return n * packed_size(D) * (int64_t)sizeof(double);
+  int64_t n = std::min<int64_t>(batch, (int64_t)sms * kCtasPerSm);
+  if (n < 1) n = 1;
+  return n * per_cta_scratch(D) * (int64_t)sizeof(double);
 }
 
 extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, int flags, double* phi,
@@ -381,7 +425,6 @@ extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, i
                              int64_t workspace_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TVK_REQUIRE(D >= 0 && D <= kPosteriorMaxD && U >= 0, "posterior: D must be in [0, 768]");
-  TVK_REQUIRE(phi != nullptr || D == 0, "posterior: phi output required");
   TVK_REQUIRE(mpk == nullptr || mpk != lpk, "posterior: Mpk must not alias Lpk (the factor is used in place)");
   if (U == 0) return TVK_OK;
   if (D == 0) {  // no latent space: prior == posterior, log|I_0| = 0
@@ -394,8 +437,11 @@ extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, i
   size_t smem = posterior_smem(D);
   cudaFuncSetAttribute(posterior_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = resident_ctas((const void*)posterior_kernel, smem, U);
-  posterior_kernel<<<grid, PT, smem, st>>>(const_cast<double*>(lpk), b, U, D, flags, phi, mpk, logdet, bphi,
-                                           status);
+  int64_t cap = workspace ? workspace_bytes / ((int64_t)NB * tmp_ld(D) * (int64_t)sizeof(double)) : 0;
+  TVK_REQUIRE(cap >= 1, "posterior: workspace too small (tvk_posterior_workspace_bytes)");
+  if (grid > cap) grid = (int)cap;
+  posterior_kernel<<<grid, PT, smem, st>>>(const_cast<double*>(lpk), b, U, D, flags, phi, mpk, logdet, bphi, status,
+                                           (double*)workspace);
   TVK_CHECK_LAUNCH("posterior");
   return TVK_OK;
 }
@@ -411,11 +457,10 @@ extern "C" int tvk_spd_solve_rows(const double* apk, const double* b, int batch,
     TVK_CHECK_LAUNCH("spd_solve_rows D=0");
     return TVK_OK;
   }
-  size_t smem = sizeof(double) * ((size_t)NB * NB + 8 * (size_t)D);
-  cudaFuncSetAttribute(spd_solve_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  size_t smem = sizeof(double) * ((size_t)2 * NB * NB);
   int grid = resident_ctas((const void*)spd_solve_rows_kernel, smem, batch);
-  int64_t cap = workspace ? workspace_bytes / (packed_size(D) * (int64_t)sizeof(double)) : 0;
-  TVK_REQUIRE(cap >= 1, "spd_solve_rows: workspace too small");
+  int64_t cap = workspace ? workspace_bytes / (per_cta_scratch(D) * (int64_t)sizeof(double)) : 0;
+  TVK_REQUIRE(cap >= 1, "spd_solve_rows: workspace too small (tvk_posterior_workspace_bytes)");
   if (grid > cap) grid = (int)cap;
   spd_solve_rows_kernel<<<grid, PT, smem, st>>>(apk, b, batch, D, R, skip, x, status, (double*)workspace);
   TVK_CHECK_LAUNCH("spd_solve_rows");
