@@ -106,7 +106,7 @@ namespace sel {
 // the per-frame top-K lists.  Two LL tile buffers let the merge of block n overlap the MMA of
 // block n+1 (named barriers FULL/EMPTY per buffer).
 constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 3;
-constexpr int NMMA = 128, NMERGE = 128, NT = NMMA + NMERGE;
+constexpr int NMMA = 128, NMERGE = 256, NT = NMMA + NMERGE;
 constexpr int BS = BN + 4;  // == 4 (mod 16): conflict-free B fragments
 constexpr int LS = BN + 1;
 using Cfg = GemmCfg<BM, BN, BK, 2, 2, NSTAGE>;  // 4 MMA warps of 32x32
