@@ -203,6 +203,7 @@ def bench_ours(args):
     full_m = pkg.GmmFull(w, mu, cov)
     n = args.frames
     x = sample_frames(w, mu, cov, n, 1000 + rank, dev)
+    log(f"[bench] rank {rank}: {n} frames generated")
     dtab, ftab = diag_m.device_table(), full_m.device_table()
     k = K_TOP
     offsets = _lib.empty((n + 1,), torch.int64)
@@ -246,6 +247,7 @@ def bench_ours(args):
     for _ in range(args.warmup):
         step()
     barrier()
+    log("[bench] warm-up done")
     clocks = Clocks(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -260,6 +262,7 @@ def bench_ours(args):
     ref_offsets = offsets.clone()
     ref_comps = comps[:entries].clone()
 
+    log(f"[bench] timed region: {ms:.1f} ms/step")
     # per-stage kernel times (CUDA events on the launching stream)
     sel = _lib.empty((n, k), torch.int32)
     sll = _lib.empty((n, k))
@@ -307,6 +310,7 @@ def bench_ours(args):
             traffic = None
     del sel, sll, gws
 
+    log("[bench] stage timing done")
     # e2e through the public API: pinned host frames -> align_frames -> host SparseAlignment
     host = torch.empty((n, F), dtype=torch.float32, pin_memory=True)
     host.copy_(x)
@@ -325,6 +329,7 @@ def bench_ours(args):
     e2e_value = world * n / e2e_s
     del host, ali
 
+    log("[bench] e2e done")
     em = None
     if args.em_utts > 0:
         em = bench_em(args, pkg, dev, rank, world, barrier, max_over_ranks)

@@ -105,7 +105,7 @@ namespace sel {
 // through a 3-stage cp.async ring of 16-deep table chunks), warps 4-7 merge the finished block into
 // the per-frame top-K lists.  Two LL tile buffers let the merge of block n overlap the MMA of
 // block n+1 (named barriers FULL/EMPTY per buffer).
-constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 3;
+constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 6;
 constexpr int NMMA = 128, NMERGE = 256, NT = NMMA + NMERGE;
 constexpr int BS = BN + 4;  // == 4 (mod 16): conflict-free B fragments
 constexpr int LS = BN + 1;
