@@ -248,15 +248,16 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
   } else {
     // ------------------------------------------------------------ merge threads (one per frame)
     const int r = tid - NMMA;
+    // KM register slots; the first KM-K hold +inf sentinels that nothing displaces, so the K live
+    // entries are v[KM-K..KM-1] and the threshold is always the static slot KM-1 (no local memory)
     double v[KM];
     int id[KM];
+    const int lead = KM - K;
 #pragma unroll
     for (int j = 0; j < KM; j++) {
-      v[j] = -INFINITY;
-      id[j] = 0x7fffffff;
+      v[j] = j < lead ? INFINITY : -INFINITY;
+      id[j] = j < lead ? -1 : 0x7fffffff;
     }
-    double wv = -INFINITY;  // current K-th entry (threshold)
-    int wi = 0x7fffffff;
     const bool live = t0 + r < T;
     for (int blk = 0; blk < nblocks; blk++) {
       const int buf = blk & 1;
@@ -266,15 +267,7 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
       if (live) {
         for (int c = 0; c < nb; c++) {
           double cv = L[c];
-          if (ranks_before(cv, n0 + c, wv, wi)) {
-            topk_insert<KM>(v, id, cv, n0 + c);
-#pragma unroll
-            for (int j = 0; j < KM; j++)
-              if (j == K - 1) {
-                wv = v[j];
-                wi = id[j];
-              }
-          }
+          if (ranks_before(cv, n0 + c, v[KM - 1], id[KM - 1])) topk_insert<KM>(v, id, cv, n0 + c);
         }
       }
       if (blk + 2 < nblocks) named_arrive(4 + buf, NT);  // EMPTY[buf]
@@ -282,9 +275,9 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
     if (live) {
 #pragma unroll
       for (int j = 0; j < KM; j++) {
-        if (j < K) {
-          lv[r * K + j] = v[j];
-          li[r * K + j] = id[j];
+        if (j >= lead) {
+          lv[r * K + (j - lead)] = v[j];
+          li[r * K + (j - lead)] = id[j];
         }
       }
     }

@@ -25,6 +25,7 @@ constexpr int GROWS = 128;      // pairs per tile
 constexpr int GT = 256;         // threads
 constexpr int GS = GP + 4;      // smem row stride (== 4 mod 16: conflict-free fragments)
 constexpr int kSortChunk = 4096;
+constexpr int64_t kGroupWindowFrames = 131072;  // 31 MB of f32 frames per window
 
 
 
@@ -151,8 +152,11 @@ __global__ void __launch_bounds__(GT) grouped_ll_kernel(const XT* x, int F, cons
   for (int i = tid; i < GROWS * GS; i += GT) sY[i] = 0.0;
   __syncthreads();
 
+  // contiguous tile range per CTA: consecutive tiles mostly share a component (P_c stays staged)
   const int64_t ntiles = (n_pairs + GROWS - 1) / GROWS;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t tile_end = min((int64_t)(blockIdx.x + 1) * per, ntiles);
+  for (int64_t tile = blockIdx.x * per; tile < tile_end; tile++) {
     const int64_t s0 = tile * GROWS;
     const int nrow = (int)((n_pairs - s0) < GROWS ? (n_pairs - s0) : GROWS);
     for (int r = tid; r < GROWS; r += GT) {
@@ -259,7 +263,9 @@ static GroupWs group_carve(void* base, int64_t n_pairs, int C) {
   return w;
 }
 
-int64_t grouped_workspace_bytes(int64_t n_pairs, int C) { return (int64_t)group_carve(nullptr, n_pairs, C).bytes; }
+int64_t grouped_workspace_bytes(int64_t n_pairs, int C) {
+  return (int64_t)group_carve(nullptr, std::min<int64_t>(n_pairs, kGroupWindowFrames * 32), C).bytes;
+}
 
 template <typename XT>
 int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, int K, const int32_t* sel,
@@ -268,26 +274,34 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
   TVK_REQUIRE(C <= 8192, "grouped full log-likelihood supports C <= 8192");
   const int64_t n_pairs = T * K;
   TVK_REQUIRE(n_pairs < (1ll << 31) - 1, "too many (frame, component) pairs for one call");
-  GroupWs w = group_carve(ws_base, n_pairs, C);
+  // frame windows sized so the window's frames and the precision table stay L2-resident while the
+  // window's pairs (sorted by component, i.e. random in frame order) gather their frame rows
+  const int64_t win = std::min<int64_t>(T, kGroupWindowFrames);
+  GroupWs w = group_carve(ws_base, win * K, C);
   TVK_REQUIRE(ws_base != nullptr && (int64_t)w.bytes <= ws_bytes, "grouped full log-likelihood: workspace too small");
-  cudaMemsetAsync(w.hist, 0, sizeof(int) * C, st);
-  int nchunks = (int)((n_pairs + kSortChunk - 1) / kSortChunk);
-  pair_hist_kernel<<<nchunks, GT, sizeof(int) * C, st>>>(sel, n_pairs, C, w.hist);
-  hist_scan_kernel<<<1, 1024, 0, st>>>(w.hist, C, w.start, w.cursor);
   size_t sc_smem = sizeof(int) * 2 * C;
   cudaFuncSetAttribute(pair_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
-  pair_scatter_kernel<<<nchunks, GT, sc_smem, st>>>(sel, n_pairs, C, w.cursor, w.sorted);
-  TVK_CHECK_LAUNCH("pair sort");
   size_t smem = sizeof(double) * (GP * GS + GROWS * GS + GP + 2 * GROWS) + sizeof(int) * 2 * GROWS;
   cudaFuncSetAttribute(grouped_ll_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, grouped_ll_kernel<XT>, GT, smem);
-  int64_t ntiles = (n_pairs + GROWS - 1) / GROWS;
-  int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * std::max(per, 1));
-  grouped_ll_kernel<XT><<<grid, GT, smem, st>>>(x, F, ptab, sel, K, w.sorted, n_pairs, sel_ll);
-  TVK_CHECK_LAUNCH("grouped_ll");
+  for (int64_t f0 = 0; f0 < T; f0 += win) {
+    const int64_t nf = std::min<int64_t>(win, T - f0);
+    const int64_t np = nf * K;
+    const int32_t* wsel = sel + f0 * K;
+    cudaMemsetAsync(w.hist, 0, sizeof(int) * C, st);
+    int nchunks = (int)((np + kSortChunk - 1) / kSortChunk);
+    pair_hist_kernel<<<nchunks, GT, sizeof(int) * C, st>>>(wsel, np, C, w.hist);
+    hist_scan_kernel<<<1, 1024, 0, st>>>(w.hist, C, w.start, w.cursor);
+    pair_scatter_kernel<<<nchunks, GT, sc_smem, st>>>(wsel, np, C, w.cursor, w.sorted);
+    TVK_CHECK_LAUNCH("pair sort");
+    int64_t ntiles = (np + GROWS - 1) / GROWS;
+    int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * std::max(per, 1));
+    grouped_ll_kernel<XT><<<grid, GT, smem, st>>>(x + f0 * F, F, ptab, wsel, K, w.sorted, np, sel_ll + f0 * K);
+    TVK_CHECK_LAUNCH("grouped_ll");
+  }
   return TVK_OK;
 }
 
