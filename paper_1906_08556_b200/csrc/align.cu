@@ -102,12 +102,11 @@ __global__ void full_table_kernel(const double* w, const double* mu, const doubl
 
 namespace sel {
 // Warp-specialized: warps 0-3 run the DMMA GEMM (64 frames x 64 components per block, K streamed
-// through a cp.async ring of 16-deep table chunks), warps 4-5 merge the finished block into the
-// per-frame top-K lists -- one thread per frame, list held in registers, branch-free insertion only
-// for candidates that beat the current K-th entry.  Two LL tile buffers let the merge of block n
-// overlap the MMA of block n+1 (named barriers FULL/EMPTY per buffer).
+// through a 3-stage cp.async ring of 16-deep table chunks), warps 4-7 merge the finished block into
+// the per-frame top-K lists.  Two LL tile buffers let the merge of block n overlap the MMA of
+// block n+1 (named barriers FULL/EMPTY per buffer).
 constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 6;
-constexpr int NMMA = 128, NMERGE = 64, NT = NMMA + NMERGE;  // one merge thread per frame
+constexpr int NMMA = 128, NMERGE = 384, NT = NMMA + NMERGE;
 constexpr int BS = BN + 4;  // == 4 (mod 16): conflict-free B fragments
 constexpr int LS = BN + 1;
 using Cfg = GemmCfg<BM, BN, BK, 2, 2, NSTAGE>;  // 4 MMA warps of 32x32
@@ -128,28 +127,7 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n));
 }
 
-template <int KM>
-__device__ __forceinline__ void topk_insert(double (&v)[KM], int (&id)[KM], double c, int ci) {
-  // new[j] = c ranks before old[j-1] ? old[j-1] : (c ranks before old[j] ? c : old[j])  (descending j)
-#pragma unroll
-  for (int j = KM - 1; j >= 1; j--) {
-    bool bp = ranks_before(c, ci, v[j - 1], id[j - 1]);
-    bool bc = ranks_before(c, ci, v[j], id[j]);
-    if (bp) {
-      v[j] = v[j - 1];
-      id[j] = id[j - 1];
-    } else if (bc) {
-      v[j] = c;
-      id[j] = ci;
-    }
-  }
-  if (ranks_before(c, ci, v[0], id[0])) {
-    v[0] = c;
-    id[0] = ci;
-  }
-}
-
-template <typename XT, int KM>
+template <typename XT>
 __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, int64_t T, int F, const double* tab,
                                                                  int C, int K, int32_t* sel_out, double* sel_val) {
   using namespace sel;
@@ -246,40 +224,55 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
     }
     cp_async_wait<0>();
   } else {
-    // ------------------------------------------------------------ merge threads (one per frame)
-    const int r = tid - NMMA;
-    // KM register slots; the first KM-K hold +inf sentinels that nothing displaces, so the K live
-    // entries are v[KM-K..KM-1] and the threshold is always the static slot KM-1 (no local memory)
-    double v[KM];
-    int id[KM];
-    const int lead = KM - K;
-#pragma unroll
-    for (int j = 0; j < KM; j++) {
-      v[j] = j < lead ? INFINITY : -INFINITY;
-      id[j] = j < lead ? -1 : 0x7fffffff;
-    }
-    const bool live = t0 + r < T;
+    // ------------------------------------------------------------ merge warps
+    const int mw = warp - NMMA / 32;
     for (int blk = 0; blk < nblocks; blk++) {
       const int buf = blk & 1;
       named_sync(2 + buf, NT);  // FULL[buf]
-      const double* L = sL + buf * BM * LS + r * LS;
+      const double* L = sL + buf * BM * LS;
       const int n0 = blk * BN, nb = min(BN, C - n0);
-      if (live) {
-        for (int c = 0; c < nb; c++) {
-          double cv = L[c];
-          if (ranks_before(cv, n0 + c, v[KM - 1], id[KM - 1])) topk_insert<KM>(v, id, cv, n0 + c);
+      for (int r = mw; r < BM; r += NMERGE / 32) {
+        if (t0 + r >= T) continue;
+        int cnt = lc[r];
+        double myv = (lane < cnt) ? lv[r * K + lane] : -INFINITY;
+        int myi = (lane < cnt) ? li[r * K + lane] : 0x7fffffff;
+        for (int base = 0; base < nb; base += 32) {
+          int ci = base + lane;
+          double cv = ci < nb ? L[r * LS + ci] : -INFINITY;
+          int gi = n0 + ci;
+          double wv = __shfl_sync(0xffffffffu, myv, K - 1);
+          int wi = __shfl_sync(0xffffffffu, myi, K - 1);
+          bool cand = ci < nb && (cnt < K || ranks_before(cv, gi, wv, wi));
+          unsigned mask = __ballot_sync(0xffffffffu, cand);
+          while (mask) {
+            int src = __ffs(mask) - 1;
+            mask &= mask - 1;
+            double v = __shfl_sync(0xffffffffu, cv, src);
+            int vi = __shfl_sync(0xffffffffu, gi, src);
+            wv = __shfl_sync(0xffffffffu, myv, K - 1);
+            wi = __shfl_sync(0xffffffffu, myi, K - 1);
+            if (cnt == K && !ranks_before(v, vi, wv, wi)) continue;
+            unsigned better = __ballot_sync(0xffffffffu, lane < cnt && ranks_before(myv, myi, v, vi));
+            int pos = __popc(better);
+            double upv = __shfl_up_sync(0xffffffffu, myv, 1);
+            int upi = __shfl_up_sync(0xffffffffu, myi, 1);
+            if (lane > pos) {
+              myv = upv;
+              myi = upi;
+            } else if (lane == pos) {
+              myv = v;
+              myi = vi;
+            }
+            cnt = min(cnt + 1, K);
+          }
         }
+        if (lane < K) {
+          lv[r * K + lane] = myv;
+          li[r * K + lane] = myi;
+        }
+        if (lane == 0) lc[r] = cnt;
       }
       if (blk + 2 < nblocks) named_arrive(4 + buf, NT);  // EMPTY[buf]
-    }
-    if (live) {
-#pragma unroll
-      for (int j = 0; j < KM; j++) {
-        if (j >= lead) {
-          lv[r * K + (j - lead)] = v[j];
-          li[r * K + (j - lead)] = id[j];
-        }
-      }
     }
   }
   __syncthreads();
@@ -589,27 +582,17 @@ extern "C" int64_t tvk_align_workspace_bytes(int64_t T, int K, int C) { return (
 
 namespace tvk {
 
-template <typename XT, int KM>
-static int launch_select_km(const XT* x, int64_t T, int F, const double* diag_table, int C, int K, int32_t* sel,
-                            double* val, cudaStream_t st) {
-  size_t smem = sel::smem_bytes(F, K);
-  TVK_REQUIRE(smem <= 227 * 1024, "align_frames: F too large for the preselection tile");
-  cudaFuncSetAttribute(select_topk_kernel<XT, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int64_t grid = (T + sel::BM - 1) / sel::BM;
-  TVK_REQUIRE(grid < (1ll << 31), "align_frames: too many frames for one call");
-  select_topk_kernel<XT, KM><<<(unsigned)grid, sel::NT, smem, st>>>(x, T, F, diag_table, C, K, sel, val);
-  TVK_CHECK_LAUNCH("select_topk");
-  return TVK_OK;
-}
-
 template <typename XT>
 static int launch_select(const XT* x, int64_t T, int F, const double* diag_table, int C, int K, int32_t* sel,
                          double* val, cudaStream_t st) {
-  if (K <= 8) return launch_select_km<XT, 8>(x, T, F, diag_table, C, K, sel, val, st);
-  if (K <= 16) return launch_select_km<XT, 16>(x, T, F, diag_table, C, K, sel, val, st);
-  if (K <= 20) return launch_select_km<XT, 20>(x, T, F, diag_table, C, K, sel, val, st);
-  if (K <= 24) return launch_select_km<XT, 24>(x, T, F, diag_table, C, K, sel, val, st);
-  return launch_select_km<XT, 32>(x, T, F, diag_table, C, K, sel, val, st);
+  size_t smem = sel::smem_bytes(F, K);
+  TVK_REQUIRE(smem <= 227 * 1024, "align_frames: F too large for the preselection tile");
+  cudaFuncSetAttribute(select_topk_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int64_t grid = (T + sel::BM - 1) / sel::BM;
+  TVK_REQUIRE(grid < (1ll << 31), "align_frames: too many frames for one call");
+  select_topk_kernel<XT><<<(unsigned)grid, sel::NT, smem, st>>>(x, T, F, diag_table, C, K, sel, val);
+  TVK_CHECK_LAUNCH("select_topk");
+  return TVK_OK;
 }
 
 template <typename XT>
