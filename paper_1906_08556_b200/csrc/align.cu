@@ -105,8 +105,8 @@ namespace sel {
 // through a 3-stage cp.async ring of 16-deep table chunks), warps 4-7 merge the finished block into
 // the per-frame top-K lists.  Two LL tile buffers let the merge of block n overlap the MMA of
 // block n+1 (named barriers FULL/EMPTY per buffer).
-constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 6;
-constexpr int NMMA = 128, NMERGE = 384, NT = NMMA + NMERGE;
+constexpr int BM = 64, BN = 64, BK = 64, NSTAGE = 2;  // long chunks: few barriers per DMMA
+constexpr int NMMA = 256, NMERGE = 384, NT = NMMA + NMERGE;  // 2 MMA warps per SMSP
 constexpr int BS = BN + 4;  // == 4 (mod 16): conflict-free B fragments
 constexpr int LS = BN + 1;
 using Cfg = GemmCfg<BM, BN, BK, 2, 2, NSTAGE>;  // 4 MMA warps of 32x32
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
 
   if (warp < NMMA / 32) {
     // ------------------------------------------------------------ MMA warps
-    const int wm = warp >> 1, wn = warp & 1;
+    const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps of 32 x 16
     const int g = lane >> 2, t = lane & 3;
     const int total = nblocks * nk;
     auto load = [&](int chunk) {
@@ -183,11 +183,11 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
     }
     int chunk = 0;
     for (int blk = 0; blk < nblocks; blk++) {
-      double acc[4][4][2];
+      double acc[4][2][2];
 #pragma unroll
       for (int i = 0; i < 4; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < 2; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
       for (int kc = 0; kc < nk; kc++, chunk++) {
         cp_async_wait<NSTAGE - 2>();
         named_sync(1, NMMA);
@@ -197,15 +197,15 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
         const double* a_s = sA + kc * BK;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-          double a[4], b[4];
+          double a[4], b[2];
 #pragma unroll
           for (int i = 0; i < 4; i++) a[i] = a_s[(wm * 32 + i * 8 + g) * AS + kk + t];
 #pragma unroll
-          for (int j = 0; j < 4; j++) b[j] = b_s[(kk + t) * BS + wn * 32 + j * 8 + g];
+          for (int j = 0; j < 2; j++) b[j] = b_s[(kk + t) * BS + wn * 16 + j * 8 + g];
 #pragma unroll
           for (int i = 0; i < 4; i++)
 #pragma unroll
-            for (int j = 0; j < 4; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            for (int j = 0; j < 2; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
       }
       const int buf = blk & 1;
@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
 #pragma unroll
       for (int i = 0; i < 4; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          int r = wm * 32 + i * 8 + g, c = wn * 32 + j * 8 + 2 * t;
+        for (int j = 0; j < 2; j++) {
+          int r = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * t;
           L[r * LS + c] = acc[i][j][0];
           L[r * LS + c + 1] = acc[i][j][1];
         }
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
 // ----------------------------------------------------------------------------- stage 2: full LL
 
 namespace fll {
-using Cfg = GemmCfg<128, 128, 16, 2, 4, 3>;
+using Cfg = GemmCfg<128, 128, 32, 2, 4, 2>;
 }
 
 // A operand: phi_k(x) = xe[i_k] * xe[j_k] with xe = [x, 1]; pairs (F,F) -> 1, (i,F) -> x_i.

@@ -104,7 +104,7 @@ __global__ void splitk_reduce(GemmArgs p) {
   }
 }
 
-using BigCfg = GemmCfg<128, 128, 16, 2, 4, 3>;
+using BigCfg = GemmCfg<128, 128, 32, 2, 4, 3>;
 using SmallCfg = GemmCfg<64, 64, 16, 2, 2, 3>;
 
 template <class Cfg, bool TA, bool TB, bool VEC>
