@@ -105,73 +105,21 @@ namespace sel {
 // through a 3-stage cp.async ring of 16-deep table chunks), warps 4-7 merge the finished block into
 // the per-frame top-K lists.  Two LL tile buffers let the merge of block n overlap the MMA of
 // block n+1 (named barriers FULL/EMPTY per buffer).
-constexpr int BM = 64, BN = 64, BK = 32, NSTAGE = 3;
-constexpr int NMMA = 256, NMERGE = 256, NT = NMMA + NMERGE;  // 2 MMA warps per SMSP
+constexpr int BM = 64, BN = 64, BK = 64, NSTAGE = 2;  // long chunks: few barriers per DMMA
+constexpr int NMMA = 256, NMERGE = 384, NT = NMMA + NMERGE;  // 2 MMA warps per SMSP
 constexpr int BS = BN + 4;  // == 4 (mod 16): conflict-free B fragments
 constexpr int LS = BN + 1;
 using Cfg = GemmCfg<BM, BN, BK, 2, 2, NSTAGE>;  // 4 MMA warps of 32x32
 __host__ __device__ inline int kpad(int F) { return ((2 * F + 1) + BK - 1) / BK * BK; }
 __host__ __device__ inline int astride(int F) { int kp = kpad(F); return kp + ((4 - kp % 16) + 16) % 16; }
 __host__ inline size_t smem_bytes(int F, int K) {
-  return sizeof(double) * ((size_t)BM * astride(F) + NSTAGE * BK * BS + 2 * BM * LS + (size_t)BM * K + BM * 32 + BM) +
-         sizeof(int) * ((size_t)BM * K + BM * 32 + 2 * BM);
+  return sizeof(double) * ((size_t)BM * astride(F) + NSTAGE * BK * BS + 2 * BM * LS + (size_t)BM * K) +
+         sizeof(int) * ((size_t)BM * K + BM);
 }
 }  // namespace sel
 
 __device__ __forceinline__ bool ranks_before(double v, int i, double w, int j) {  // (v,i) strictly better
   return v > w || (v == w && i < j);
-}
-
-// Bitonic network over the 32 lanes of a warp: (v, i) pairs sorted best-first (ranks_before order).
-__device__ __forceinline__ void warp_bitonic_sort_desc(double& v, int& i, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      double pv = __shfl_xor_sync(0xffffffffu, v, j);
-      int pi = __shfl_xor_sync(0xffffffffu, i, j);
-      bool want_better = ((lane & j) == 0) == ((lane & k) == 0);
-      bool take = want_better ? ranks_before(pv, pi, v, i) : ranks_before(v, i, pv, pi);
-      if (take) {
-        v = pv;
-        i = pi;
-      }
-    }
-  }
-}
-
-// Merge cnt buffered candidates into the best-first K-list (K <= 32); returns the new K-th entry.
-__device__ __forceinline__ void merge_candidates(const double* bvals, const int* bidx, int cnt, double* lvals,
-                                                 int* lidx, int K, int lane, double& thv, int& thi) {
-  __syncwarp();
-  double v = lane < cnt ? bvals[lane] : -INFINITY;
-  int i = lane < cnt ? bidx[lane] : 0x7fffffff;
-  warp_bitonic_sort_desc(v, i, lane);
-  double lv_ = lane < K ? lvals[lane] : -INFINITY;
-  int li_ = lane < K ? lidx[lane] : 0x7fffffff;
-  double rv = __shfl_sync(0xffffffffu, v, 31 - lane);
-  int ri = __shfl_sync(0xffffffffu, i, 31 - lane);
-  if (ranks_before(rv, ri, lv_, li_)) {  // top-32 of the union as a bitonic sequence
-    lv_ = rv;
-    li_ = ri;
-  }
-#pragma unroll
-  for (int j = 16; j > 0; j >>= 1) {  // bitonic merge, best-first
-    double pv = __shfl_xor_sync(0xffffffffu, lv_, j);
-    int pi = __shfl_xor_sync(0xffffffffu, li_, j);
-    bool take = ((lane & j) == 0) ? ranks_before(pv, pi, lv_, li_) : ranks_before(lv_, li_, pv, pi);
-    if (take) {
-      lv_ = pv;
-      li_ = pi;
-    }
-  }
-  if (lane < K) {
-    lvals[lane] = lv_;
-    lidx[lane] = li_;
-  }
-  thv = __shfl_sync(0xffffffffu, lv_, K - 1);
-  thi = __shfl_sync(0xffffffffu, li_, K - 1);
-  __syncwarp();
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
@@ -189,13 +137,9 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
   double* sA = smem;                          // [BM][AS]
   double* sB = sA + BM * AS;                  // [NSTAGE][BK][BS]
   double* sL = sB + NSTAGE * BK * BS;         // [2][BM][LS]
-  double* lv = sL + 2 * BM * LS;              // [BM][K] best-first lists
-  double* bv = lv + BM * K;                   // [BM][32] candidate buffers
-  double* tv = bv + BM * 32;                  // [BM] thresholds
-  int* li = reinterpret_cast<int*>(tv + BM);  // [BM][K]
-  int* bi = li + BM * K;                      // [BM][32]
-  int* ti = bi + BM * 32;                     // [BM]
-  int* lc = ti + BM;                          // [BM] buffered candidate counts
+  double* lv = sL + 2 * BM * LS;              // [BM][K]
+  int* li = reinterpret_cast<int*>(lv + BM * K);  // [BM][K]
+  int* lc = li + BM * K;                      // [BM]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t t0 = (int64_t)blockIdx.x * BM;
   const int nblocks = (C + BN - 1) / BN, nk = KP / BK;
@@ -215,15 +159,7 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
     }
     sA[r * AS + k] = v;
   }
-  for (int r = tid; r < BM; r += NT) {
-    lc[r] = 0;
-    tv[r] = -INFINITY;
-    ti[r] = 0x7fffffff;
-  }
-  for (int idx = tid; idx < BM * K; idx += NT) {
-    lv[idx] = -INFINITY;
-    li[idx] = 0x7fffffff;
-  }
+  for (int r = tid; r < BM; r += NT) lc[r] = 0;
   __syncthreads();
 
   if (warp < NMMA / 32) {
@@ -288,10 +224,7 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
     }
     cp_async_wait<0>();
   } else {
-    // ------------------------------------------------------------ merge warps (warp per frame)
-    // Buffered top-K: candidates that beat the frame's current K-th entry are appended to a 32-slot
-    // buffer (ballot + popc, no sorting); a full buffer is bitonic-sorted and bitonic-merged into the
-    // K-list, which raises the threshold.  ~5 merges per frame instead of ~100 single insertions.
+    // ------------------------------------------------------------ merge warps
     const int mw = warp - NMMA / 32;
     for (int blk = 0; blk < nblocks; blk++) {
       const int buf = blk & 1;
@@ -300,44 +233,46 @@ __global__ void __launch_bounds__(sel::NT, 1) select_topk_kernel(const XT* x, in
       const int n0 = blk * BN, nb = min(BN, C - n0);
       for (int r = mw; r < BM; r += NMERGE / 32) {
         if (t0 + r >= T) continue;
-        double thv = tv[r];
-        int thi = ti[r];
         int cnt = lc[r];
+        double myv = (lane < cnt) ? lv[r * K + lane] : -INFINITY;
+        int myi = (lane < cnt) ? li[r * K + lane] : 0x7fffffff;
         for (int base = 0; base < nb; base += 32) {
           int ci = base + lane;
           double cv = ci < nb ? L[r * LS + ci] : -INFINITY;
           int gi = n0 + ci;
-          bool pass = ci < nb && ranks_before(cv, gi, thv, thi);
-          unsigned m = __ballot_sync(0xffffffffu, pass);
-          if (!m) continue;
-          if (cnt + __popc(m) > 32) {
-            merge_candidates(bv + r * 32, bi + r * 32, cnt, lv + r * K, li + r * K, K, lane, thv, thi);
-            cnt = 0;
-            pass = pass && ranks_before(cv, gi, thv, thi);
-            m = __ballot_sync(0xffffffffu, pass);
+          double wv = __shfl_sync(0xffffffffu, myv, K - 1);
+          int wi = __shfl_sync(0xffffffffu, myi, K - 1);
+          bool cand = ci < nb && (cnt < K || ranks_before(cv, gi, wv, wi));
+          unsigned mask = __ballot_sync(0xffffffffu, cand);
+          while (mask) {
+            int src = __ffs(mask) - 1;
+            mask &= mask - 1;
+            double v = __shfl_sync(0xffffffffu, cv, src);
+            int vi = __shfl_sync(0xffffffffu, gi, src);
+            wv = __shfl_sync(0xffffffffu, myv, K - 1);
+            wi = __shfl_sync(0xffffffffu, myi, K - 1);
+            if (cnt == K && !ranks_before(v, vi, wv, wi)) continue;
+            unsigned better = __ballot_sync(0xffffffffu, lane < cnt && ranks_before(myv, myi, v, vi));
+            int pos = __popc(better);
+            double upv = __shfl_up_sync(0xffffffffu, myv, 1);
+            int upi = __shfl_up_sync(0xffffffffu, myi, 1);
+            if (lane > pos) {
+              myv = upv;
+              myi = upi;
+            } else if (lane == pos) {
+              myv = v;
+              myi = vi;
+            }
+            cnt = min(cnt + 1, K);
           }
-          if (pass) {
-            int pos = cnt + __popc(m & ((1u << lane) - 1));
-            bv[r * 32 + pos] = cv;
-            bi[r * 32 + pos] = gi;
-          }
-          cnt += __popc(m);
-          __syncwarp();
         }
-        if (lane == 0) {
-          lc[r] = cnt;
-          tv[r] = thv;
-          ti[r] = thi;
+        if (lane < K) {
+          lv[r * K + lane] = myv;
+          li[r * K + lane] = myi;
         }
-        __syncwarp();
+        if (lane == 0) lc[r] = cnt;
       }
       if (blk + 2 < nblocks) named_arrive(4 + buf, NT);  // EMPTY[buf]
-    }
-    for (int r = mw; r < BM; r += NMERGE / 32) {  // flush the remaining candidates
-      if (t0 + r >= T) continue;
-      double thv;
-      int thi;
-      merge_candidates(bv + r * 32, bi + r * 32, lc[r], lv + r * K, li + r * K, K, lane, thv, thi);
     }
   }
   __syncthreads();
