@@ -303,8 +303,10 @@ def bench_ours(args):
     prof = os.path.join(REPO, "profiles", "r01_ncu_summary.json")
     traffic = None
     if os.path.exists(prof):
-        try:
-            per_frame = json.load(open(prof))["select_topk"]["dram_bytes_per_frame"]
+        try:  # DRAM bytes/frame of the dominant kernel from the committed ncu --set full capture
+            reps = json.load(open(prof))["reports"]
+            per_frame = [k["dram_bytes_per_frame"] for r in reps.values() for k in r
+                         if k["kernel"].startswith("tvk::select_topk") and "dram_bytes_per_frame" in k][0]
             traffic = per_frame * n
         except Exception:
             traffic = None
