@@ -165,7 +165,7 @@ int64_t tvk_posterior_workspace_bytes(int D, int batch);
 
 /* Batched latent posterior (tvm.py:183-215) from packed precisions (factored in place):
  *   L_u = Lpk[u] (+ I);  R R^T = L_u (Cholesky);  phi_u = L_u^-1 b_u;
- *   Mpk[u] = packed(L_u^-1 [+ phi_u phi_u^T]) (must not alias Lpk);  logdet[u] = log|L_u|;
+ *   Mpk[u] = packed(L_u^-1 [+ phi_u phi_u^T]) (may alias Lpk: computed in place);  logdet[u] = log|L_u|;
  *   bphi[u] = b_u . phi_u.   Any output pointer except phi may be NULL.
  * status[u] = TVK_ITEM_NOT_SPD when L_u is not positive definite. */
 int tvk_posterior(const double* lpk, const double* b, int U, int D, int flags, double* phi, double* mpk,

@@ -167,15 +167,13 @@ def posterior_batch(dm: DeviceModel, ws: Workspace, n, fm, want_moment=True, sta
     work = _lib.empty((splits * Ub * D,)) if splits > 1 else None
     dgemm(fm, ws.W, b, Ub, D, K, beta=1.0, splits=splits, work=work)  # b = p e1 + sum_c W_c' f_c
     phi = _lib.empty((Ub, D))
-    Mpk = _lib.empty((Ub, P)) if want_moment else None
+    Mpk = Lpk if want_moment else None  # factored in place: M overwrites L (L2-resident working set)
     logdet = _lib.empty((Ub,))
     bphi = _lib.empty((Ub,))
     status = status_out if status_out is not None else _lib.empty((Ub,), torch.int32)
     flags = POST_ADD_IDENTITY | (0 if covariance else POST_MOMENT)
-    ws_bytes = int(_lib.load().tvk_posterior_workspace_bytes(D, Ub))
-    scratch = _lib.empty((max(ws_bytes // 8, 1),))
     call("tvk_posterior", ptr(Lpk), ptr(b), Ub, D, flags, ptr(phi), ptr(Mpk), ptr(logdet), ptr(bphi), ptr(status),
-         ptr(scratch), ws_bytes, stream())
+         None, 0, stream())
     return phi, Mpk, logdet, bphi, status, b
 
 

@@ -1,15 +1,15 @@
 // Batched SPD factor / inverse / solve for the i-vector posterior (tvm.py:183-215) and the
 // T update (tvm.py:317-334), on packed-lower D x D matrices (D = 400 at the configs).
 //
-// One CTA per matrix (persistent over the batch), 8 warps.  Blocked right-looking Cholesky
-// in place on the packed storage with 32-wide panels; every O(D^3) part is a 32x32x32 tile
-// product on the FP64 tensor pipe (DMMA.8x8x4) whose fragments are loaded straight from the
-// (L2-resident) packed matrix:
-//   potrf  : diag block in shared memory, panel TRSM row-parallel, trailing SYRK as tile MMAs
-//   trtri  : Y = R^-1 row block by row block (T_IJ = sum_K R_IK Y_KJ staged in shared memory)
-//   lauum  : Phi = Y^T Y tile MMAs, epilogue adds phi phi^T and writes the packed moment
-//            M = Phi + phi phi^T that the A-accumulation GEMM consumes (tvm.py:298-301)
-//   solves : phi = L^-1 b by forward/backward substitution with R (cho_solve semantics).
+// One CTA (8 warps) per SM, persistent over the batch, one matrix at a time, factored IN PLACE so
+// that the 148 resident matrices (148 x 642 KB) stay L2-resident.  Every O(D^3) part is a
+// 32x32x32 tile product on the FP64 tensor pipe (DMMA.8x8x4), fragments loaded from L2:
+//   potrf : 32x32 diagonal block by one warp in shared memory, panel TRSM row-parallel,
+//           trailing SYRK tile-parallel;
+//   trtri : Y = R^-1 row block by row block, T_IJ = sum_K R_IK Y_KJ staged in shared memory;
+//   phi   : phi = Y^T (Y b) (two triangular mat-vecs: L^-1 b without a sequential solve);
+//   lauum : M = Y^T Y (+ phi phi^T) row block by row block, in place (diagonal tile staged),
+//           i.e. the packed moment the A-accumulation GEMM consumes (tvm.py:298-301).
 #include <math.h>
 
 #include "common.cuh"
@@ -18,9 +18,9 @@
 
 namespace tvk {
 
-constexpr int PT = 128;  // threads per CTA (4 warps; 4 CTAs per SM overlap the serial panel phases)
+constexpr int PT = 256;  // threads per CTA (8 warps), one CTA per SM
+constexpr int NW = PT / 32;
 constexpr int NB = 32;   // panel / tile width
-constexpr int kCtasPerSm = 4;
 constexpr int kPosteriorMaxD = 768;
 
 struct Opnd {
@@ -75,12 +75,12 @@ __device__ __forceinline__ double ld_elem(const Opnd& o, int r, int c) {
 // acc(32x32) += A(32 x klen) * B(klen x 32); A logical (i,k), B logical (k,j).
 __device__ __forceinline__ void tile_mma(double (&acc)[4][4][2], const Opnd& A, const Opnd& B, int klen, int lane) {
   const int g = lane >> 2, t = lane & 3;
-  // two k-steps of fragments in flight (16 loads) per 32 MMAs: bounded registers, 4 CTAs/SM
+  // four k-steps of fragments in flight (32 loads) per 64 MMAs
 #pragma unroll 1
-  for (int ks0 = 0; ks0 < 8; ks0 += 2) {
-    double a[2][4], b[2][4];
+  for (int ks0 = 0; ks0 < 8; ks0 += 4) {
+    double a[4][4], b[4][4];
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
+    for (int h = 0; h < 4; h++) {
       int k = (ks0 + h) * 4 + t;
       bool kin = k < klen;
 #pragma unroll
@@ -96,7 +96,7 @@ __device__ __forceinline__ void tile_mma(double (&acc)[4][4][2], const Opnd& A, 
       }
     }
 #pragma unroll
-    for (int h = 0; h < 2; h++)
+    for (int h = 0; h < 4; h++)
 #pragma unroll
       for (int fi = 0; fi < 4; fi++)
 #pragma unroll
@@ -125,27 +125,47 @@ __device__ __forceinline__ void acc_foreach(const double (&acc)[4][4][2], int la
 
 // ------------------------------------------------------------------ blocked Cholesky (in place, packed)
 
+// n x n (n <= 32) lower Cholesky of the shared-memory block a (row stride n) by warp 0 alone.
+__device__ void warp_cholesky(double* a, int n, int* bad, int lane) {
+  for (int k = 0; k < n; k++) {
+    if (lane == 0) {
+      double d = a[k * n + k];
+      if (!(d > 0.0)) *bad = 1;
+      else a[k * n + k] = sqrt(d);
+    }
+    __syncwarp();
+    if (*bad) return;
+    const double piv = a[k * n + k];
+    if (lane > k && lane < n) a[lane * n + k] /= piv;
+    __syncwarp();
+    if (lane > k && lane < n) {
+      const double lik = a[lane * n + k];
+      for (int j = k + 1; j <= lane; j++) a[lane * n + j] -= lik * a[j * n + k];
+    }
+    __syncwarp();
+  }
+}
+
 // Returns false (uniformly across the CTA) if the matrix is not positive definite.
 __device__ bool packed_cholesky(double* P, int n, double* sdiag /* NB*NB */, int* bad) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nblk = (n + NB - 1) / NB;
   for (int kb = 0; kb < nblk; kb++) {
     const int k0 = kb * NB, kw = min(NB, n - k0);
-    // (1) factor the diagonal block in shared memory
     for (int idx = tid; idx < kw * kw; idx += PT) {
       int r = idx / kw, c = idx % kw;
       sdiag[idx] = c <= r ? P[packed_index(k0 + r, k0 + c)] : 0.0;
     }
     if (tid == 0) *bad = 0;
     __syncthreads();
-    block_cholesky(sdiag, kw, bad);
+    if (warp == 0) warp_cholesky(sdiag, kw, bad, lane);
     __syncthreads();
     if (*bad) return false;
     for (int idx = tid; idx < kw * kw; idx += PT) {
       int r = idx / kw, c = idx % kw;
       if (c <= r) P[packed_index(k0 + r, k0 + c)] = sdiag[idx];
     }
-    // (2) panel: rows below, X = W R_kk^-T (row-parallel forward substitution)
+    // panel: rows below, X = W R_kk^-T (row-parallel forward substitution)
     for (int i = k0 + kw + tid; i < n; i += PT) {
       double* row = P + packed_index(i, k0);
       double x[NB];
@@ -165,10 +185,10 @@ __device__ bool packed_cholesky(double* P, int n, double* sdiag /* NB*NB */, int
         if (j < kw) row[j] = x[j];
     }
     __syncthreads();
-    // (3) trailing update of the lower triangle: C_IJ -= P_I P_J^T, tiles I >= J > kb
+    // trailing update of the lower triangle: C_IJ -= P_I P_J^T, tiles I >= J > kb
     const int nt = nblk - kb - 1;
     const int ntiles = nt * (nt + 1) / 2;
-    for (int tix = warp; tix < ntiles; tix += PT / 32) {
+    for (int tix = warp; tix < ntiles; tix += NW) {
       int I = 0, base = 0;
       while (base + I + 1 <= tix) {
         base += I + 1;
@@ -189,33 +209,13 @@ __device__ bool packed_cholesky(double* P, int n, double* sdiag /* NB*NB */, int
   return true;
 }
 
-// forward R z = b then backward R^T x = z (warp 0), z/x in shared memory (in place in v)
-__device__ void packed_cho_solve_warp(const double* P, int n, double* v, int lane) {
-  for (int i = 0; i < n; i++) {
-    const double* row = P + packed_index(i, 0);
-    double s = 0.0;
-    for (int j = lane; j < i; j += 32) s += row[j] * v[j];
-    s = warp_sum(s);
-    if (lane == 0) v[i] = (v[i] - s) / row[i];
-    __syncwarp();
-  }
-  for (int i = n - 1; i >= 0; i--) {
-    const double* row = P + packed_index(i, 0);
-    double xi = v[i] / row[i];
-    __syncwarp();
-    for (int j = lane; j < i; j += 32) v[j] -= row[j] * xi;
-    if (lane == 0) v[i] = xi;
-    __syncwarp();
-  }
-}
-
 // ------------------------------------------------------------------ SPD inverse (trtri + lauum)
 
-// After packed_cholesky: L holds R (lower).  Overwrites L with Y = R^-1 (row block by row block:
-// Y_IJ = -Y_II sum_{K=J}^{I-1} R_IK Y_KJ, staged through the per-CTA scratch `tmp` [NB][ldt]) and
-// writes M = Y^T Y (= (R R^T)^-1) (+ v v^T if v != NULL) packed into M.
-__device__ void packed_inverse_from_chol(double* L, int D, double* M, const double* v, double* tmp, int ldt,
-                                        double* sdiag, double* sinv) {
+__host__ __device__ inline int tmp_ld(int D) { return ((D + 11) / 16) * 16 + 4; }  // == 4 (mod 16)
+
+// After packed_cholesky (L holds R): overwrite L with Y = R^-1 (row block by row block:
+// Y_IJ = -Y_II sum_{K=J}^{I-1} R_IK Y_KJ with T_IJ staged in the shared `tmp` [NB][ldt]).
+__device__ void packed_trtri(double* L, int D, double* tmp, int ldt, double* sdiag, double* sinv) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nblk = (D + NB - 1) / NB;
   for (int I = 0; I < nblk; I++) {
@@ -225,16 +225,18 @@ __device__ void packed_inverse_from_chol(double* L, int D, double* M, const doub
       sdiag[idx] = (r < iw && c <= r) ? L[packed_index(i0 + r, i0 + c)] : (r == c ? 1.0 : 0.0);
     }
     __syncthreads();
-    for (int j = tid; j < NB; j += PT) {  // column j of Y_II (forward substitution)
+    if (warp == NW - 1) {  // Y_II = R_II^-1, lane = column (forward substitution)
+      const int j = lane;
       for (int r = 0; r < j; r++) sinv[r * NB + j] = 0.0;
       sinv[j * NB + j] = 1.0 / sdiag[j * NB + j];
       for (int r = j + 1; r < NB; r++) {
-        double s = 0.0;
-        for (int k = j; k < r; k++) s += sdiag[r * NB + k] * sinv[k * NB + j];
-        sinv[r * NB + j] = -s / sdiag[r * NB + r];
+        double acc = 0.0;
+        for (int k = j; k < r; k++) acc += sdiag[r * NB + k] * sinv[k * NB + j];
+        sinv[r * NB + j] = -acc / sdiag[r * NB + r];
       }
     }
-    for (int J = warp; J < I; J += PT / 32) {  // T_IJ = sum_{K=J}^{I-1} R_IK Y_KJ
+    for (int J = warp; J < I; J += NW - 1) {  // T_IJ = sum_{K=J}^{I-1} R_IK Y_KJ  (warps 0..NW-2)
+      if (warp == NW - 1) break;
       double acc[4][4][2];
       zero_acc(acc);
       for (int K = J; K < I; K++)
@@ -242,7 +244,7 @@ __device__ void packed_inverse_from_chol(double* L, int D, double* M, const doub
       acc_foreach(acc, lane, [&](int r, int c, double val) { tmp[r * ldt + J * NB + c] = val; });
     }
     __syncthreads();
-    for (int J = warp; J < I; J += PT / 32) {  // Y_IJ = -Y_II T_IJ (overwrites R_IJ)
+    for (int J = warp; J < I; J += NW) {  // Y_IJ = -Y_II T_IJ (overwrites R_IJ)
       double acc[4][4][2];
       zero_acc(acc);
       tile_mma(acc, dense_op(sinv, NB, NB, NB, 0, 0, false), dense_op(tmp, ldt, NB, ldt, 0, J * NB, false), NB, lane);
@@ -256,42 +258,52 @@ __device__ void packed_inverse_from_chol(double* L, int D, double* M, const doub
     }
     __syncthreads();
   }
-  // M_IJ = sum_{K>=I} Y_KI^T Y_KJ (+ v_i v_j), lower tiles I >= J
-  const int ntiles = nblk * (nblk + 1) / 2;
-  for (int tix = warp; tix < ntiles; tix += PT / 32) {
-    int I = 0, base = 0;
-    while (base + I + 1 <= tix) {
-      base += I + 1;
-      I++;
-    }
-    int J = tix - base;
-    double acc[4][4][2];
-    zero_acc(acc);
-    for (int K = I; K < nblk; K++)
-      tile_mma(acc, packed_op(L, D, K * NB, I * NB, true), packed_op(L, D, K * NB, J * NB, false),
-               min(NB, D - K * NB), lane);
-    acc_foreach(acc, lane, [&](int r, int c, double val) {
-      int gi = I * NB + r, gj = J * NB + c;
-      if (gi < D && gj <= gi) M[packed_index(gi, gj)] = v ? val + v[gi] * v[gj] : val;
-    });
-  }
-  __syncthreads();
 }
 
-__host__ __device__ inline int tmp_ld(int D) { return ((D + 11) / 16) * 16 + 4; }  // == 4 (mod 16)
+// M = Y^T Y (+ v v^T) written over Y (M may alias L): row block I ascending; the off-diagonal tiles
+// of row I only read rows K >= I and their own slot, the diagonal tile (which every tile of the
+// row reads through the K = I term) is staged in `dtmp` and stored after the row completes.
+__device__ void packed_lauum(double* L, int D, double* M, const double* v, double* dtmp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nblk = (D + NB - 1) / NB;
+  for (int I = 0; I < nblk; I++) {
+    for (int J = warp; J <= I; J += NW) {
+      double acc[4][4][2];
+      zero_acc(acc);
+      for (int K = I; K < nblk; K++)
+        tile_mma(acc, packed_op(L, D, K * NB, I * NB, true), packed_op(L, D, K * NB, J * NB, false),
+                 min(NB, D - K * NB), lane);
+      acc_foreach(acc, lane, [&](int r, int c, double val) {
+        int gi = I * NB + r, gj = J * NB + c;
+        if (gi >= D || gj > gi) return;
+        double out = v ? val + v[gi] * v[gj] : val;
+        if (J == I) dtmp[r * NB + c] = out;
+        else M[packed_index(gi, gj)] = out;
+      });
+    }
+    __syncthreads();
+    for (int idx = tid; idx < NB * NB; idx += PT) {
+      int r = idx / NB, c = idx % NB, gi = I * NB + r, gj = I * NB + c;
+      if (gi < D && c <= r) M[packed_index(gi, gj)] = dtmp[idx];
+    }
+    __syncthreads();
+  }
+}
 
 // ------------------------------------------------------------------ posterior kernel
 
-__global__ void __launch_bounds__(PT, kCtasPerSm) posterior_kernel(double* lpk, const double* bvec, int U, int D,
-                                                                   int flags, double* phi_out, double* mpk,
-                                                                   double* logdet_out, double* bphi_out,
-                                                                   int32_t* status, double* scratch) {
+__global__ void __launch_bounds__(PT, 1) posterior_kernel(double* lpk, const double* bvec, int U, int D, int flags,
+                                                          double* phi_out, double* mpk, double* logdet_out,
+                                                          double* bphi_out, int32_t* status) {
   extern __shared__ __align__(16) double sm[];
   const int ldt = tmp_ld(D);
-  double* tmp = scratch + (int64_t)blockIdx.x * NB * ldt;  // [NB][ldt] (L2-resident)
-  double* sdiag = sm;                                      // [NB*NB]
-  double* sinv = sdiag + NB * NB;                          // [NB*NB]
-  double* vb = sinv + NB * NB;                             // [D]  phi
+  double* tmp = sm;                 // [NB][ldt]
+  double* sdiag = tmp + NB * ldt;   // [NB*NB]
+  double* sinv = sdiag + NB * NB;   // [NB*NB]
+  double* dtmp = sinv + NB * NB;    // [NB*NB]
+  double* vb = dtmp + NB * NB;      // [D] b, then phi
+  double* vz = vb + D;              // [D] Y b
+  double* vp = vz + D;              // [D] phi
   __shared__ int bad;
   __shared__ double red;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -307,26 +319,33 @@ __global__ void __launch_bounds__(PT, kCtasPerSm) posterior_kernel(double* lpk, 
       continue;
     }
     if (tid == 0 && status) status[u] = TVK_ITEM_OK;
-    // log|L| and phi = L^-1 b (cho_solve)
     if (warp == 0) {
       double s = 0.0;
       for (int i = lane; i < D; i += 32) s += log(L[packed_index(i, i)]);
       s = warp_sum(s);
       if (lane == 0) red = 2.0 * s;
     }
-    if (bvec) {
-      for (int i = tid; i < D; i += PT) vb[i] = bvec[(int64_t)u * D + i];
-      __syncthreads();
-      if (warp == 0) packed_cho_solve_warp(L, D, vb, lane);
-      __syncthreads();
-      if (phi_out)
-        for (int i = tid; i < D; i += PT) phi_out[(int64_t)u * D + i] = vb[i];
+    for (int i = tid; i < D; i += PT) vb[i] = bvec ? bvec[(int64_t)u * D + i] : 0.0;
+    packed_trtri(L, D, tmp, ldt, sdiag, sinv);  // L <- Y = R^-1 (syncs inside)
+    // phi = Y^T (Y b): z_i = sum_{j<=i} Y_ij b_j (rows), phi_j = sum_{i>=j} Y_ij z_i (columns)
+    for (int i = warp; i < D; i += NW) {
+      const double* row = L + packed_index(i, 0);
+      double s = 0.0;
+      for (int j = lane; j <= i; j += 32) s += row[j] * vb[j];
+      s = warp_sum(s);
+      if (lane == 0) vz[i] = s;
     }
     __syncthreads();
-    if (warp == 1 && (bphi_out || logdet_out)) {
+    for (int j = tid; j < D; j += PT) {
       double s = 0.0;
-      if (bvec)
-        for (int i = lane; i < D; i += 32) s += bvec[(int64_t)u * D + i] * vb[i];
+      for (int i = j; i < D; i++) s += L[packed_index(i, j)] * vz[i];
+      if (phi_out) phi_out[(int64_t)u * D + j] = s;
+      vp[j] = s;
+    }
+    __syncthreads();
+    if (warp == 0 && (bphi_out || logdet_out)) {
+      double s = 0.0;
+      for (int i = lane; i < D; i += 32) s += vb[i] * vp[i];
       s = warp_sum(s);
       if (lane == 0) {
         if (bphi_out) bphi_out[u] = s;
@@ -335,28 +354,27 @@ __global__ void __launch_bounds__(PT, kCtasPerSm) posterior_kernel(double* lpk, 
     }
     if (mpk == nullptr) continue;
     const bool moment = (flags & TVK_POST_MOMENT) && bvec;
-    packed_inverse_from_chol(L, D, mpk + (int64_t)u * P, moment ? vb : nullptr, tmp, ldt, sdiag, sinv);
+    packed_lauum(L, D, mpk + (int64_t)u * P, moment ? vp : nullptr, dtmp);
   }
 }
 
 // ------------------------------------------------------------------ row solve (update_T)
 
-// X_c = B_c A_c^-1 via the explicit SPD inverse (Cholesky, trtri, lauum) and a tile GEMM against
-// the symmetric packed inverse: all O(D^3) work on the tensor pipe.
-__global__ void __launch_bounds__(PT, kCtasPerSm) spd_solve_rows_kernel(const double* apk, const double* bmat,
-                                                                        int batch, int D, int R,
-                                                                        const int32_t* skip, double* x,
-                                                                        int32_t* status, double* scratch) {
+// X_c = B_c A_c^-1 via the explicit SPD inverse (Cholesky, trtri, lauum in place on a scratch copy)
+// and a tile GEMM against the symmetric packed inverse: all O(D^3) work on the tensor pipe.
+__global__ void __launch_bounds__(PT, 1) spd_solve_rows_kernel(const double* apk, const double* bmat, int batch,
+                                                               int D, int R, const int32_t* skip, double* x,
+                                                               int32_t* status, double* scratch) {
   extern __shared__ __align__(16) double sm[];
-  double* sdiag = sm;
+  const int ldt = tmp_ld(D);
+  double* tmp = sm;
+  double* sdiag = tmp + NB * ldt;
   double* sinv = sdiag + NB * NB;
+  double* dtmp = sinv + NB * NB;
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t P = packed_size(D);
-  const int ldt = tmp_ld(D);
-  double* W = scratch + (int64_t)blockIdx.x * (2 * P + NB * ldt);
-  double* Winv = W + P;
-  double* tmp = Winv + P;
+  double* W = scratch + (int64_t)blockIdx.x * P;
   const int nblk = (D + NB - 1) / NB, rblk = (R + NB - 1) / NB;
   for (int c = blockIdx.x; c < batch; c += gridDim.x) {
     if (skip && skip[c]) {
@@ -371,17 +389,17 @@ __global__ void __launch_bounds__(PT, kCtasPerSm) spd_solve_rows_kernel(const do
       continue;
     }
     if (tid == 0 && status) status[c] = TVK_ITEM_OK;
-    packed_inverse_from_chol(W, D, Winv, nullptr, tmp, ldt, sdiag, sinv);
-    // X (R x D) = B (R x D) A^-1 (D x D symmetric, packed lower)
+    packed_trtri(W, D, tmp, ldt, sdiag, sinv);
+    packed_lauum(W, D, W, nullptr, dtmp);  // W <- A^-1 (packed)
     const double* B = bmat + (int64_t)c * R * D;
     double* X = x + (int64_t)c * R * D;
-    for (int tix = warp; tix < rblk * nblk; tix += PT / 32) {
+    for (int tix = warp; tix < rblk * nblk; tix += NW) {
       const int I = tix / nblk, J = tix % nblk;
       double acc[4][4][2];
       zero_acc(acc);
       for (int K = 0; K < nblk; K++) {
         Opnd Bo = dense_op(B, D, R, D, I * NB, K * NB, false);
-        Opnd Ao = packed_op(Winv, D, K * NB, J * NB, false);
+        Opnd Ao = packed_op(W, D, K * NB, J * NB, false);
         Ao.sym = true;
         tile_mma(acc, Bo, Ao, min(NB, D - K * NB), lane);
       }
@@ -394,30 +412,25 @@ __global__ void __launch_bounds__(PT, kCtasPerSm) spd_solve_rows_kernel(const do
   }
 }
 
-static int resident_ctas(const void* kern, size_t smem, int items) {
-  int dev = 0, sms = 148, per = 1;
+static int resident_ctas(int items) {
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, PT, smem);
-  if (per < 1) per = 1;
-  int g = sms * per;
-  return items < g ? items : g;
+  return items < sms ? items : sms;
 }
 
-static size_t posterior_smem(int D) { return sizeof(double) * ((size_t)2 * NB * NB + D); }
-
-static int64_t per_cta_scratch(int D) { return 2 * packed_size(D) + (int64_t)NB * tmp_ld(D); }
+static size_t kernel_smem(int D) { return sizeof(double) * ((size_t)NB * tmp_ld(D) + 3 * NB * NB + 3 * (size_t)D); }
 
 }  // namespace tvk
 
 using namespace tvk;
 
 extern "C" int64_t tvk_posterior_workspace_bytes(int D, int batch) {
+  // tvk_spd_solve_rows: one packed matrix per resident CTA; tvk_posterior needs none
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t n = std::min<int64_t>(batch, (int64_t)sms * kCtasPerSm);
-  if (n < 1) n = 1;
-  return n * per_cta_scratch(D) * (int64_t)sizeof(double);
+  int64_t n = std::min<int64_t>(std::max(batch, 1), sms);
+  return n * packed_size(D) * (int64_t)sizeof(double);
 }
 
 extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, int flags, double* phi,
@@ -425,7 +438,6 @@ extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, i
                              int64_t workspace_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TVK_REQUIRE(D >= 0 && D <= kPosteriorMaxD && U >= 0, "posterior: D must be in [0, 768]");
-  TVK_REQUIRE(mpk == nullptr || mpk != lpk, "posterior: Mpk must not alias Lpk (the factor is used in place)");
   if (U == 0) return TVK_OK;
   if (D == 0) {  // no latent space: prior == posterior, log|I_0| = 0
     if (logdet) cudaMemsetAsync(logdet, 0, sizeof(double) * U, st);
@@ -434,14 +446,11 @@ extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, i
     TVK_CHECK_LAUNCH("posterior D=0");
     return TVK_OK;
   }
-  size_t smem = posterior_smem(D);
+  size_t smem = kernel_smem(D);
+  TVK_REQUIRE(smem <= 227 * 1024, "posterior: D too large for the shared-memory panel");
   cudaFuncSetAttribute(posterior_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int grid = resident_ctas((const void*)posterior_kernel, smem, U);
-  int64_t cap = workspace ? workspace_bytes / ((int64_t)NB * tmp_ld(D) * (int64_t)sizeof(double)) : 0;
-  TVK_REQUIRE(cap >= 1, "posterior: workspace too small (tvk_posterior_workspace_bytes)");
-  if (grid > cap) grid = (int)cap;
-  posterior_kernel<<<grid, PT, smem, st>>>(const_cast<double*>(lpk), b, U, D, flags, phi, mpk, logdet, bphi, status,
-                                           (double*)workspace);
+  posterior_kernel<<<resident_ctas(U), PT, smem, st>>>(const_cast<double*>(lpk), b, U, D, flags, phi, mpk, logdet,
+                                                        bphi, status);
   TVK_CHECK_LAUNCH("posterior");
   return TVK_OK;
 }
@@ -457,9 +466,11 @@ extern "C" int tvk_spd_solve_rows(const double* apk, const double* b, int batch,
     TVK_CHECK_LAUNCH("spd_solve_rows D=0");
     return TVK_OK;
   }
-  size_t smem = sizeof(double) * ((size_t)2 * NB * NB);
-  int grid = resident_ctas((const void*)spd_solve_rows_kernel, smem, batch);
-  int64_t cap = workspace ? workspace_bytes / (per_cta_scratch(D) * (int64_t)sizeof(double)) : 0;
+  size_t smem = kernel_smem(D);
+  TVK_REQUIRE(smem <= 227 * 1024, "spd_solve_rows: D too large for the shared-memory panel");
+  cudaFuncSetAttribute(spd_solve_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int grid = resident_ctas(batch);
+  int64_t cap = workspace ? workspace_bytes / (packed_size(D) * (int64_t)sizeof(double)) : 0;
   TVK_REQUIRE(cap >= 1, "spd_solve_rows: workspace too small (tvk_posterior_workspace_bytes)");
   if (grid > cap) grid = (int)cap;
   spd_solve_rows_kernel<<<grid, PT, smem, st>>>(apk, b, batch, D, R, skip, x, status, (double*)workspace);
