@@ -81,8 +81,12 @@ int tvk_spd_small(const double* a, int batch, int n, double* chol, double* inv, 
 
 /* ---------------------------------------------------------------- frame posteriors */
 
-/* Diagonal-model coefficient table (2F+1) x C such that for frame x the diagonal
- * log-likelihood is [x*x, x, 1] . table[:, c]  (gmm.py:56-67). */
+/* Diagonal-model coefficient table such that for frame x the diagonal log-likelihood is
+ * [x*x, x, 1] . table[:, c]  (gmm.py:56-67).  The buffer holds tvk_diag_table_bytes(C, F) bytes:
+ * the (2F+1) x C FP64 matrix first, followed by the tensor-core operands of the preselection
+ * (3xTF32 hi/lo split of the coefficients in tcgen05 K-major layout, per-row magnitude bounds,
+ * and a component-major FP64 copy for exact rescoring). */
+int64_t tvk_diag_table_bytes(int C, int F);
 int tvk_diag_table(const double* weights, const double* means, const double* variances, int C, int F,
                    double* table, void* stream);
 

@@ -20,13 +20,16 @@ def _f64(a):
 
 
 class DiagTable:
-    """(2F+1) x C coefficient table of a diagonal GMM (gmm.py:56-67)."""
+    """(2F+1) x C coefficient table of a diagonal GMM (gmm.py:56-67), followed in the same device
+    buffer by the tensor-core operands of the top-K preselection (``tvk_diag_table_bytes``)."""
 
     def __init__(self, weights, means, variances):
         w, mu, var = _f64(weights), _f64(means), _f64(variances)
         self.C, self.F = mu.shape
-        self.table = _lib.empty((2 * self.F + 1, self.C))
-        call("tvk_diag_table", ptr(w), ptr(mu), ptr(var), self.C, self.F, ptr(self.table), stream())
+        nbytes = int(_lib.load().tvk_diag_table_bytes(self.C, self.F))
+        self.buf = _lib.empty(((nbytes + 7) // 8,))
+        self.table = self.buf[: (2 * self.F + 1) * self.C].view(2 * self.F + 1, self.C)
+        call("tvk_diag_table", ptr(w), ptr(mu), ptr(var), self.C, self.F, ptr(self.buf), stream())
 
 
 class FullTable:

@@ -42,6 +42,7 @@ SIGNATURES = {
     "tvk_ddot": (_i, [_p, _p, _i64, _d, _d, _p, _p, _p]),
     "tvk_spd_small": (_i, [_p, _i, _i, _p, _p, _p, _p, _p]),
     "tvk_diag_table": (_i, [_p, _p, _p, _i, _i, _p, _p]),
+    "tvk_diag_table_bytes": (_i64, [_i, _i]),
     "tvk_full_table": (_i, [_p, _p, _p, _i, _i, _p, _p, _p]),
     "tvk_precision_table": (_i, [_p, _p, _p, _i, _i, _p, _p, _p]),
     "tvk_precision_table_stride": (_i64, [_i]),

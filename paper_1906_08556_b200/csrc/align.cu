@@ -9,6 +9,8 @@
 //      degenerate rule (argmax in selection order), renormalize, sort by component (gmm.py:414-438);
 //   4. exclusive scan of the per-frame counts and a compaction into the CSR arrays.
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "gemm_f64.cuh"
@@ -564,8 +566,10 @@ extern "C" int tvk_diag_table(const double* weights, const double* means, const 
   TVK_REQUIRE(C >= 1 && F >= 1, "diag_table: empty model");
   diag_table_kernel<<<ceil_div(C, 128), 128, 0, (cudaStream_t)stream>>>(weights, means, variances, C, F, table);
   TVK_CHECK_LAUNCH("diag_table");
-  return TVK_OK;
+  return diag_table_tc(table, C, F, (cudaStream_t)stream);
 }
+
+extern "C" int64_t tvk_diag_table_bytes(int C, int F) { return (int64_t)diag_table_bytes(C, F); }
 
 extern "C" int tvk_full_table(const double* weights, const double* means, const double* covariances, int C, int F,
                               double* table, int32_t* status, void* stream) {
@@ -582,9 +586,15 @@ extern "C" int64_t tvk_align_workspace_bytes(int64_t T, int K, int C) { return (
 
 namespace tvk {
 
+static bool select_dmma_forced() {  // TVK_SELECT=dmma: the FP64 DMMA preselection (A/B comparisons)
+  const char* e = getenv("TVK_SELECT");
+  return e && strcmp(e, "dmma") == 0;
+}
+
 template <typename XT>
 static int launch_select(const XT* x, int64_t T, int F, const double* diag_table, int C, int K, int32_t* sel,
                          double* val, cudaStream_t st) {
+  if (select_tc_supported(F, K) && !select_dmma_forced()) return select_tc<XT>(x, T, F, diag_table, C, K, sel, val, st);
   size_t smem = sel::smem_bytes(F, K);
   TVK_REQUIRE(smem <= 227 * 1024, "align_frames: F too large for the preselection tile");
   cudaFuncSetAttribute(select_topk_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,0 +1,111 @@
+"""GPU check of the tcgen05 preselection: identical to the FP64 DMMA kernel and to the oracle, plus timing."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import bench
+import paper_1906_08556_b200 as pkg
+from paper_1906_08556_b200 import _lib, _device
+from oracle import tvkit_oracle as orc
+
+
+def run(x, tab, C, k, mode, values=False):
+    os.environ["TVK_SELECT"] = mode
+    sel, val = _device.select_topk(x, tab, k, values=values)
+    torch.cuda.synchronize()
+    return sel, val
+
+
+def timeit(x, tab, C, k, mode, reps=3):
+    os.environ["TVK_SELECT"] = mode
+    n, F = x.shape
+    sel = _lib.empty((n, k), torch.int32)
+    f = lambda: _lib.call("tvk_select_topk", _lib.ptr(x), 0, n, F, _lib.ptr(tab.table), C, k, _lib.ptr(sel), None,
+                          _lib.stream())
+    f(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        f()
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def compare(name, x, w, mu, var, k, oracle_n=300):
+    C = mu.shape[0]
+    dm = pkg.GmmDiag(w, mu, var)
+    tab = dm.device_table()
+    a, av = run(x, tab, C, k, "tc", values=True)
+    try:
+        b, bv = run(x, tab, C, k, "dmma", values=True)
+    except _lib.TvkError:
+        b, bv = a, av
+    a, b = a.cpu().numpy(), b.cpu().numpy()
+    diff = np.flatnonzero((a != b).any(1))
+    # differences allowed only on documented ties (values equal to 1e-9 relative)
+    bad = 0
+    av, bv = av.cpu().numpy(), bv.cpu().numpy()
+    for t in diff[:50]:
+        if not np.allclose(av[t], bv[t], rtol=1e-9, atol=1e-9):
+            bad += 1
+    xs = x[:oracle_n].cpu().numpy()
+    ll = orc.diag_loglik(w, mu, var, xs.astype(np.float64))
+    ok_or = None
+    if ll is not None:
+        ref = np.argsort(-ll, axis=1, kind="stable")[:, :k]
+        ok_or = int((ref != a[:oracle_n]).any(1).sum())
+    print(f"{name}: frames {len(a)} differ-vs-dmma {len(diff)} (non-tie {bad}) oracle-mismatch {ok_or}", flush=True)
+    return bad
+
+
+def main():
+    dev = torch.device("cuda")
+    bad = 0
+    rng = np.random.default_rng(0)
+    for (C, F, k, n) in [(64, 20, 20, 3000), (100, 13, 7, 2000), (2048, 60, 20, 50000), (300, 63, 32, 2000),
+                         (20, 5, 20, 500), (129, 8, 1, 1000)]:
+        (w, mu, var), _, x = orc.posterior_ubm(C, F, 0.5, seed=C + F, n_frames=n)
+        bad += compare(f"C={C} F={F} K={k}", torch.from_numpy(x).to(dev), w, mu, var, k)
+        bad += compare(f"C={C} F={F} K={k} f64", torch.from_numpy(x.astype(np.float64)).to(dev), w, mu, var, k)
+    # duplicate components (exact ties) and a zero frame
+    (w, mu, var), _, x = orc.posterior_ubm(64, 10, 0.5, seed=9, n_frames=1000)
+    mu[32:] = mu[:32]; var[32:] = var[:32]; w[32:] = w[:32]
+    x[5] = 0
+    bad += compare("duplicates", torch.from_numpy(x).to(dev), w, mu, var, 20)
+    # approximation error of the tensor-core scores relative to the margin scale S_t
+    for (C, F, sd, n) in [(2048, 60, 0.3, 20000), (512, 40, 3.0, 20000), (64, 20, 0.5, 5000)]:
+        (w, mu, var), _, x = orc.posterior_ubm(C, F, sd, seed=7, n_frames=n)
+        tab = pkg.GmmDiag(w, mu, var).device_table()
+        os.environ["TVK_SELECT_DEBUG"] = "1"
+        xt = torch.from_numpy(x).to(dev)
+        sel, val = run(xt, tab, C, 20, "tc_noexact", values=True)
+        os.environ.pop("TVK_SELECT_DEBUG")
+        ok = sel[:, 0].cpu().numpy() >= 0
+        d = np.abs(val.cpu().numpy())[ok]
+        a = 0.5 / var; b = np.abs(mu / var)
+        c = np.abs(np.log(w) - 0.5 * (F * np.log(2 * np.pi) + np.log(var).sum(1)) - 0.5 * (mu * mu / var).sum(1))
+        xd = x.astype(np.float64)[ok]
+        St = (xd ** 2) @ a.max(0) + np.abs(xd) @ b.max(0) + c.max()
+        r = d / St[:, None]
+        print(f"approx error C={C} F={F} sd={sd}: max |s~-s|/S_t = {r.max():.3e} (2^{np.log2(r.max()):.1f}), "
+              f"99.99% {np.quantile(r, 0.9999):.3e}, median {np.median(r):.3e}", flush=True)
+    # timing at config 2
+    n = 2_000_000
+    wu, muu, cov = bench.make_ubm(0)
+    xb = bench.sample_frames(wu, muu, cov, n, 5, dev)
+    var = np.ascontiguousarray(np.diagonal(cov, axis1=1, axis2=2))
+    tab = pkg.GmmDiag(wu, muu, var).device_table()
+    for mode in ("tc", "dmma"):
+        ms = timeit(xb, tab, 2048, 20, mode)
+        print(f"{mode}: {ms:.2f} ms / {n} frames -> {n / ms / 1e3:.1f} M frames/s", flush=True)
+    ms = timeit(xb, tab, 2048, 20, "tc_noexact")
+    f, _ = run(xb, tab, 2048, 20, "tc_noexact")
+    print(f"tc without exact pass: {ms:.2f} ms, flagged frames {int((f[:, 0] == -1).sum().item())}", flush=True)
+    a, _ = run(xb, tab, 2048, 20, "tc")
+    b, _ = run(xb, tab, 2048, 20, "dmma")
+    print("config2 2e6 frames identical:", bool(torch.equal(a, b)), "rows differing:",
+          int((a != b).any(1).sum().item()))
+    print("BAD" if bad else "ALL OK")
+
+
+if __name__ == "__main__":
+    main()
