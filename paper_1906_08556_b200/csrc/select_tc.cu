@@ -23,6 +23,7 @@
 //   warp 2: TMEM allocator (512 columns = 4 accumulator buffers of 128 components);
 //   warps 4-7: epilogue (A-operand producer, candidate window, exact clusters, output).
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -34,14 +35,20 @@ namespace stc {
 
 constexpr int TM = 128;        // frames per tile = MMA M = TMEM lanes
 constexpr int NC = 128;        // components per chunk = MMA N
-constexpr int NBUF = 4;        // TMEM accumulator buffers
-constexpr int NST = 4;         // B ring stages, one k-step (hi + lo) each
-constexpr int STAGE = 8192;    // bytes per stage: 128 comps x 8 k x (hi, lo) x 4 B
-constexpr int NEPI = 128;      // epilogue threads
+// TMEM columns: [0,128) acc 0 | [128,256) acc 1 | [256,384) A hi | [384,512) A lo
+constexpr int RING = 98304;    // B ring bytes: NST stages of STAGE bytes (runtime split, see Pipe)
+constexpr int XS = 64;         // smem row stride (floats) of the staged frame tile, >= F + 1
+constexpr int MAXST = 12;
+constexpr int CL = 1;          // CTAs per cluster sharing every B stage by TMA multicast (4 measured slower)
+constexpr int KSTEP = 8192;    // blob bytes per k-step: 128 comps x 8 k x (hi, lo) x 4 B
+constexpr int H = 2;           // epilogue warps per TMEM lane quarter (each takes half of a chunk's columns)
+constexpr int NEPI = 128 * H;  // epilogue threads
 constexpr int NT = 128 + NEPI;
-constexpr int CAP = 32;        // candidate buffer entries per frame
-constexpr float KAPPA = 1.0f / 65536.0f;  // 64x the max observed error, 5.6x the RN worst case
-constexpr int MAX_F = 63;      // A tile (2 x 128 x (2F+1) x 4 B) must fit next to the ring
+constexpr int CAP = 24;        // candidate buffer entries per (frame, half)
+constexpr int WMAX = 24;       // merged window entries per frame
+constexpr float KAPPA = 1.0f / 65536.0f;  // 3xTF32 bound: 28x the max observed error
+constexpr float KAPPA1 = 1.0f / 4096.0f;   // pass-0 slack (heuristic: the window check below is exact)
+constexpr int MAX_F = 63;      // A hi/lo (2F+1 columns each, padded to 8) must fit in TMEM columns 256-511
 
 __host__ __device__ inline int kp(int F) { return (2 * F + 1 + 7) / 8 * 8; }  // [x^2, x, 1], padded
 __host__ __device__ inline int nchunks(int C) { return (C + NC - 1) / NC; }
@@ -55,7 +62,7 @@ __host__ __device__ inline Layout layout(int C, int F) {
   Layout L;
   size_t off = al(sizeof(double) * (size_t)(2 * F + 1) * C, 1024);
   L.blob = off;
-  off += (size_t)nchunks(C) * (kp(F) / 8) * STAGE;
+  off += (size_t)nchunks(C) * (kp(F) / 8) * KSTEP;
   L.maxes = off;
   off = al(off + sizeof(float) * (2 * F + 1), 256);
   L.exact = off;
@@ -64,8 +71,9 @@ __host__ __device__ inline Layout layout(int C, int F) {
   return L;
 }
 
-inline size_t smem_bytes(int F) {
-  return (size_t)2 * TM * kp(F) * 4 + (size_t)NST * STAGE + (size_t)CAP * NEPI * (4 + 4 + 8) + 256;
+inline size_t smem_bytes(int) {
+  return (size_t)RING + (size_t)TM * XS * 4 + (size_t)CAP * NEPI * 8 + (size_t)WMAX * TM * 16 +
+         (size_t)TM * 8 + 256;
 }
 
 // ---------------------------------------------------------------- table construction
@@ -83,10 +91,11 @@ __global__ void build_blob_kernel(const double* tab, int C, int F, float* blob) 
     float wf = (float)w;
     float hi = tc::tf32_round(wf);
     float lo = tc::tf32_round(wf - hi);
-    size_t base = ((size_t)n * KS + s) * (STAGE / 4);
+    // hi words of all (chunk, k-step) tiles first, then the lo words: 4 KB per tile each
+    size_t base = ((size_t)n * KS + s) * 1024, lo_off = (size_t)NCH * KS * 1024;
     uint32_t o = tc::kmajor_offset(r, kk, 8) / 4;
     blob[base + o] = hi;
-    blob[base + 1024 + o] = lo;
+    blob[lo_off + base + o] = lo;
   }
 }
 
@@ -140,6 +149,7 @@ __device__ __forceinline__ bool better(double v, int i, double w, int j) {
 // value-only descending top list: insert t (branch-free min/max chain), read the K-th entry
 template <int NK>
 __device__ __forceinline__ void insert_top(float (&top)[NK], float t) {
+  t = fmaxf(t, -INFINITY);  // NaN (padded components) inserts as -inf
 #pragma unroll
   for (int i = 0; i < NK; i++) {
     const float hi = fmaxf(top[i], t);
@@ -147,6 +157,21 @@ __device__ __forceinline__ void insert_top(float (&top)[NK], float t) {
     top[i] = hi;
   }
 }
+// Accumulator buffer b = n % 2 hosts chunk n of either pass: the number of earlier uses of b (its
+// mbarrier phase) at (tile li, pass, chunk n), for both sides.
+__device__ __forceinline__ uint32_t buf_uses(int b, uint32_t li, int pass, int n, int NCH) {
+  const uint32_t per_pass = (NCH - b + 1) / 2;
+  return (2 * li + pass) * per_pass + n / 2;
+}
+
+template <int G>
+__device__ __forceinline__ float group_max(const float (&v)[32], int o) {
+  float a = v[o];
+#pragma unroll
+  for (int i = 1; i < G; i++) a = fmaxf(a, v[o + i]);  // NaN (padded components) is ignored
+  return a;
+}
+
 // With K < NK the first NK-K slots hold +inf sentinels, so the K-th largest is always top[NK-1]
 // (a runtime-indexed read would push the list to local memory).
 template <int NK>
@@ -155,31 +180,42 @@ __device__ __forceinline__ float kth_of(const float (&top)[NK], int) {
 }
 
 // ---------------------------------------------------------------- main kernel
+struct Pipe {  // B-ring geometry and back-off of the single-thread roles (tunable, TVK_SEL_PIPE)
+  int stage_bytes, sp0, sp1, sleep_prod, sleep_mma;
+};
+
 template <typename XT, int NK>
 __global__ void __launch_bounds__(NT, 1)
     select_tc_kernel(const XT* __restrict__ x, int64_t T, int F, int C, int K, const float* __restrict__ blob,
-                     const float* __restrict__ maxes, const double* __restrict__ exact, float kappa, int debug,
-                     int32_t* __restrict__ sel_out, double* __restrict__ val_out) {
+                     const float* __restrict__ maxes, const double* __restrict__ exact, float kappa, float kappa1,
+                     int group, int debug, Pipe pipe, int32_t* __restrict__ sel_out, double* __restrict__ val_out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KP = kp(F), KS = KP / 8, NCH = nchunks(C);
-  uint8_t* sAhi = smem;
-  uint8_t* sAlo = smem + TM * KP * 4;
-  uint8_t* ring = sAlo + TM * KP * 4;
-  float* cv = reinterpret_cast<float*>(ring + NST * STAGE);  // [CAP][NEPI]
-  int* ci = reinterpret_cast<int*>(cv + CAP * NEPI);          // [CAP][NEPI]
-  double* ev = reinterpret_cast<double*>(ci + CAP * NEPI);    // [CAP][NEPI]
-  __shared__ uint64_t full[NST], empty[NST], tfull[NBUF], tempty[NBUF], afull, aempty;
+  uint8_t* ring = smem;                                             // [NST][STAGE]
+  float* xs = reinterpret_cast<float*>(ring + RING);                // [TM][XS] frames of the tile (f32)
+  const int STAGE = pipe.stage_bytes, NST = RING / STAGE;
+  float* cv = xs + TM * XS;                                         // [CAP][NEPI] approx scores
+  int* ci = reinterpret_cast<int*>(cv + CAP * NEPI);                // [CAP][NEPI] components
+  float* mv = reinterpret_cast<float*>(ci + CAP * NEPI);            // [WMAX][TM] merged window
+  int* mi = reinterpret_cast<int*>(mv + WMAX * TM);                 // [WMAX][TM]
+  double* ev = reinterpret_cast<double*>(mi + WMAX * TM);           // [WMAX][TM] exact scores
+  float* kth1 = reinterpret_cast<float*>(ev + WMAX * TM);           // [TM] K-th of the second half
+  int* cnt1 = reinterpret_cast<int*>(kth1 + TM);                    // [TM] window size of the second half
+  __shared__ uint64_t full[MAXST], empty[MAXST], tfull[2], tempty[2], afull, aempty;
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (T + TM - 1) / TM;
+  // every CTA runs the same number of tiles (the B stream is shared by the cluster); tiles past the
+  // end are all-dead rows
+  const int64_t iters = (ntiles + gridDim.x - 1) / gridDim.x;
 
   if (tid == 0) {
     for (int i = 0; i < NST; i++) {
       tc::mbar_init(&full[i], 1);
-      tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&empty[i], CL);
     }
-    for (int i = 0; i < NBUF; i++) {
+    for (int i = 0; i < 2; i++) {
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], NEPI / 32);
     }
@@ -190,51 +226,73 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 2) tc::tmem_alloc<512>(&tmem_base);
   tc::fence_before_sync();
   __syncthreads();
+  tc::cluster_sync();  // barrier inits visible to the peers' multicast copies and commits
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base;
+  const uint32_t tA_hi = tmem + 256, tA_lo = tmem + 384;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    // Every stage lands in all CL CTAs of the cluster: this CTA copies its 1/CL share of each piece
+    // with multicast, and a slot is refilled only after all CL MMA issuers released it.
     if (lane == 0) {
+      const uint32_t crank = tc::cluster_ctarank();
+      const uint16_t mask = (uint16_t)((1u << CL) - 1u);
+      const float* blob_lo = blob + (size_t)NCH * KS * 1024;
       uint32_t q = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        for (int n = 0; n < NCH; n++)
-          for (int s = 0; s < KS; s++, q++) {
-            const int slot = q % NST;
-            tc::mbar_wait_backoff(&empty[slot], ((q / NST) & 1) ^ 1);
-            tc::mbar_arrive_expect_tx(&full[slot], STAGE);
-            tc::bulk_g2s(ring + slot * STAGE, blob + ((size_t)n * KS + s) * (STAGE / 4), STAGE, &full[slot]);
-          }
+      for (int64_t it = 0; it < iters; it++)
+        for (int pass = 0; pass < 2; pass++) {
+          const int SP = pass == 0 ? pipe.sp0 : pipe.sp1;  // k-steps per stage
+          for (int n = 0; n < NCH; n++)
+            for (int s0 = 0; s0 < KS; s0 += SP, q++) {
+              const int slot = q % NST, ns = min(SP, KS - s0);
+              tc::mbar_wait_backoff(&empty[slot], ((q / NST) & 1) ^ 1, pipe.sleep_prod);
+              const uint32_t piece = ns * 4096, share = piece / CL;  // hi (and lo) words of ns k-steps
+              tc::mbar_arrive_expect_tx(&full[slot], pass == 0 ? piece : 2 * piece);
+              const size_t src = ((size_t)n * KS + s0) * 1024 + crank * (share / 4);
+              uint8_t* dst = ring + slot * STAGE + crank * share;
+              tc::bulk_g2s_mc(dst, blob + src, share, &full[slot], mask);
+              if (pass == 1) tc::bulk_g2s_mc(dst + piece, blob_lo + src, share, &full[slot], mask);
+            }
+        }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------ MMA issuer (A from TMEM)
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_tf32(TM, NC);
-      const uint32_t a_hi = tc::smem_u32(sAhi), a_lo = tc::smem_u32(sAlo), rb = tc::smem_u32(ring);
-      const uint32_t sbo_a = 8 * KP * 4;
-      uint32_t q = 0, g = 0, li = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, li++) {
-        tc::mbar_wait_backoff(&afull, li & 1);
+      const uint32_t rb = tc::smem_u32(ring);
+      uint32_t q = 0, li = 0;
+      const uint16_t mask = (uint16_t)((1u << CL) - 1u);
+      for (int64_t it = 0; it < iters; it++, li++) {
+        tc::mbar_wait_backoff(&afull, li & 1, 64);
         tc::fence_after_sync();
-        for (int n = 0; n < NCH; n++, g++) {
-          const int b = g % NBUF;
-          tc::mbar_wait_backoff(&tempty[b], ((g / NBUF) & 1) ^ 1);
-          tc::fence_after_sync();
-          const uint32_t d = tmem + b * NC;
-          for (int s = 0; s < KS; s++, q++) {
-            const int slot = q % NST;
-            tc::mbar_wait_backoff(&full[slot], (q / NST) & 1);
+        for (int pass = 0; pass < 2; pass++) {
+          const int SP = pass == 0 ? pipe.sp0 : pipe.sp1;
+          for (int n = 0; n < NCH; n++) {
+            const int b = n % 2;
+            tc::mbar_wait_backoff(&tempty[b], (buf_uses(b, li, pass, n, NCH) & 1) ^ 1, pipe.sleep_mma);
             tc::fence_after_sync();
-            const uint64_t bh = tc::smem_desc(rb + slot * STAGE, 128, 256);
-            const uint64_t bl = tc::smem_desc(rb + slot * STAGE + 4096, 128, 256);
-            const uint64_t ah = tc::smem_desc(a_hi + 256 * s, 128, sbo_a);
-            const uint64_t alo = tc::smem_desc(a_lo + 256 * s, 128, sbo_a);
-            tc::mma_tf32(d, ah, bh, idesc, s > 0);
-            tc::mma_tf32(d, ah, bl, idesc, 1);
-            tc::mma_tf32(d, alo, bh, idesc, 1);
-            tc::mma_commit(&empty[slot]);
+            const uint32_t d = tmem + b * NC;
+            for (int s0 = 0; s0 < KS; s0 += SP, q++) {
+              const int slot = q % NST, ns = min(SP, KS - s0);
+              tc::mbar_wait_backoff(&full[slot], (q / NST) & 1, pipe.sleep_mma);
+              tc::fence_after_sync();
+              if (debug != 3) {  // debug 3: copies only
+                for (int i = 0; i < ns; i++) {
+                  const int s = s0 + i;
+                  const uint64_t bh = tc::smem_desc(rb + slot * STAGE + i * 4096, 128, 256);
+                  tc::mma_tf32_ts(d, tA_hi + 8 * s, bh, idesc, s > 0);
+                  if (pass == 1) {  // 3xTF32: a_hi b_hi + a_hi b_lo + a_lo b_hi
+                    const uint64_t bl = tc::smem_desc(rb + slot * STAGE + (ns + i) * 4096, 128, 256);
+                    tc::mma_tf32_ts(d, tA_hi + 8 * s, bl, idesc, 1);
+                    tc::mma_tf32_ts(d, tA_lo + 8 * s, bh, idesc, 1);
+                  }
+                }
+              }
+              tc::mma_commit_mc(&empty[slot], mask);  // releases the slot in every CTA of the cluster
+            }
+            tc::mma_commit(&tfull[b]);
           }
-          tc::mma_commit(&tfull[b]);
         }
         tc::mma_commit(&aempty);
       }
@@ -242,227 +300,309 @@ __global__ void __launch_bounds__(NT, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const int e = tid - 128;            // 0..127
-    const int r = (warp & 3) * 32 + lane;  // TMEM lane = frame row of the tile
+    const int e = tid - 128;                // 0..NEPI-1
+    const int h = e / 128;                  // column half of every chunk
+    const int r = (warp & 3) * 32 + lane;   // TMEM lane = frame row of the tile
     const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    const uint32_t sbo_a = 8 * KP * 4;
     const float* amax = maxes;
     const float* bmax = maxes + F;
     const float cmax = maxes[2 * F];
 
-    auto build_A = [&](int64_t tile) -> float {  // returns the margin m of this thread's frame
+    // Features [x^2, x, 1, 0...] of this thread's frame, TF32 hi (part 0, TMEM columns 256+) or lo
+    // (part 1, columns 384+) words.  Each half writes the 64 columns it reads of every accumulator.
+    const int FP = F | 1;  // odd row stride: conflict-free row-per-thread reads
+    // coalesced load of the tile's frames (as f32) into smem; all epilogue threads, then a barrier
+    auto load_x = [&](int64_t tile) {
+      const int64_t base = tile * TM;
+      for (int i = e; i < TM * F; i += NEPI) {
+        const int rr = i / F, cc = i - rr * F;
+        xs[rr * FP + cc] = base + rr < T ? (float)x[(base + rr) * F + cc] : 0.0f;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
+    };
+    auto build_A = [&](int64_t tile) {
       const int64_t t = tile * TM + r;
       const bool ok = t < T;
-      const XT* xr = x + (ok ? t : 0) * F;
-      float S = cmax;
-      for (int j = 0; j < KP / 4; j++) {
-        float hv[4], lv[4];
+      const float* xr = xs + r * FP;
+      for (int j = 2 * h; j < 2 * h + 2 && 32 * j < KP; j++) {
+        float wh[32], wl[32];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int k = 4 * j + u;
+        for (int u = 0; u < 32; u++) {
+          const int k = 32 * j + u;
           float v = 0.0f;
           if (ok && k == 2 * F) {
             v = 1.0f;
           } else if (ok && k < 2 * F) {
-            const float xv = (float)xr[k < F ? k : k - F];
-            if (k < F) {
-              v = xv * xv;
-              S += v * amax[k];
-            } else {
-              v = xv;
-              S += fabsf(xv) * bmax[k - F];
-            }
+            const float xv = xr[k < F ? k : k - F];
+            v = k < F ? xv * xv : xv;
           }
-          hv[u] = tc::tf32_round(v);
-          lv[u] = tc::tf32_round(v - hv[u]);
+          wh[u] = tc::tf32_round(v);
+          wl[u] = tc::tf32_round(v - wh[u]);
         }
-        const uint32_t o = (uint32_t)((r >> 3) * sbo_a + j * 128 + (r & 7) * 16);
-        *reinterpret_cast<float4*>(sAhi + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-        *reinterpret_cast<float4*>(sAlo + o) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+        tc::tmem_st32(lane_addr + 256 + 32 * j, wh);
+        tc::tmem_st32(lane_addr + 384 + 32 * j, wl);
       }
-      tc::fence_proxy_async();
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
       tc::mbar_arrive(&afull);
-      return ok ? kappa * S : INFINITY;
+    };
+    // margin scale S_t = sum_f x_f^2 max|a_f| + |x_f| max|b_f| + max|c|
+    auto scale = [&](int64_t tile) -> float {
+      const int64_t t = tile * TM + r;
+      if (t >= T) return INFINITY;
+      const float* xr = xs + r * FP;
+      float S = cmax;
+      for (int f = 0; f < F; f++) {
+        const float xv = (float)xr[f];
+        S += xv * xv * amax[f] + fabsf(xv) * bmax[f];
+      }
+      return S;
     };
 
     int64_t tile = blockIdx.x;
-    float m = tile < ntiles ? build_A(tile) : 0.0f;
-    uint32_t g = 0, li = 0;
-    for (; tile < ntiles; tile += gridDim.x, li++) {
+    if (iters > 0) {
+      load_x(tile);
+      build_A(tile);
+    }
+    float S = iters > 0 ? scale(tile) : 0.0f;
+    uint32_t li = 0;
+    // debug 6: per-phase clock64 timeline of CTA 0, epilogue thread 0 (into val_out)
+    const bool tl = debug == 6 && blockIdx.x == 0 && e == 0 && val_out;
+    auto mark = [&](int it, int ph) {
+      if (tl && it < 64) val_out[it * 8 + ph] = (double)clock64();
+    };
+    for (int64_t it = 0; it < iters; it++, tile += gridDim.x, li++) {
+      mark(it, 0);
       const int64_t t = tile * TM + r;
+      const float m = kappa * S, m2 = 2.0f * m;
+      const bool live = t < T && isfinite(S);  // rows past T (and non-finite frames) take nothing
+
+      // ---- pass 0 (1xTF32): K-th largest of the group maxima, a lower bound of the K-th exact score
       float top[NK];
 #pragma unroll
       for (int i = 0; i < NK; i++) top[i] = i < NK - K ? INFINITY : -INFINITY;
-      const float m2 = 2.0f * m;
-      bool live = t < T && isfinite(m);  // rows past T (and non-finite frames) take nothing
-      float thr = live ? -INFINITY : INFINITY;
-      int cnt = 0, done = 0;
-      bool ovf = false;
-#define TVK_FLUSH()                                                         \
-  do {                                                                      \
-    for (; done < cnt; done++) insert_top<NK>(top, cv[done * NEPI + e]);    \
-    thr = live ? kth_of<NK>(top, K) - m2 : INFINITY;                        \
-  } while (0)
+      for (int n = 0; n < NCH; n++) {
+        const int b = n % 2;
+        tc::mbar_wait(&tfull[b], buf_uses(b, li, 0, n, NCH) & 1);
+        tc::fence_after_sync();
+        const uint32_t col = b * NC + h * (NC / H);
+        float v[2][32];
+        tc::tmem_ld32(lane_addr + col, v[0]);
+        tc::tmem_ld32(lane_addr + col + 32, v[1]);
+        tc::tmem_ld_wait();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[b]);
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          if (debug >= 2) continue;  // diagnostics: MMA/producer pipeline only
+          if (group == 32) {
+            insert_top<NK>(top, group_max<32>(v[j], 0));
+          } else if (group == 8) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) insert_top<NK>(top, group_max<8>(v[j], 8 * q));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; q++) insert_top<NK>(top, v[j][q]);
+          }
+        }
+      }
+      mark(it, 1);
+      mark(it, 2);
 
-      for (int n = 0; n < NCH; n++, g++) {
-        const int b = g % NBUF;
-        tc::mbar_wait(&tfull[b], (g / NBUF) & 1);
+      // union of both halves' lists: half 1 publishes, half 0 merges and publishes the threshold
+      if (h == 1) {
+#pragma unroll
+        for (int i = 0; i < NK; i++) mv[i * TM + r] = top[i];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
+      if (h == 0) {
+#pragma unroll
+        for (int i = 0; i < NK; i++) insert_top<NK>(top, i >= NK - K ? mv[i * TM + r] : -INFINITY);
+        // every exact score of the K group maxima is >= (their 1xTF32 score) - kappa1 S
+        kth1[r] = kth_of<NK>(top, K) - kappa1 * S - 3.0f * m;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
+      const float thr = live ? kth1[r] : INFINITY;
+      if (it + 1 < iters) load_x(tile + gridDim.x);  // frames of the next tile, read after its A is free
+      mark(it, 3);
+
+      // ---- pass 1 (3xTF32): collect every score >= thr
+      int cnt = 0;
+      bool ovf = false;
+      for (int n = 0; n < NCH; n++) {
+        const int b = n % 2;
+        tc::mbar_wait(&tfull[b], buf_uses(b, li, 1, n, NCH) & 1);
         tc::fence_after_sync();
 #pragma unroll 1
-        for (int j = 0; j < NC / 32; j++) {
+        for (int j = 0; j < NC / 32 / H; j++) {
+          const int col = h * (NC / H) + j * 32;
           float v[32];
-          tc::tmem_ld32(lane_addr + b * NC + j * 32, v);
+          tc::tmem_ld32(lane_addr + b * NC + col, v);
           tc::tmem_ld_wait();
-          if (j == NC / 32 - 1) {
+          if (j == NC / 32 / H - 1) {
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[b]);
           }
-          const int c0 = n * NC + j * 32;
-          int u0 = 0;
-          while (true) {  // one pass; repeated from the first dropped score when the buffer filled up
-            int drop = 32;
+          if (debug >= 2) continue;
+          const int c0 = n * NC + col;
 #pragma unroll
-            for (int u = 0; u < 32; u++) {
-              const float s = v[u];
-              if (u >= u0 && s >= thr) {
-                if (cnt < CAP) {
-                  cv[cnt * NEPI + e] = s;
-                  ci[cnt * NEPI + e] = c0 + u;
-                  cnt++;
-                } else if (drop == 32) {
-                  drop = u;
-                }
+          for (int u = 0; u < 32; u++) {
+            if (v[u] >= thr) {
+              if (cnt < CAP) {
+                cv[cnt * NEPI + e] = v[u];
+                ci[cnt * NEPI + e] = c0 + u;
               }
+              cnt++;
             }
-            TVK_FLUSH();
-            if (drop == 32) break;
-            int w = 0;  // compact: drop entries below the raised threshold
-            for (int i = 0; i < cnt; i++) {
-              const float cvv = cv[i * NEPI + e];
-              if (cvv >= thr) {
-                cv[w * NEPI + e] = cvv;
-                ci[w * NEPI + e] = ci[i * NEPI + e];
-                w++;
-              }
-            }
-            cnt = done = w;
-            if (cnt == CAP) {
-              ovf = true;
-              live = false;
-              thr = INFINITY;
-              break;
-            }
-            u0 = drop;
           }
         }
       }
 
       // A operand of the next tile (all MMAs of this tile have completed: their last chunk was read)
+      mark(it, 4);
       const int64_t next = tile + gridDim.x;
-      float m_next = 0.0f;
-      if (next < ntiles) {
+      float S_next = 0.0f;
+      if (it + 1 < iters) {
         tc::mbar_wait(&aempty, li & 1);
-        m_next = build_A(next);
+        build_A(next);
+        S_next = scale(next);
       }
 
-      // ---- window, clusters, exact order for frame t
+      mark(it, 5);
+      // ---- half lists sorted by s~ desc (index asc on ties)
+      ovf = cnt > CAP;
+      const int W = (t < T && !ovf) ? cnt : 0;
+      {
+        for (int p = 0; p < W; p++) {
+          int bi = p;
+          float bv = cv[p * NEPI + e];
+          int bc = ci[p * NEPI + e];
+          for (int i = p + 1; i < W; i++) {
+            const float vv = cv[i * NEPI + e];
+            const int cc = ci[i * NEPI + e];
+            if (vv > bv || (vv == bv && cc < bc)) {
+              bv = vv;
+              bc = cc;
+              bi = i;
+            }
+          }
+          if (bi != p) {
+            cv[bi * NEPI + e] = cv[p * NEPI + e];
+            ci[bi * NEPI + e] = ci[p * NEPI + e];
+            cv[p * NEPI + e] = bv;
+            ci[p * NEPI + e] = bc;
+          }
+        }
+      }
+      if (h == 1) cnt1[r] = ovf ? -1 : W;
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
+
+      // ---- half 0 merges both halves into the frame window and flags the entries needing FP64
       bool good = false;
-      unsigned need = 0u;  // window positions whose exact FP64 score is needed
-      if (t < T) {
-        const float tk = kth_of<NK>(top, K);
-        int W = 0;  // window entries, compacted to the front
-        for (int i = 0; i < cnt; i++) {
-          const float cvv = cv[i * NEPI + e];
-          if (cvv >= tk - m2) {
-            cv[W * NEPI + e] = cvv;
-            ci[W * NEPI + e] = ci[i * NEPI + e];
-            W++;
-          }
-        }
-        good = !ovf && W >= K && isfinite(tk) && isfinite(m);
+      unsigned need = 0u;
+      if (h == 0 && t < T) {
+        const int W1 = cnt1[r];
+        good = live && !ovf && W1 >= 0 && W + W1 >= K;
         if (good) {
-          for (int p = 0; p < W; p++) {  // selection sort by s~ (desc), index asc on equal s~
-            int bi = p;
-            float bv = cv[p * NEPI + e];
-            int bc = ci[p * NEPI + e];
-            for (int i = p + 1; i < W; i++) {
-              const float vv = cv[i * NEPI + e];
-              const int cc = ci[i * NEPI + e];
-              if (vv > bv || (vv == bv && cc < bc)) {
-                bv = vv;
-                bc = cc;
-                bi = i;
+          const float lb = thr;
+          const int o1 = e + 128;
+          int i0 = 0, i1 = 0, Wm = 0;
+          while (Wm < WMAX) {
+            const bool a0 = i0 < W && cv[i0 * NEPI + e] >= lb;
+            const bool a1 = i1 < W1 && cv[i1 * NEPI + o1] >= lb;
+            if (!a0 && !a1) break;
+            bool take0 = a0;
+            if (a0 && a1) {
+              const float v0 = cv[i0 * NEPI + e], v1 = cv[i1 * NEPI + o1];
+              take0 = v0 > v1 || (v0 == v1 && ci[i0 * NEPI + e] < ci[i1 * NEPI + o1]);
+            }
+            if (take0) {
+              mv[Wm * TM + r] = cv[i0 * NEPI + e];
+              mi[Wm * TM + r] = ci[i0 * NEPI + e];
+              i0++;
+            } else {
+              mv[Wm * TM + r] = cv[i1 * NEPI + o1];
+              mi[Wm * TM + r] = ci[i1 * NEPI + o1];
+              i1++;
+            }
+            Wm++;
+          }
+          // the collected K-th (a lower bound of the true K-th) must clear the collection threshold,
+          // otherwise window entries may have been skipped (pass-0 slack too small): exact path
+          if (Wm < K || mv[(K - 1) * TM + r] - m2 < thr) {
+            good = false;
+          } else {
+            const float lim = mv[(K - 1) * TM + r] - m2;  // the exact frame window
+            int We = K;
+            while (We < Wm && mv[We * TM + r] >= lim) We++;
+            const bool more = (i0 < W && cv[i0 * NEPI + e] >= lim) || (i1 < W1 && cv[i1 * NEPI + o1] >= lim);
+            if (We == WMAX && more) good = false;  // window larger than the merge buffer
+            for (int p = 0; good && p < K;) {
+              int q = p + 1;
+              while (q < We && mv[(q - 1) * TM + r] - mv[q * TM + r] <= m2) q++;
+              if (q - p > 1 || val_out || debug) need |= (q - p >= 32 ? 0xffffffffu : ((1u << (q - p)) - 1u)) << p;
+              p = q;
+            }
+          }
+        }
+        if (!good) sel_out[t * K] = -1;  // recomputed by select_exact_kernel
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // half 1 may now reuse its candidate buffer
+      mark(it, 6);
+      if (h == 0) {
+        {  // exact FP64 scores of the flagged entries: one converged pass over the warp
+          const XT* xr = x + (t < T ? t : 0) * F;
+          unsigned rest = need;
+          while (__any_sync(0xffffffffu, rest != 0u)) {
+            const int i = rest ? __ffs(rest) - 1 : -1;
+            rest &= rest - 1u;
+            if (i >= 0) ev[i * TM + r] = exact_score(xr, exact + (int64_t)mi[i * TM + r] * (2 * F + 2), F);
+          }
+        }
+        if (good) {
+          if (debug) {  // diagnostics: s~ - s of the s~-ordered window
+            for (int i = 0; i < K; i++) {
+              sel_out[t * K + i] = mi[i * TM + r];
+              if (val_out) val_out[t * K + i] = (double)mv[i * TM + r] - ev[i * TM + r];
+            }
+          } else {
+            for (int p = 0; p < 32;) {  // re-sort each flagged cluster by the exact rank
+              if (!((need >> p) & 1u)) {
+                p++;
+                continue;
               }
-            }
-            if (bi != p) {
-              cv[bi * NEPI + e] = cv[p * NEPI + e];
-              ci[bi * NEPI + e] = ci[p * NEPI + e];
-              cv[p * NEPI + e] = bv;
-              ci[p * NEPI + e] = bc;
-            }
-          }
-          // clusters (runs with gaps <= 2m) that reach into the first K positions; all of the
-          // first K positions when the caller wants the values
-          for (int p = 0; p < K;) {
-            int q = p + 1;
-            while (q < W && cv[(q - 1) * NEPI + e] - cv[q * NEPI + e] <= m2) q++;
-            if (q - p > 1 || val_out || debug)
-              need |= (q - p >= 32 ? 0xffffffffu : ((1u << (q - p)) - 1u)) << p;
-            p = q;
-          }
-        } else {
-          sel_out[t * K] = -1;  // recomputed by select_exact_kernel
-        }
-      }
-      {  // exact FP64 scores of the flagged entries: one converged pass over the warp
-        const XT* xr = x + (t < T ? t : 0) * F;
-        unsigned rest = need;
-        while (__any_sync(0xffffffffu, rest != 0u)) {
-          const int i = rest ? __ffs(rest) - 1 : -1;
-          rest &= rest - 1u;
-          if (i >= 0) ev[i * NEPI + e] = exact_score(xr, exact + (int64_t)ci[i * NEPI + e] * (2 * F + 2), F);
-        }
-      }
-      if (good) {
-        if (debug) {  // diagnostics: approximate scores of the s~-ordered window, before exact re-sorting
-          for (int i = 0; i < K; i++) {
-            sel_out[t * K + i] = ci[i * NEPI + e];
-            if (val_out) val_out[t * K + i] = (double)cv[i * NEPI + e] - ev[i * NEPI + e];
-          }
-        } else {
-          for (int p = 0; p < 32;) {  // re-sort each flagged cluster by the exact rank
-            if (!((need >> p) & 1u)) {
-              p++;
-              continue;
-            }
-            int q = p + 1;
-            while (q < 32 && ((need >> q) & 1u) && cv[(q - 1) * NEPI + e] - cv[q * NEPI + e] <= m2) q++;
-            for (int i = p + 1; i < q; i++) {
-              const double vv = ev[i * NEPI + e];
-              const int cc = ci[i * NEPI + e];
-              int k = i;
-              while (k > p && better(vv, cc, ev[(k - 1) * NEPI + e], ci[(k - 1) * NEPI + e])) {
-                ev[k * NEPI + e] = ev[(k - 1) * NEPI + e];
-                ci[k * NEPI + e] = ci[(k - 1) * NEPI + e];
-                k--;
+              int q = p + 1;
+              while (q < 32 && ((need >> q) & 1u) && mv[(q - 1) * TM + r] - mv[q * TM + r] <= m2) q++;
+              for (int i = p + 1; i < q; i++) {
+                const double vv = ev[i * TM + r];
+                const int cc = mi[i * TM + r];
+                int k = i;
+                while (k > p && better(vv, cc, ev[(k - 1) * TM + r], mi[(k - 1) * TM + r])) {
+                  ev[k * TM + r] = ev[(k - 1) * TM + r];
+                  mi[k * TM + r] = mi[(k - 1) * TM + r];
+                  k--;
+                }
+                ev[k * TM + r] = vv;
+                mi[k * TM + r] = cc;
               }
-              ev[k * NEPI + e] = vv;
-              ci[k * NEPI + e] = cc;
+              p = q;
             }
-            p = q;
-          }
-          for (int i = 0; i < K; i++) {
-            sel_out[t * K + i] = ci[i * NEPI + e];
-            if (val_out) val_out[t * K + i] = ev[i * NEPI + e];
+            for (int i = 0; i < K; i++) {
+              sel_out[t * K + i] = mi[i * TM + r];
+              if (val_out) val_out[t * K + i] = ev[i * TM + r];
+            }
           }
         }
       }
-      m = m_next;
+      mark(it, 7);
+      S = S_next;
     }
   }
   tc::fence_before_sync();
   __syncthreads();
+  tc::cluster_sync();  // no peer may still multicast into this CTA's ring or arrive on its barriers
   if (warp == 2) tc::tmem_dealloc<512>(tmem);
 }
 
@@ -562,13 +702,41 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   auto kern = stc::select_tc_kernel<XT, NK>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int64_t ntiles = (T + stc::TM - 1) / stc::TM;
-  int grid = (int)std::min<int64_t>(ntiles, num_sms());
+  int64_t want = (ntiles + stc::CL - 1) / stc::CL * stc::CL;
+  int grid = (int)std::min<int64_t>(want, num_sms() / stc::CL * stc::CL);
   const char* ek = getenv("TVK_SELECT_KAPPA");
   const float kappa = ek ? (float)atof(ek) : stc::KAPPA;
   const char* ed = getenv("TVK_SELECT_DEBUG");
   const int debug = ed ? atoi(ed) : 0;
-  kern<<<grid, stc::NT, smem, st>>>(x, T, F, C, K, (const float*)(base + L.blob), (const float*)(base + L.maxes),
-                                    (const double*)(base + L.exact), kappa, debug, sel, val);
+  const char* ek1 = getenv("TVK_SELECT_KAPPA1");
+  const float kappa1 = ek1 ? (float)atof(ek1) : stc::KAPPA1;
+  // group maxima of 32 (or 8, or single scores) while at least 2K groups exist
+  const int group = C >= 64 * K ? 32 : (C >= 16 * K ? 8 : 1);
+  stc::Pipe pipe{32768, 8, 4, 64, 0};  // 3 stages of 32 KB
+  if (const char* ep = getenv("TVK_SEL_PIPE"))  // stage_bytes,sp0,sp1,sleep_prod,sleep_mma
+    sscanf(ep, "%d,%d,%d,%d,%d", &pipe.stage_bytes, &pipe.sp0, &pipe.sp1, &pipe.sleep_prod, &pipe.sleep_mma);
+  TVK_REQUIRE(pipe.stage_bytes >= 8192 && stc::RING % pipe.stage_bytes == 0 && stc::RING / pipe.stage_bytes <= stc::MAXST &&
+                  pipe.sp0 * 4096 <= pipe.stage_bytes && pipe.sp1 * 8192 <= pipe.stage_bytes && pipe.sp0 > 0 && pipe.sp1 > 0,
+              "select_tc: bad TVK_SEL_PIPE");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(stc::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = stc::CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, x, T, F, C, K, (const float*)(base + L.blob),
+                                      (const float*)(base + L.maxes), (const double*)(base + L.exact), kappa, kappa1,
+                                      group, debug, pipe, sel, val);
+  if (le != cudaSuccess) {
+    set_error("select_tc launch: %s", cudaGetErrorString(le));
+    return TVK_ERR_CUDA;
+  }
   TVK_CHECK_LAUNCH("select_tc");
   const char* dbg = getenv("TVK_SELECT");
   if (dbg && strcmp(dbg, "tc_noexact") == 0) return TVK_OK;  // diagnostics: leave flagged frames at -1

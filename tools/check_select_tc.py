@@ -97,6 +97,25 @@ def main():
     for mode in ("tc", "dmma"):
         ms = timeit(xb, tab, 2048, 20, mode)
         print(f"{mode}: {ms:.2f} ms / {n} frames -> {n / ms / 1e3:.1f} M frames/s", flush=True)
+    for pipe in ("32768,8,4,64,0", "16384,4,2,64,0", "49152,12,6,64,0", "24576,6,3,64,0"):
+        os.environ["TVK_SEL_PIPE"] = pipe
+        os.environ["TVK_SELECT_DEBUG"] = "2"
+        ms2 = timeit(xb, tab, 2048, 20, "tc_noexact")
+        os.environ.pop("TVK_SELECT_DEBUG")
+        ms = timeit(xb, tab, 2048, 20, "tc_noexact")
+        print(f"pipe {pipe}: pipeline only {ms2:.2f} ms, full {ms:.2f} ms", flush=True)
+    os.environ.pop("TVK_SEL_PIPE")
+    for dbg, what in (("2", "pipeline only"), ("3", "copies only")):
+        os.environ["TVK_SELECT_DEBUG"] = dbg
+        ms = timeit(xb, tab, 2048, 20, "tc_noexact")
+        os.environ.pop("TVK_SELECT_DEBUG")
+        print(f"tc {what}: {ms:.2f} ms", flush=True)
+    for k1 in ("0.0009765625", "0.00048828125", "0.0001220703125", "3.0517578125e-05"):
+        os.environ["TVK_SELECT_KAPPA1"] = k1
+        ms = timeit(xb, tab, 2048, 20, "tc_noexact")
+        f, _ = run(xb, tab, 2048, 20, "tc_noexact")
+        print(f"kappa1 {k1}: {ms:.2f} ms, flagged {int((f[:, 0] == -1).sum().item())}", flush=True)
+    os.environ.pop("TVK_SELECT_KAPPA1")
     ms = timeit(xb, tab, 2048, 20, "tc_noexact")
     f, _ = run(xb, tab, 2048, 20, "tc_noexact")
     print(f"tc without exact pass: {ms:.2f} ms, flagged frames {int((f[:, 0] == -1).sum().item())}", flush=True)

@@ -1,0 +1,24 @@
+"""Per-phase timeline (clock64) of the tcgen05 preselection epilogue, CTA 0 (TVK_SELECT_DEBUG=6)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import bench
+import paper_1906_08556_b200 as pkg
+from paper_1906_08556_b200 import _lib, _device
+n = 2_000_000
+w, mu, cov = bench.make_ubm(0)
+x = bench.sample_frames(w, mu, cov, n, 5, torch.device("cuda"))
+tab = pkg.GmmDiag(w, mu, np.ascontiguousarray(np.diagonal(cov, axis1=1, axis2=2))).device_table()
+for dbg in ("6", "2"):
+    os.environ["TVK_SELECT_DEBUG"] = dbg
+    os.environ["TVK_SELECT"] = "tc_noexact"
+    sel, val = _device.select_topk(x, tab, 20, values=True)
+    sel, val = _device.select_topk(x, tab, 20, values=True)
+    torch.cuda.synchronize()
+    v = val.view(-1)[:64 * 8].cpu().numpy().reshape(64, 8)
+    names = ["start", "pass0 done", "A_lo built", "thr ready", "pass1 done", "nextA built", "merge done", "tile end"]
+    d = np.diff(v[2:12], axis=1)
+    print("debug", dbg, "mean cycles per phase (tiles 2-11):")
+    for i in range(7):
+        print(f"  {names[i]:>12s} -> {names[i + 1]:<12s}: {d[:, i].mean():9.0f}")
+    print("  tile total:", np.diff(v[2:12, 0]).mean())
