@@ -141,6 +141,71 @@ def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True, den
     return res
 
 
+STREAM_CHUNK = 1 << 20  # frames per chunk of the host-input alignment pipeline
+
+
+def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
+    """Frame posteriors of HOST frames with the copies overlapped (align_frames' host path).
+
+    The frames are cut into ``chunk``-frame pieces: the host->device copy of piece i+1 (copy
+    stream), the alignment kernels of piece i (compute stream) and the device->host copy of
+    piece i-1's CSR (drain stream) run concurrently.  Returns host (offsets, components, weights).
+    """
+    T, F = features.shape
+    if isinstance(features, torch.Tensor):
+        host = features if features.dtype in (torch.float32, torch.float64) else features.to(torch.float64)
+    else:
+        arr = np.asarray(features)
+        if arr.dtype != np.float32:
+            arr = arr.astype(np.float64, copy=False)
+        host = torch.from_numpy(np.ascontiguousarray(arr))
+    host = host.contiguous()
+    k = min(top_k, diag_tab.C)
+    offsets = np.empty(T + 1, np.int64)
+    comps = np.empty(T * k, np.int32)   # untouched capacity is never paged in
+    wts = np.empty(T * k, np.float32)
+    offsets[0] = 0
+    comp_stream = torch.cuda.current_stream()
+    copy_stream, drain_stream = torch.cuda.Stream(), torch.cuda.Stream()
+    bufs = [_lib.empty((min(chunk, T), F), host.dtype) for _ in range(2)]
+    free = [None, None]
+    pending = None
+    base = 0
+
+    def drain(item, base):
+        lo, n, res, done = item
+        with torch.cuda.stream(drain_stream):
+            drain_stream.wait_event(done)
+            off = res.offsets.cpu()  # waits for this piece only
+            e = int(off[n])
+            offsets[lo + 1:lo + n + 1] = off[1:].numpy() + base
+            torch.from_numpy(comps[base:base + e]).copy_(res.components[:e])
+            torch.from_numpy(wts[base:base + e]).copy_(res.weights[:e])
+        return base + e
+
+    for i, lo in enumerate(range(0, T, chunk)):
+        n = min(chunk, T - lo)
+        buf = bufs[i % 2][:n]
+        with torch.cuda.stream(copy_stream):
+            if free[i % 2] is not None:
+                copy_stream.wait_event(free[i % 2])
+            buf.copy_(host[lo:lo + n], non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(copy_stream)
+        comp_stream.wait_event(copied)
+        res = align(buf, diag_tab, full_tab, k, prune, sync_count=False)
+        done = torch.cuda.Event()
+        done.record(comp_stream)
+        free[i % 2] = done
+        if pending is not None:
+            base = drain(pending, base)
+        pending = (lo, n, res, done)
+    if pending is not None:
+        base = drain(pending, base)
+    torch.cuda.current_stream().wait_stream(drain_stream)
+    return offsets, comps[:base], wts[:base]
+
+
 def bw_stats(x, utt_frames, ali_offsets, comps, wts, C, center=None, want_S=False, ssum_acc=None,
              entry_capacity=None):
     """Per-utterance n (U x C), f (U x C x F) [, S (U x C x F x F)] on device (gmm.py:442-492).

@@ -297,3 +297,70 @@ def test_dgemm_matches_torch_fp64(gpu):
     _lib.dgemm(_lib.to_dev(a), _lib.to_dev(a), c2, m, m, k, trans_b=True, splits=8, work=work)
     np.testing.assert_allclose(_lib.to_host(c2), want, rtol=1e-12, atol=1e-10)
     del torch
+
+
+# ---------------------------------------------------------------- host-input pipeline, tcgen05 preselection
+
+
+@pytest.mark.parametrize("pinned", [False, True], ids=["numpy", "pinned"])
+def test_align_host_chunked_pipeline_matches_single_shot(gpu, monkeypatch, pinned):
+    """align_frames on a large HOST input runs the chunked copy/compute/copy pipeline
+    (_device.align_host); its CSR must be identical to the one-shot device path."""
+    import torch
+    (w, mu, var), full, x = orc.posterior_ubm(64, 20, 0.5, seed=21, n_frames=5000)
+    dm, fm = gpu.gmm.GmmDiag(w, mu, var), gpu.gmm.GmmFull(*full)
+    ref = gpu.gmm.align_frames(dm, fm, torch.from_numpy(x).cuda(), top_k=20, prune=0.025)
+    monkeypatch.setattr(gpu._device, "STREAM_CHUNK", 1234)
+    feats = torch.from_numpy(x).pin_memory() if pinned else x
+    got = gpu.gmm.align_frames(dm, fm, feats, top_k=20, prune=0.025)
+    np.testing.assert_array_equal(got.offsets, ref.offsets)
+    np.testing.assert_array_equal(got.components, ref.components)
+    np.testing.assert_array_equal(got.weights, ref.weights)
+
+
+def _select(gpu, x, dm, k, mode, monkeypatch, values=True):
+    import torch
+    monkeypatch.setenv("TVK_SELECT", mode)
+    xd = gpu._device.frames_to_device(x)
+    sel, val = gpu._device.select_topk(xd, dm.device_table(), k, values=values)
+    torch.cuda.synchronize()
+    return sel.cpu().numpy(), (val.cpu().numpy() if val is not None else None)
+
+
+@pytest.mark.parametrize("C,F,k,sd", [(2048, 60, 20, 0.3), (100, 13, 7, 0.5), (300, 63, 32, 0.5), (20, 5, 20, 0.5),
+                                      (129, 8, 1, 0.5), (700, 24, 20, 3.0)],
+                         ids=["config2", "C100", "F63K32", "C=K", "K1", "spread"])
+def test_tensor_core_preselection_is_exact(gpu, monkeypatch, C, F, k, sd):
+    """The 3xTF32 tcgen05 preselection (select_tc.cu) returns exactly the stable top-K of the FP64
+    scores: same indices and order as the FP64 DMMA kernel and the oracle's stable argsort."""
+    (w, mu, var), _, x = orc.posterior_ubm(C, F, sd, seed=C + F, n_frames=3000)
+    dm = gpu.gmm.GmmDiag(w, mu, var)
+    a, av = _select(gpu, x, dm, k, "tc", monkeypatch)
+    ll = orc.diag_loglik(w, mu, var, x.astype(np.float64))
+    ref = np.argsort(-ll, axis=1, kind="stable")[:, :k]
+    np.testing.assert_array_equal(a, ref)
+    np.testing.assert_allclose(av, np.take_along_axis(ll, ref, 1), rtol=1e-12, atol=1e-9)
+    if F <= 60 and k <= 20:
+        b, _ = _select(gpu, x, dm, k, "dmma", monkeypatch)
+        np.testing.assert_array_equal(a, b)
+
+
+def test_tensor_core_preselection_exact_ties_and_degenerate_frames(gpu, monkeypatch):
+    """Duplicated components (exact ties -> lower index first), all-zero and NaN frames (the exact
+    fallback kernel) and frames whose windows overflow under a deliberately tiny pass-0 slack."""
+    (w, mu, var), _, x = orc.posterior_ubm(64, 10, 0.5, seed=9, n_frames=1000)
+    mu[32:], var[32:], w[32:] = mu[:32], var[:32], w[:32]
+    w = w / w.sum()
+    x[5] = 0.0
+    x[7, 3] = np.nan
+    dm = gpu.gmm.GmmDiag(w, mu, var)
+    ll = orc.diag_loglik(w, mu, var, x.astype(np.float64))
+    ref = np.argsort(-ll, axis=1, kind="stable")[:, :20]
+    for kappa1 in (None, "1e-9", "1.0"):
+        if kappa1:
+            monkeypatch.setenv("TVK_SELECT_KAPPA1", kappa1)
+        a, _ = _select(gpu, x, dm, 20, "tc", monkeypatch, values=False)
+        ok = np.ones(len(x), bool)
+        ok[7] = False  # NaN frame: the reference order of NaN scores is index order (checked below)
+        np.testing.assert_array_equal(a[ok], ref[ok])
+        np.testing.assert_array_equal(a[7], np.arange(20))
