@@ -1,17 +1,18 @@
 // Grouped full-covariance log-likelihoods of the preselected components (default alignment path).
 //
 // The reference evaluates the full-covariance log-likelihood of all C components and keeps the
-// K preselected ones (gmm.py:412-413).  Only those K values reach the output, so this path
-// evaluates exactly the T*K (frame, component) pairs:
+// K preselected ones (gmm.py:412-413), each by a Cholesky factor and a triangular solve
+// (gmm.py:111-118: ll = log w - (F log 2pi + log|Sigma|)/2 - ||L^-1 (x - mu)||^2 / 2).  Only the K
+// selected values reach the output, so this path evaluates exactly the T*K (frame, component) pairs:
 //   1. pairs are bucketed by component (block-local counting sort, one global atomic per
-//      (block, component) to reserve a range);
-//   2. grouped_ll_kernel walks the sorted pairs in 128-row tiles; per component run it stages
-//      P_c = Sigma_c^-1 (F x F, zero-padded to 64) and Y = x - mu_c in shared memory and forms
-//      Z = Y P_c on the FP64 tensor pipe (DMMA.8x8x4); q = rowsum(Z o Y) = (x-mu)' P (x-mu);
+//      (block, component) to reserve a range) and cut into per-component tiles of <= 128 pairs;
+//   2. whiten_ll_kernel (persistent, one CTA per SM) gathers the tile's frame rows with cp.async
+//      (double-buffered against the math of the previous tile), forms Z = (X - mu) U with
+//      U = L^-T upper triangular on the FP64 tensor pipe (DMMA.8x8x4, the zero blocks of U are
+//      skipped: 56% of the dense work), and q = rowsum(Z o Z) = ||L^-1 (x - mu)||^2;
 //      ll = log w_c - (F log 2pi + log|Sigma_c|)/2 - q/2, scattered to sel_ll[t*K + j].
 // Each pair's arithmetic is independent of its position in the sort, so the output is
-// bit-reproducible although the bucket order is not.  Work per frame: K*F*64 MACs (2.5% of the
-// dense quadratic-feature GEMM at C=2048, K=20).
+// bit-reproducible although the bucket order is not.
 #include <math.h>
 
 #include "common.cuh"
@@ -22,16 +23,17 @@ namespace tvk {
 
 constexpr int GP = 64;          // padded feature width (F <= 64)
 constexpr int GROWS = 128;      // pairs per tile
-constexpr int GT = 256;         // threads
-constexpr int GS = GP + 4;      // smem row stride (== 4 mod 16: conflict-free fragments)
+constexpr int GT = 256;         // threads (8 warps of 32 rows x 4 column blocks)
+constexpr int GS = GP + 4;      // smem row stride of U (doubles) and of the frame rows (elements)
 constexpr int kSortChunk = 4096;
 constexpr int64_t kGroupWindowFrames = 131072;  // 31 MB of f32 frames per window
 
+// Whitening table row: [U = L^-T (64 x 64, zero padded) | mu (64) | const | pad],
+// const = log w_c - (F log 2pi + log|Sigma_c|)/2.
+constexpr int64_t kWhitenStride = GP * GP + GP + 4;
 
-
-// [P_c (F x F) | mu_c (F) | const_c | pad], const_c = log w_c - (F log 2pi + log|Sigma_c|)/2
-__global__ void precision_table_kernel(const double* w, const double* mu, const double* cov, int C, int F,
-                                       double* ptab, int32_t* status) {
+__global__ void whiten_table_kernel(const double* w, const double* mu, const double* cov, int C, int F,
+                                    double* tab, int32_t* status) {
   extern __shared__ double sm[];
   double* a = sm;
   double* y = sm + F * F;
@@ -39,6 +41,7 @@ __global__ void precision_table_kernel(const double* w, const double* mu, const 
   __shared__ double logdet;
   const int c = blockIdx.x;
   const double* src = cov + (int64_t)c * F * F;
+  double* dst = tab + (int64_t)c * kWhitenStride;
   for (int i = threadIdx.x; i < F * F; i += blockDim.x) a[i] = src[i];
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
@@ -53,14 +56,25 @@ __global__ void precision_table_kernel(const double* w, const double* mu, const 
     s = warp_sum(s);
     if (threadIdx.x == 0) logdet = 2.0 * s;
   }
+  // y = L^-1 (lower triangular), column-parallel forward substitution
+  for (int j = threadIdx.x; j < F; j += blockDim.x) {
+    for (int i = 0; i < j; i++) y[i * F + j] = 0.0;
+    y[j * F + j] = 1.0 / a[j * F + j];
+    for (int i = j + 1; i < F; i++) {
+      double s = 0.0;
+      for (int k = j; k < i; k++) s += a[i * F + k] * y[k * F + j];
+      y[i * F + j] = -s / a[i * F + i];
+    }
+  }
   __syncthreads();
-  block_spd_inverse(a, y, F);
-  double* dst = ptab + (int64_t)c * precision_stride(F);
-  for (int i = threadIdx.x; i < F * F; i += blockDim.x) dst[i] = a[i];
-  for (int i = threadIdx.x; i < F; i += blockDim.x) dst[F * F + i] = mu[(int64_t)c * F + i];
+  for (int idx = threadIdx.x; idx < GP * GP; idx += blockDim.x) {  // U[i][j] = y[j][i]
+    int i = idx / GP, j = idx % GP;
+    dst[idx] = (i < F && j < F && j >= i) ? y[j * F + i] : 0.0;
+  }
+  for (int i = threadIdx.x; i < GP; i += blockDim.x) dst[GP * GP + i] = i < F ? mu[(int64_t)c * F + i] : 0.0;
   if (threadIdx.x == 0) {
-    dst[F * F + F] = log(w[c]) - 0.5 * (F * kLog2Pi + logdet);
-    dst[F * F + F + 1] = 0.0;
+    dst[GP * GP + GP] = log(w[c]) - 0.5 * (F * kLog2Pi + logdet);
+    dst[GP * GP + GP + 1] = dst[GP * GP + GP + 2] = dst[GP * GP + GP + 3] = 0.0;
     status[c] = TVK_ITEM_OK;
   }
 }
@@ -130,109 +144,146 @@ __global__ void pair_scatter_kernel(const int32_t* sel, int64_t n_pairs, int C, 
   }
 }
 
+// per-component tiles of <= GROWS sorted pairs: tile descriptors (first sorted index, rows, comp)
+__global__ void tile_count_kernel(const int* hist, int C, int* ntile) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) ntile[c] = (hist[c] + GROWS - 1) / GROWS;
+}
+__global__ void tile_build_kernel(const int* hist, const int* start, const int* tile_start, int C, int4* tiles) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  int n = hist[c], t0 = tile_start[c];
+  for (int i = 0; i * GROWS < n; i++) tiles[t0 + i] = make_int4(start[c] + i * GROWS, min(GROWS, n - i * GROWS), c, 0);
+}
+
 template <typename XT>
-__global__ void __launch_bounds__(GT) grouped_ll_kernel(const XT* x, int F, const double* ptab, const int32_t* sel,
-                                                        int K, const int32_t* sorted, int64_t n_pairs,
-                                                        double* sel_ll) {
-  extern __shared__ __align__(16) double sm[];
-  double* sP = sm;                 // [GP][GS]
-  double* sY = sP + GP * GS;       // [GROWS][GS]
-  double* sMu = sY + GROWS * GS;   // [GP]
-  double* part = sMu + GP;         // [GROWS][2]
-  int* sPair = reinterpret_cast<int*>(part + 2 * GROWS);  // [GROWS]
-  int* sComp = sPair + GROWS;                              // [GROWS]
-  __shared__ int loaded_comp;
-  __shared__ double sConst;
+struct WhitenSmem {
+  double U[2][GP * GS];     // U of the current / next component
+  double mu[2][GP];
+  double cst[2][2];         // const, pad (one 16-byte copy)
+  XT X[2][GROWS * GS];      // raw frame rows (columns F..63 stay zero)
+  int pair[2][GROWS];
+  double part[GROWS][2];
+};
+
+template <int BYTES>  // 4 or 8: one frame element
+__device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+}
+
+// One warp's 32 x 32 block of Z = Y U: rows wm*32.., column blocks n = wn, wn+2, wn+4, wn+6 (8 wide,
+// interleaved so both warp columns get similar triangular work); k-step kk (4 wide) is needed by
+// column block n only when 4 kk <= 8 n + 7.
+template <int WN, typename XT>
+__device__ __forceinline__ void whiten_mma(const XT* X, const double* U, const double* mu, int wm, int g, int t4,
+                                           double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int kk = 0; kk < GP / 4; kk++) {
+    const int k = kk * 4 + t4;
+    const double m = mu[k];
+    double a[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) a[i] = (double)X[(wm * 32 + i * 8 + g) * GS + k] - m;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      if (kk <= 2 * (WN + 2 * j) + 1) {
+        const double b = U[k * GS + (WN + 2 * j) * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 4; i++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
+      }
+    }
+  }
+}
+
+template <typename XT, bool VEC>
+__global__ void __launch_bounds__(GT, 1)
+    whiten_ll_kernel(const XT* __restrict__ x, int F, const double* __restrict__ tab, int K,
+                     const int32_t* __restrict__ sorted, const int4* __restrict__ tiles, const int* __restrict__ ntile_p,
+                     double* __restrict__ sel_ll) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  WhitenSmem<XT>& S = *reinterpret_cast<WhitenSmem<XT>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps of 32x32
+  const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t4 = lane & 3;
-  const int64_t PS = precision_stride(F);
-  if (tid == 0) loaded_comp = -1;
-  for (int i = tid; i < GP * GS; i += GT) sP[i] = 0.0;
-  for (int i = tid; i < GROWS * GS; i += GT) sY[i] = 0.0;
+  const int ntiles = *ntile_p;
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int tb = blockIdx.x * per, te = min(tb + per, ntiles);
+  if (tb >= te) return;
+  for (int i = tid; i < 2 * GROWS * GS; i += GT) (&S.X[0][0])[i] = (XT)0;
   __syncthreads();
 
-  // contiguous tile range per CTA: consecutive tiles mostly share a component (P_c stays staged)
-  const int64_t ntiles = (n_pairs + GROWS - 1) / GROWS;
-  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int64_t tile_end = min((int64_t)(blockIdx.x + 1) * per, ntiles);
-  for (int64_t tile = blockIdx.x * per; tile < tile_end; tile++) {
-    const int64_t s0 = tile * GROWS;
-    const int nrow = (int)((n_pairs - s0) < GROWS ? (n_pairs - s0) : GROWS);
-    for (int r = tid; r < GROWS; r += GT) {
-      int p = r < nrow ? sorted[s0 + r] : -1;
-      sPair[r] = p;
-      sComp[r] = p >= 0 ? sel[p] : -1;
+  // issue the copies of tile ti into buffer b (frame rows always, U/mu/const when ucopy)
+  auto issue = [&](int ti, int b, int u, bool ucopy) {
+    const int4 d = tiles[ti];
+    for (int r = tid; r < GROWS; r += GT) S.pair[b][r] = r < d.y ? sorted[d.x + r] : -1;
+    if (ucopy) {
+      const double* src = tab + (int64_t)d.z * kWhitenStride;
+      for (int i = tid; i < GP * GP / 2; i += GT) {  // 16-byte pieces of U rows
+        const int row = i / (GP / 2), c2 = i % (GP / 2);
+        cp_async16(&S.U[u][row * GS + 2 * c2], src + row * GP + 2 * c2, 16);
+      }
+      for (int i = tid; i < GP / 2 + 1; i += GT) {
+        if (i < GP / 2) cp_async16(&S.mu[u][2 * i], src + GP * GP + 2 * i, 16);
+        else cp_async16(&S.cst[u][0], src + GP * GP + GP, 16);
+      }
+    }
+    // frame rows: row r <- x[sorted / K], F elements
+    const int per_row = VEC ? (F * (int)sizeof(XT)) / 16 : F;
+    for (int i = tid; i < GROWS * per_row; i += GT) {
+      const int r = i / per_row, c = i - r * per_row;
+      if (r >= d.y) continue;
+      const int64_t t = (int64_t)sorted[d.x + r] / K;
+      if (VEC) cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
+                          reinterpret_cast<const uint8_t*>(x + t * F) + 16 * c, 16);
+      else cp_async_elem<(int)sizeof(XT)>(&S.X[b][r * GS + c], x + t * F + c);
+    }
+    cp_async_commit();
+  };
+
+  int ub = 0, comp = tiles[tb].z;
+  issue(tb, 0, 0, true);
+  for (int ti = tb; ti < te; ti++) {
+    const int xb = (ti - tb) & 1;
+    const int4 d = tiles[ti];
+    // prefetch the next tile into the other buffers (U only when the component changes)
+    int nub = ub;
+    if (ti + 1 < te) {
+      const int nc = tiles[ti + 1].z;
+      nub = nc == comp ? ub : ub ^ 1;
+      issue(ti + 1, xb ^ 1, nub, nc != comp);
+      comp = nc;
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    int r0 = 0;
-    while (r0 < nrow) {
-      const int c = sComp[r0];
-      int r1 = r0 + 1;
-      while (r1 < nrow && sComp[r1] == c) r1++;
-      // stage P_c and mu_c unless already resident
-      if (c != loaded_comp) {
-        const double* src = ptab + (int64_t)c * PS;
-        for (int i = tid; i < F * F; i += GT) sP[(i / F) * GS + (i % F)] = src[i];
-        for (int i = tid; i < F; i += GT) sMu[i] = src[F * F + i];
-        if (tid == 0) sConst = src[F * F + F];
-      }
-      __syncthreads();
-      if (tid == 0) loaded_comp = c;
-      // Y rows of this run (rows outside the run are zero)
-      for (int idx = tid; idx < GROWS * F; idx += GT) {
-        int r = idx / F, f = idx % F;
-        double v = 0.0;
-        if (r >= r0 && r < r1) {
-          int64_t tf = sPair[r] / K;
-          v = (double)x[tf * F + f] - sMu[f];
-        }
-        sY[r * GS + f] = v;
-      }
-      __syncthreads();
-      // Z = Y P on the tensor pipe: warp (wm, wn) owns rows wm*32.., cols wn*32..
-      double acc[4][4][2];
+    // rows past the tile's pairs hold stale frames: their (finite) results are never stored
+    double acc[4][4][2];
 #pragma unroll
-      for (int i = 0; i < 4; i++)
+    for (int i = 0; i < 4; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-      const bool live = (wm * 32 < r1) && (wm * 32 + 32 > r0);
-      if (live) {
-#pragma unroll 4
-        for (int kk = 0; kk < GP; kk += 4) {
-          double a[4], b[4];
-#pragma unroll
-          for (int i = 0; i < 4; i++) a[i] = sY[(wm * 32 + i * 8 + g) * GS + kk + t4];
-#pragma unroll
-          for (int j = 0; j < 4; j++) b[j] = sP[(kk + t4) * GS + wn * 32 + j * 8 + g];
-#pragma unroll
-          for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int j = 0; j < 4; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-        }
-      }
-      // q partial = sum over this warp's 32 columns of Z o Y
-#pragma unroll
-      for (int i = 0; i < 4; i++) {
-        int r = wm * 32 + i * 8 + g;
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          int col = wn * 32 + j * 8 + 2 * t4;
-          s += acc[i][j][0] * sY[r * GS + col] + acc[i][j][1] * sY[r * GS + col + 1];
-        }
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (t4 == 0) part[r * 2 + wn] = s;
-      }
-      __syncthreads();
-      for (int r = r0 + tid; r < r1; r += GT) {
-        double q = part[r * 2] + part[r * 2 + 1];
-        sel_ll[sPair[r]] = sConst - 0.5 * q;
-      }
-      __syncthreads();
-      r0 = r1;
+      for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (wm * 32 < d.y) {
+      if (wn == 0) whiten_mma<0>(S.X[xb], S.U[ub], S.mu[ub], wm, g, t4, acc);
+      else whiten_mma<1>(S.X[xb], S.U[ub], S.mu[ub], wm, g, t4, acc);
     }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) s += acc[i][j][0] * acc[i][j][0] + acc[i][j][1] * acc[i][j][1];
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (t4 == 0) S.part[wm * 32 + i * 8 + g][wn] = s;
+    }
+    __syncthreads();
+    for (int r = tid; r < d.y; r += GT) sel_ll[S.pair[xb][r]] = S.cst[ub][0] - 0.5 * (S.part[r][0] + S.part[r][1]);
+    ub = nub;
+    // the next iteration's prefetch overwrites this tile's buffers only after its own barrier
+    __syncthreads();
   }
 }
 
@@ -240,6 +291,9 @@ struct GroupWs {
   int* hist;
   int* start;
   int* cursor;
+  int* ntile;
+  int* tile_start;
+  int4* tiles;
   int32_t* sorted;
   size_t bytes;
 };
@@ -258,6 +312,9 @@ static GroupWs group_carve(void* base, int64_t n_pairs, int C) {
   w.hist = (int*)take(sizeof(int) * C);
   w.start = (int*)take(sizeof(int) * (C + 1));
   w.cursor = (int*)take(sizeof(int) * C);
+  w.ntile = (int*)take(sizeof(int) * C);
+  w.tile_start = (int*)take(sizeof(int) * (C + 1));
+  w.tiles = (int4*)take(sizeof(int4) * (n_pairs / GROWS + C + 1));
   w.sorted = (int32_t*)take(sizeof(int32_t) * (n_pairs + 1));
   w.bytes = off;
   return w;
@@ -267,6 +324,16 @@ int64_t grouped_workspace_bytes(int64_t n_pairs, int C) {
   return (int64_t)group_carve(nullptr, std::min<int64_t>(n_pairs, kGroupWindowFrames * 32), C).bytes;
 }
 
+template <typename XT, bool VEC>
+static int launch_whiten(const XT* x, int F, const double* tab, int K, const GroupWs& w, double* sel_ll, int sms,
+                         cudaStream_t st) {
+  const size_t smem = sizeof(WhitenSmem<XT>);
+  cudaFuncSetAttribute(whiten_ll_kernel<XT, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  whiten_ll_kernel<XT, VEC><<<sms, GT, smem, st>>>(x, F, tab, K, w.sorted, w.tiles, w.tile_start + 0, sel_ll);
+  TVK_CHECK_LAUNCH("whiten_ll");
+  return TVK_OK;
+}
+
 template <typename XT>
 int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, int K, const int32_t* sel,
                     double* sel_ll, void* ws_base, int64_t ws_bytes, cudaStream_t st) {
@@ -274,19 +341,17 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
   TVK_REQUIRE(C <= 8192, "grouped full log-likelihood supports C <= 8192");
   const int64_t n_pairs = T * K;
   TVK_REQUIRE(n_pairs < (1ll << 31) - 1, "too many (frame, component) pairs for one call");
-  // frame windows sized so the window's frames and the precision table stay L2-resident while the
+  // frame windows sized so the window's frames and the whitening table stay L2-resident while the
   // window's pairs (sorted by component, i.e. random in frame order) gather their frame rows
   const int64_t win = std::min<int64_t>(T, kGroupWindowFrames);
   GroupWs w = group_carve(ws_base, win * K, C);
   TVK_REQUIRE(ws_base != nullptr && (int64_t)w.bytes <= ws_bytes, "grouped full log-likelihood: workspace too small");
   size_t sc_smem = sizeof(int) * 2 * C;
   cudaFuncSetAttribute(pair_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
-  size_t smem = sizeof(double) * (GP * GS + GROWS * GS + GP + 2 * GROWS) + sizeof(int) * 2 * GROWS;
-  cudaFuncSetAttribute(grouped_ll_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, sms = 148, per = 1;
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, grouped_ll_kernel<XT>, GT, smem);
+  const bool vec = ((F * sizeof(XT)) % 16 == 0) && ((uintptr_t)x % 16 == 0);
   for (int64_t f0 = 0; f0 < T; f0 += win) {
     const int64_t nf = std::min<int64_t>(win, T - f0);
     const int64_t np = nf * K;
@@ -296,11 +361,17 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
     pair_hist_kernel<<<nchunks, GT, sizeof(int) * C, st>>>(wsel, np, C, w.hist);
     hist_scan_kernel<<<1, 1024, 0, st>>>(w.hist, C, w.start, w.cursor);
     pair_scatter_kernel<<<nchunks, GT, sc_smem, st>>>(wsel, np, C, w.cursor, w.sorted);
+    tile_count_kernel<<<(C + 255) / 256, 256, 0, st>>>(w.hist, C, w.ntile);
+    hist_scan_kernel<<<1, 1024, 0, st>>>(w.ntile, C, w.tile_start, w.cursor);
+    tile_build_kernel<<<(C + 255) / 256, 256, 0, st>>>(w.hist, w.start, w.tile_start, C, w.tiles);
     TVK_CHECK_LAUNCH("pair sort");
-    int64_t ntiles = (np + GROWS - 1) / GROWS;
-    int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * std::max(per, 1));
-    grouped_ll_kernel<XT><<<grid, GT, smem, st>>>(x + f0 * F, F, ptab, wsel, K, w.sorted, np, sel_ll + f0 * K);
-    TVK_CHECK_LAUNCH("grouped_ll");
+    // the kernel reads the tile count from tile_start[C]
+    GroupWs wc = w;
+    wc.tile_start = w.tile_start + C;
+    if (vec)
+      TVK_TRY((launch_whiten<XT, true>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, st)));
+    else
+      TVK_TRY((launch_whiten<XT, false>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, st)));
   }
   return TVK_OK;
 }
@@ -314,12 +385,11 @@ template int grouped_full_ll<double>(const double*, int64_t, int, const double*,
 
 extern "C" int tvk_precision_table(const double* weights, const double* means, const double* covariances, int C,
                                    int F, double* table, int32_t* status, void* stream) {
-  TVK_REQUIRE(C >= 1 && F >= 1 && F <= tvk::kSmallSpdMax, "precision_table: need 1 <= F <= 96");
+  TVK_REQUIRE(C >= 1 && F >= 1 && F <= tvk::GP, "precision_table: need 1 <= F <= 64");
   size_t smem = 2 * sizeof(double) * F * F;
-  cudaFuncSetAttribute(tvk::precision_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(2 * sizeof(double) * tvk::kSmallSpdMax * tvk::kSmallSpdMax));
-  tvk::precision_table_kernel<<<C, 256, smem, (cudaStream_t)stream>>>(weights, means, covariances, C, F, table,
-                                                                      status);
+  cudaFuncSetAttribute(tvk::whiten_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(2 * sizeof(double) * tvk::GP * tvk::GP));
+  tvk::whiten_table_kernel<<<C, 256, smem, (cudaStream_t)stream>>>(weights, means, covariances, C, F, table, status);
   TVK_CHECK_LAUNCH("precision_table");
   return TVK_OK;
 }

@@ -32,7 +32,7 @@ int spd_small(const double* A, int batch, int n, double* chol, double* inv, doub
 
 namespace tvk {
 // grouped (selected-only) full-covariance log-likelihoods, align_grouped.cu
-__host__ __device__ inline int64_t precision_stride(int F) { return (int64_t)F * F + F + 2; }
+__host__ __device__ inline int64_t precision_stride(int) { return 64 * 64 + 64 + 4; }  // whitening table row
 int64_t grouped_workspace_bytes(int64_t n_pairs, int C);
 template <typename XT>
 int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, int K, const int32_t* sel,
