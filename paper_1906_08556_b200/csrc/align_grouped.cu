@@ -158,9 +158,9 @@ __global__ void tile_build_kernel(const int* hist, const int* start, const int* 
 
 template <typename XT>
 struct WhitenSmem {
-  double U[2][GP * GS];     // U of the current / next component
-  double mu[2][GP];
-  double cst[2][2];         // const, pad (one 16-byte copy)
+  double U[GP * GS];        // U of the staged component (single buffer: 2 CTAs fit per SM)
+  double mu[GP];
+  double cst[2];            // const, pad (one 16-byte copy)
   XT X[2][GROWS * GS];      // raw frame rows (columns F..63 stay zero)
   int pair[2][GROWS];
   double part[GROWS][2];
@@ -199,7 +199,7 @@ __device__ __forceinline__ void whiten_mma(const XT* X, const double* U, const d
 }
 
 template <typename XT, bool VEC>
-__global__ void __launch_bounds__(GT, 1)
+__global__ void __launch_bounds__(GT, 2)
     whiten_ll_kernel(const XT* __restrict__ x, int F, const double* __restrict__ tab, int K,
                      const int32_t* __restrict__ sorted, const int4* __restrict__ tiles, const int* __restrict__ ntile_p,
                      double* __restrict__ sel_ll) {
@@ -216,45 +216,52 @@ __global__ void __launch_bounds__(GT, 1)
   __syncthreads();
 
   // issue the copies of tile ti into buffer b (frame rows always, U/mu/const when ucopy)
-  auto issue = [&](int ti, int b, int u, bool ucopy) {
+  auto stage_U = [&](int c) {  // U, mu, const of component c
+    const double* src = tab + (int64_t)c * kWhitenStride;
+    for (int i = tid; i < GP * GP / 2; i += GT) {  // 16-byte pieces of U rows
+      const int row = i / (GP / 2), c2 = i % (GP / 2);
+      cp_async16(&S.U[row * GS + 2 * c2], src + row * GP + 2 * c2, 16);
+    }
+    for (int i = tid; i < GP / 2 + 1; i += GT) {
+      if (i < GP / 2) cp_async16(&S.mu[2 * i], src + GP * GP + 2 * i, 16);
+      else cp_async16(&S.cst[0], src + GP * GP + GP, 16);
+    }
+    cp_async_commit();
+  };
+  auto issue = [&](int ti, int b) {
     const int4 d = tiles[ti];
     for (int r = tid; r < GROWS; r += GT) S.pair[b][r] = r < d.y ? sorted[d.x + r] : -1;
-    if (ucopy) {
-      const double* src = tab + (int64_t)d.z * kWhitenStride;
-      for (int i = tid; i < GP * GP / 2; i += GT) {  // 16-byte pieces of U rows
-        const int row = i / (GP / 2), c2 = i % (GP / 2);
-        cp_async16(&S.U[u][row * GS + 2 * c2], src + row * GP + 2 * c2, 16);
-      }
-      for (int i = tid; i < GP / 2 + 1; i += GT) {
-        if (i < GP / 2) cp_async16(&S.mu[u][2 * i], src + GP * GP + 2 * i, 16);
-        else cp_async16(&S.cst[u][0], src + GP * GP + GP, 16);
-      }
-    }
-    // frame rows: row r <- x[sorted / K], F elements
+    // frame rows: row r <- x[sorted / K], F elements; warp w copies rows w, w+8, ... (lanes over
+    // 16-byte pieces), lane j first fetches the frame index of the warp's j-th row
     const int per_row = VEC ? (F * (int)sizeof(XT)) / 16 : F;
-    for (int i = tid; i < GROWS * per_row; i += GT) {
-      const int r = i / per_row, c = i - r * per_row;
-      if (r >= d.y) continue;
-      const int64_t t = (int64_t)sorted[d.x + r] / K;
-      if (VEC) cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
-                          reinterpret_cast<const uint8_t*>(x + t * F) + 16 * c, 16);
-      else cp_async_elem<(int)sizeof(XT)>(&S.X[b][r * GS + c], x + t * F + c);
+    const int myrow = warp + (GT / 32) * lane;
+    const int myframe = (lane < GROWS / (GT / 32) && myrow < d.y) ? sorted[d.x + myrow] / K : 0;
+    for (int j = 0; j < GROWS / (GT / 32); j++) {
+      const int r = warp + (GT / 32) * j;
+      const int fr = __shfl_sync(0xffffffffu, myframe, j);
+      if (r >= d.y) break;
+      const XT* src = x + (int64_t)fr * F;
+      for (int c = lane; c < per_row; c += 32) {
+        if (VEC) cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
+                            reinterpret_cast<const uint8_t*>(src) + 16 * c, 16);
+        else cp_async_elem<(int)sizeof(XT)>(&S.X[b][r * GS + c], src + c);
+      }
     }
     cp_async_commit();
   };
 
-  int ub = 0, comp = tiles[tb].z;
-  issue(tb, 0, 0, true);
+  int comp = -1;
+  issue(tb, 0);
   for (int ti = tb; ti < te; ti++) {
     const int xb = (ti - tb) & 1;
     const int4 d = tiles[ti];
-    // prefetch the next tile into the other buffers (U only when the component changes)
-    int nub = ub;
+    if (d.z != comp) {  // new component: stage U (the previous tile's math is done)
+      stage_U(d.z);
+      comp = d.z;
+    }
+    // prefetch the next tile's frame rows into the other buffer
     if (ti + 1 < te) {
-      const int nc = tiles[ti + 1].z;
-      nub = nc == comp ? ub : ub ^ 1;
-      issue(ti + 1, xb ^ 1, nub, nc != comp);
-      comp = nc;
+      issue(ti + 1, xb ^ 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -267,8 +274,8 @@ __global__ void __launch_bounds__(GT, 1)
 #pragma unroll
       for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
     if (wm * 32 < d.y) {
-      if (wn == 0) whiten_mma<0>(S.X[xb], S.U[ub], S.mu[ub], wm, g, t4, acc);
-      else whiten_mma<1>(S.X[xb], S.U[ub], S.mu[ub], wm, g, t4, acc);
+      if (wn == 0) whiten_mma<0>(S.X[xb], S.U, S.mu, wm, g, t4, acc);
+      else whiten_mma<1>(S.X[xb], S.U, S.mu, wm, g, t4, acc);
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) {
@@ -280,8 +287,7 @@ __global__ void __launch_bounds__(GT, 1)
       if (t4 == 0) S.part[wm * 32 + i * 8 + g][wn] = s;
     }
     __syncthreads();
-    for (int r = tid; r < d.y; r += GT) sel_ll[S.pair[xb][r]] = S.cst[ub][0] - 0.5 * (S.part[r][0] + S.part[r][1]);
-    ub = nub;
+    for (int r = tid; r < d.y; r += GT) sel_ll[S.pair[xb][r]] = S.cst[0] - 0.5 * (S.part[r][0] + S.part[r][1]);
     // the next iteration's prefetch overwrites this tile's buffers only after its own barrier
     __syncthreads();
   }
@@ -329,7 +335,7 @@ static int launch_whiten(const XT* x, int F, const double* tab, int K, const Gro
                          cudaStream_t st) {
   const size_t smem = sizeof(WhitenSmem<XT>);
   cudaFuncSetAttribute(whiten_ll_kernel<XT, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  whiten_ll_kernel<XT, VEC><<<sms, GT, smem, st>>>(x, F, tab, K, w.sorted, w.tiles, w.tile_start + 0, sel_ll);
+  whiten_ll_kernel<XT, VEC><<<2 * sms, GT, smem, st>>>(x, F, tab, K, w.sorted, w.tiles, w.tile_start + 0, sel_ll);
   TVK_CHECK_LAUNCH("whiten_ll");
   return TVK_OK;
 }
