@@ -142,15 +142,30 @@ def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True, den
 
 
 STREAM_CHUNK = 1 << 20  # frames per chunk of the host-input alignment pipeline
+_staging = {}             # (chunk, k) -> pinned host staging slots, reused across calls
+_copier = None
+
+
+def _pinned_slots(chunk, k):
+    key = (chunk, k)
+    if key not in _staging:
+        _staging.clear()
+        _staging[key] = [(torch.empty(chunk + 1, dtype=torch.int64, pin_memory=True),
+                          torch.empty(chunk * k, dtype=torch.int32, pin_memory=True),
+                          torch.empty(chunk * k, dtype=torch.float32, pin_memory=True)) for _ in range(2)]
+    return _staging[key]
 
 
 def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
-    """Frame posteriors of HOST frames with the copies overlapped (align_frames' host path).
+    """Frame posteriors of HOST frames with every copy overlapped (align_frames' host path).
 
-    The frames are cut into ``chunk``-frame pieces: the host->device copy of piece i+1 (copy
-    stream), the alignment kernels of piece i (compute stream) and the device->host copy of
-    piece i-1's CSR (drain stream) run concurrently.  Returns host (offsets, components, weights).
+    The frames are cut into ``chunk``-frame pieces.  Piece i+1's host->device copy (copy stream),
+    piece i's alignment kernels (compute stream), piece i-1's device->host copy of its CSR into
+    pinned staging (drain stream) and piece i-2's copy from staging into the returned arrays (a
+    host worker thread) all run concurrently.  Returns host (offsets, components, weights).
     """
+    global _copier
+    import concurrent.futures as cf
     T, F = features.shape
     if isinstance(features, torch.Tensor):
         host = features if features.dtype in (torch.float32, torch.float64) else features.to(torch.float64)
@@ -161,28 +176,49 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
         host = torch.from_numpy(np.ascontiguousarray(arr))
     host = host.contiguous()
     k = min(top_k, diag_tab.C)
+    chunk = min(chunk, T)
     offsets = np.empty(T + 1, np.int64)
     comps = np.empty(T * k, np.int32)   # untouched capacity is never paged in
     wts = np.empty(T * k, np.float32)
     offsets[0] = 0
+    if _copier is None:
+        _copier = cf.ThreadPoolExecutor(max_workers=1, thread_name_prefix="tvk-copy")
+    slots = _pinned_slots(chunk, k)
+    slot_busy = [None, None]
     comp_stream = torch.cuda.current_stream()
     copy_stream, drain_stream = torch.cuda.Stream(), torch.cuda.Stream()
-    bufs = [_lib.empty((min(chunk, T), F), host.dtype) for _ in range(2)]
+    bufs = [_lib.empty((chunk, F), host.dtype) for _ in range(2)]
     free = [None, None]
     pending = None
     base = 0
 
-    def drain(item, base):
+    def unstage(lo, n, e, base, st, ev):
+        ev.synchronize()
+        off_st, c_st, w_st = st
+        np.add(off_st[1:n + 1].numpy(), base, out=offsets[lo + 1:lo + n + 1])
+        comps[base:base + e] = c_st[:e].numpy()
+        wts[base:base + e] = w_st[:e].numpy()
+
+    def drain(item, base, slot):
         lo, n, res, done = item
+        if slot_busy[slot] is not None:
+            slot_busy[slot].result()  # staging slot free again
+        st = slots[slot]
         with torch.cuda.stream(drain_stream):
             drain_stream.wait_event(done)
-            off = res.offsets.cpu()  # waits for this piece only
-            e = int(off[n])
-            offsets[lo + 1:lo + n + 1] = off[1:].numpy() + base
-            torch.from_numpy(comps[base:base + e]).copy_(res.components[:e])
-            torch.from_numpy(wts[base:base + e]).copy_(res.weights[:e])
+            st[0][:n + 1].copy_(res.offsets, non_blocking=True)
+            got = torch.cuda.Event()
+            got.record(drain_stream)
+            got.synchronize()
+            e = int(st[0][n])
+            st[1][:e].copy_(res.components[:e], non_blocking=True)
+            st[2][:e].copy_(res.weights[:e], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(drain_stream)
+        slot_busy[slot] = _copier.submit(unstage, lo, n, e, base, st, ev)
         return base + e
 
+    nd = 0
     for i, lo in enumerate(range(0, T, chunk)):
         n = min(chunk, T - lo)
         buf = bufs[i % 2][:n]
@@ -198,10 +234,14 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
         done.record(comp_stream)
         free[i % 2] = done
         if pending is not None:
-            base = drain(pending, base)
+            base = drain(pending, base, nd % 2)
+            nd += 1
         pending = (lo, n, res, done)
     if pending is not None:
-        base = drain(pending, base)
+        base = drain(pending, base, nd % 2)
+    for f in slot_busy:
+        if f is not None:
+            f.result()
     torch.cuda.current_stream().wait_stream(drain_stream)
     return offsets, comps[:base], wts[:base]
 

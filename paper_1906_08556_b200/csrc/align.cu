@@ -594,7 +594,7 @@ static bool select_dmma_forced() {  // TVK_SELECT=dmma: the FP64 DMMA preselecti
 template <typename XT>
 static int launch_select(const XT* x, int64_t T, int F, const double* diag_table, int C, int K, int32_t* sel,
                          double* val, cudaStream_t st) {
-  if (select_tc_supported(F, K) && !select_dmma_forced()) return select_tc<XT>(x, T, F, diag_table, C, K, sel, val, st);
+  if (select_tc_supported(F, K, C) && !select_dmma_forced()) return select_tc<XT>(x, T, F, diag_table, C, K, sel, val, st);
   size_t smem = sel::smem_bytes(F, K);
   TVK_REQUIRE(smem <= 227 * 1024, "align_frames: F too large for the preselection tile");
   cudaFuncSetAttribute(select_topk_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -43,7 +43,7 @@ namespace tvk {
 // tensor-core diagonal preselection, select_tc.cu
 size_t diag_table_bytes(int C, int F);
 int diag_table_tc(const double* tab, int C, int F, cudaStream_t st);
-bool select_tc_supported(int F, int K);
+bool select_tc_supported(int F, int K, int C);
 template <typename XT>
 int select_tc(const XT* x, int64_t T, int F, const double* tab, int C, int K, int32_t* sel, double* val,
               cudaStream_t st);

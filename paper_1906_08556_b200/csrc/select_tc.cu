@@ -188,7 +188,8 @@ template <typename XT, int NK>
 __global__ void __launch_bounds__(NT, 1)
     select_tc_kernel(const XT* __restrict__ x, int64_t T, int F, int C, int K, const float* __restrict__ blob,
                      const float* __restrict__ maxes, const double* __restrict__ exact, float kappa, float kappa1,
-                     int group, int debug, Pipe pipe, int32_t* __restrict__ sel_out, double* __restrict__ val_out) {
+                     int group, int debug, Pipe pipe, int* __restrict__ flagged, int32_t* __restrict__ sel_out,
+                     double* __restrict__ val_out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KP = kp(F), KS = KP / 8, NCH = nchunks(C);
   uint8_t* ring = smem;                                             // [NST][STAGE]
@@ -547,7 +548,10 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
         }
-        if (!good) sel_out[t * K] = -1;  // recomputed by select_exact_kernel
+        if (!good) {  // recomputed by select_exact_kernel
+          sel_out[t * K] = -1;
+          flagged[1 + atomicAdd(flagged, 1)] = (int)t;
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // half 1 may now reuse its candidate buffer
       mark(it, 6);
@@ -607,58 +611,62 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // ---------------------------------------------------------------- exact path for flagged frames
-// One warp per flagged frame: lanes score components lane, lane+32, ... in FP64 and keep a sorted
-// lane-local top-K; K rounds of a warp arg-best merge the 32 lists.
+// One CTA per flagged frame (list written by select_tc_kernel): every thread scores C/256
+// components in FP64, the CTA keeps the scores in shared memory and extracts the stable top-K by K
+// rounds of a block arg-best.
+constexpr int XT_THREADS = 256;
 template <typename XT>
-__global__ void select_exact_kernel(const XT* __restrict__ x, int64_t T, int F, int C, int K,
-                                    const double* __restrict__ exact, int32_t* __restrict__ sel_out,
-                                    double* __restrict__ val_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = wid * 32; base < T; base += nw * 32) {
-    const int64_t tl = base + lane;
-    unsigned flagged = __ballot_sync(0xffffffffu, tl < T && sel_out[tl * K] == -1);
-    while (flagged) {
-      const int src = __ffs(flagged) - 1;
-      flagged &= flagged - 1;
-      const int64_t t = base + src;
-      const XT* xr = x + t * F;
-      double lv[32];
-      int li[32];
-      int n = 0;
-      for (int c = lane; c < C; c += 32) {
-        const double v = exact_score(xr, exact + (int64_t)c * (2 * F + 2), F);
-        if (n == K && !better(v, c, lv[K - 1], li[K - 1])) continue;
-        int p = n < K ? n++ : K - 1;
-        while (p > 0 && better(v, c, lv[p - 1], li[p - 1])) {
-          lv[p] = lv[p - 1];
-          li[p] = li[p - 1];
-          p--;
+__global__ void __launch_bounds__(XT_THREADS) select_exact_kernel(const XT* __restrict__ x, int F, int C, int K,
+                                                                  const double* __restrict__ exact,
+                                                                  const int* __restrict__ flagged,
+                                                                  int32_t* __restrict__ sel_out,
+                                                                  double* __restrict__ val_out) {
+  extern __shared__ double sc[];  // [C] scores, then [ceil(C/32)] taken bits
+  unsigned* taken = reinterpret_cast<unsigned*>(sc + C);
+  __shared__ double rv[XT_THREADS / 32];
+  __shared__ int ri[XT_THREADS / 32];
+  const int n = flagged[0];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int f = blockIdx.x; f < n; f += gridDim.x) {
+    const int64_t t = flagged[1 + f];
+    const XT* xr = x + t * F;
+    for (int c = tid; c < C; c += XT_THREADS) sc[c] = exact_score(xr, exact + (int64_t)c * (2 * F + 2), F);
+    for (int i = tid; i < (C + 31) / 32; i += XT_THREADS) taken[i] = 0u;
+    __syncthreads();
+    for (int k = 0; k < K; k++) {
+      double bv = NAN;
+      int bi = 0x7fffffff;
+      for (int c = tid; c < C; c += XT_THREADS) {
+        const double v = sc[c];
+        if (!((taken[c >> 5] >> (c & 31)) & 1u) && better(v, c, bv, bi)) {
+          bv = v;
+          bi = c;
         }
-        lv[p] = v;
-        li[p] = c;
       }
-      int head = 0;
-      for (int k = 0; k < K; k++) {
-        double hv = head < n ? lv[head] : NAN;
-        int hi = head < n ? li[head] : 0x7fffffff;
-        double bv = hv;
-        int bi = hi;
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (better(ov, oi, bv, bi)) {
-            bv = ov;
-            bi = oi;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (better(ov, oi, bv, bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        rv[warp] = bv;
+        ri[warp] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < XT_THREADS / 32; w++)
+          if (better(rv[w], ri[w], bv, bi)) {
+            bv = rv[w];
+            bi = ri[w];
           }
-        }
-        if (head < n && hi == bi) head++;
-        if (lane == 0) {
-          sel_out[t * K + k] = bi;
-          if (val_out) val_out[t * K + k] = bv;
-        }
+        sel_out[t * K + k] = bi;
+        if (val_out) val_out[t * K + k] = bv;
+        taken[bi >> 5] |= 1u << (bi & 31);
       }
+      __syncthreads();
     }
   }
 }
@@ -680,7 +688,7 @@ int diag_table_tc(const double* tab, int C, int F, cudaStream_t st) {
   return TVK_OK;
 }
 
-bool select_tc_supported(int F, int K) { return F <= stc::MAX_F && K >= 1 && K <= 32; }
+bool select_tc_supported(int F, int K, int C) { return F <= stc::MAX_F && K >= 1 && K <= 32 && C <= 16384; }
 
 static int num_sms() {
   static int n = 0;
@@ -718,6 +726,12 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   TVK_REQUIRE(pipe.stage_bytes >= 8192 && stc::RING % pipe.stage_bytes == 0 && stc::RING / pipe.stage_bytes <= stc::MAXST &&
                   pipe.sp0 * 4096 <= pipe.stage_bytes && pipe.sp1 * 8192 <= pipe.stage_bytes && pipe.sp0 > 0 && pipe.sp1 > 0,
               "select_tc: bad TVK_SEL_PIPE");
+  int* flagged = nullptr;  // [count | frame indices], stream-ordered scratch
+  if (cudaMallocAsync((void**)&flagged, sizeof(int) * (T + 1), st) != cudaSuccess) {
+    set_error("select_tc: cannot allocate %lld bytes of scratch", (long long)(sizeof(int) * (T + 1)));
+    return TVK_ERR_CUDA;
+  }
+  cudaMemsetAsync(flagged, 0, sizeof(int), st);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(stc::NT);
@@ -732,17 +746,23 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   cfg.numAttrs = 1;
   cudaError_t le = cudaLaunchKernelEx(&cfg, kern, x, T, F, C, K, (const float*)(base + L.blob),
                                       (const float*)(base + L.maxes), (const double*)(base + L.exact), kappa, kappa1,
-                                      group, debug, pipe, sel, val);
+                                      group, debug, pipe, flagged, sel, val);
   if (le != cudaSuccess) {
     set_error("select_tc launch: %s", cudaGetErrorString(le));
     return TVK_ERR_CUDA;
   }
   TVK_CHECK_LAUNCH("select_tc");
   const char* dbg = getenv("TVK_SELECT");
-  if (dbg && strcmp(dbg, "tc_noexact") == 0) return TVK_OK;  // diagnostics: leave flagged frames at -1
-  stc::select_exact_kernel<XT><<<num_sms() * 4, 256, 0, st>>>(x, T, F, C, K, (const double*)(base + L.exact), sel,
-                                                               val);
+  if (dbg && strcmp(dbg, "tc_noexact") == 0) {  // diagnostics: leave flagged frames at -1
+    cudaFreeAsync(flagged, st);
+    return TVK_OK;
+  }
+  const size_t xsm = sizeof(double) * C + sizeof(unsigned) * ((C + 31) / 32);
+  cudaFuncSetAttribute(stc::select_exact_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
+  stc::select_exact_kernel<XT><<<num_sms() * 2, stc::XT_THREADS, xsm, st>>>(x, F, C, K, (const double*)(base + L.exact),
+                                                                             flagged, sel, val);
   TVK_CHECK_LAUNCH("select_exact");
+  cudaFreeAsync(flagged, st);
   return TVK_OK;
 }
 

@@ -29,9 +29,13 @@ METRICS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_active_pct",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_mem_active_pct",
+    "l1tex__m_xbar2l1tex_read_bytes.sum": "l2_to_sm",
+    "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active": "hmma_inst_pct",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
-         "second": 1e3}
+         "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
 
 
 def report(path):
@@ -53,7 +57,7 @@ def report(path):
             if name == "duration":
                 v *= SCALE.get(u, 1.0)  # -> ms
                 name = "duration_ms"
-            elif name.startswith("dram_") and not name.endswith("pct"):
+            elif (name.startswith("dram_") or name == "l2_to_sm") and not name.endswith("pct"):
                 v *= SCALE.get(u, 1.0)  # -> bytes
                 name += "_bytes"
             k[name] = v

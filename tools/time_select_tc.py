@@ -21,7 +21,6 @@ def t(mode, dbg=None, reps=3):
     e1.record(); torch.cuda.synchronize()
     os.environ.pop("TVK_SELECT_DEBUG", None)
     return e0.elapsed_time(e1) / reps
-ref = None
 print(f"full {t('tc'):.2f} ms, no-exact {t('tc_noexact'):.2f}, pipeline {t('tc_noexact', '2'):.2f}, copies {t('tc_noexact', '3'):.2f}")
-a = sel.clone(); t("dmma", reps=1)
+t("tc", reps=1); a = sel.clone(); t("dmma", reps=1)
 print("identical to dmma:", bool(torch.equal(a, sel)))
