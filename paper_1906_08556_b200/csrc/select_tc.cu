@@ -27,6 +27,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -35,12 +37,13 @@ namespace stc {
 
 constexpr int TM = 128;        // frames per tile = MMA M = TMEM lanes
 constexpr int NC = 128;        // components per chunk = MMA N
-// TMEM columns: [0,128) acc 0 | [128,256) acc 1 | [256,384) A hi | [384,512) A lo
+// TMEM columns: [0,128) acc 0 | [128,256) acc 1 | [256,320) A hi | [320,384) A lo | [384,512) acc 2
+// (A: two f16 per 32-bit column)
 constexpr int RING = 98304;    // B ring bytes: NST stages of STAGE bytes (runtime split, see Pipe)
 constexpr int XS = 64;         // smem row stride (floats) of the staged frame tile, >= F + 1
 constexpr int MAXST = 12;
 constexpr int CL = 1;          // CTAs per cluster sharing every B stage by TMA multicast (4 measured slower)
-constexpr int KSTEP = 8192;    // blob bytes per k-step: 128 comps x 8 k x (hi, lo) x 4 B
+constexpr int KSTEP = 8192;    // blob bytes per k16-step: 128 comps x 16 k x (hi, lo) x 2 B
 constexpr int H = 2;           // epilogue warps per TMEM lane quarter (each takes half of a chunk's columns)
 constexpr int NEPI = 128 * H;  // epilogue threads
 constexpr int NT = 128 + NEPI;
@@ -48,23 +51,25 @@ constexpr int CAP = 24;        // candidate buffer entries per (frame, half)
 constexpr int WMAX = 24;       // merged window entries per frame
 constexpr float KAPPA = 1.0f / 65536.0f;  // 3xTF32 bound: 28x the max observed error
 constexpr float KAPPA1 = 1.0f / 4096.0f;   // pass-0 slack (heuristic: the window check below is exact)
-constexpr int MAX_F = 63;      // A hi/lo (2F+1 columns each, padded to 8) must fit in TMEM columns 256-511
+constexpr int MAX_F = 63;      // A hi/lo (2F+1 f16, padded to 16, two per column) in TMEM columns 256-383
 
-__host__ __device__ inline int kp(int F) { return (2 * F + 1 + 7) / 8 * 8; }  // [x^2, x, 1], padded
+__host__ __device__ inline int kp(int F) { return (2 * F + 1 + 15) / 16 * 16; }  // [x^2, x, 1], padded to K=16
 __host__ __device__ inline int nchunks(int C) { return (C + NC - 1) / NC; }
 
 // Layout of the tensor-core part of the diagonal table (after the (2F+1) x C FP64 table).
 struct Layout {
-  size_t blob, maxes, exact, total;
+  size_t blob, maxes, colscale, exact, total;
 };
 __host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
 __host__ __device__ inline Layout layout(int C, int F) {
   Layout L;
   size_t off = al(sizeof(double) * (size_t)(2 * F + 1) * C, 1024);
   L.blob = off;
-  off += (size_t)nchunks(C) * (kp(F) / 8) * KSTEP;
+  off += (size_t)nchunks(C) * (kp(F) / 16) * KSTEP;
   L.maxes = off;
   off = al(off + sizeof(float) * (2 * F + 1), 256);
+  L.colscale = off;
+  off = al(off + sizeof(float) * kp(F), 256);
   L.exact = off;
   off += sizeof(double) * (size_t)C * (2 * F + 2);
   L.total = al(off, 256);
@@ -77,25 +82,34 @@ inline size_t smem_bytes(int) {
 }
 
 // ---------------------------------------------------------------- table construction
-// blob[(n*KS + s)*2048 + h*1024 + kmajor(r, kk)/4] = {hi,lo}(W[s*8+kk][n*128+r]), W = [a; b] rows of tab.
-__global__ void build_blob_kernel(const double* tab, int C, int F, float* blob) {
-  const int KS = kp(F) / 8, NCH = nchunks(C);
-  int64_t total = (int64_t)NCH * NC * kp(F);
+// 3xFP16 operands.  Feature column k of W is scaled by 2^e_k (e_k puts max_c |W[k][c]| in [2^8, 2^9),
+// exact), rounded to f32 and split hi = f16(w), lo = f16(w - hi): both carry 11 significant bits,
+// like TF32, and the three products a_hi b_hi + a_hi b_lo + a_lo b_hi are exact in the f32
+// accumulator.  The frame side is scaled by 2^-e_k (colscale) so that A'B' = AB.
+// blob layout: per (chunk n, k16-step s) a 4 KB tile of 128 components x 16 f16 in K-major
+// core-matrix order, all hi tiles first, then all lo tiles.
+__device__ __forceinline__ int col_exponent(float mx) { return mx > 0.0f ? 8 - ilogbf(mx) : 0; }
+
+__global__ void build_blob_kernel(const double* tab, int C, int F, const float* maxes, __half* blob,
+                                  float* colscale) {
+  const int KP = kp(F), KS = KP / 16, NCH = nchunks(C);
+  int64_t total = (int64_t)NCH * NC * KP;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    int k = (int)(idx % kp(F));
-    int cc = (int)(idx / kp(F));
-    int n = cc / NC, r = cc % NC, s = k / 8, kk = k % 8;
+    int k = (int)(idx % KP);
+    int cc = (int)(idx / KP);
+    int n = cc / NC, r = cc % NC, s = k / 16, kk = k % 16;
+    const int e = k <= 2 * F ? col_exponent(maxes[k]) : 0;
     // padded components get a NaN constant term: their score is NaN and never enters a window
     double w = (k <= 2 * F) ? (cc < C ? tab[(int64_t)k * C + cc] : (k == 2 * F ? (double)NAN : 0.0)) : 0.0;
-    float wf = (float)w;
-    float hi = tc::tf32_round(wf);
-    float lo = tc::tf32_round(wf - hi);
-    // hi words of all (chunk, k-step) tiles first, then the lo words: 4 KB per tile each
-    size_t base = ((size_t)n * KS + s) * 1024, lo_off = (size_t)NCH * KS * 1024;
-    uint32_t o = tc::kmajor_offset(r, kk, 8) / 4;
+    float wf = (float)ldexp(w, e);
+    __half hi = __float2half_rn(wf);
+    __half lo = __float2half_rn(wf - __half2float(hi));
+    size_t base = ((size_t)n * KS + s) * 2048, lo_off = (size_t)NCH * KS * 2048;
+    uint32_t o = tc::kmajor_offset16(r, kk, 16) / 2;
     blob[base + o] = hi;
     blob[lo_off + base + o] = lo;
+    if (cc == 0) colscale[k] = ldexpf(1.0f, -e);
   }
 }
 
@@ -157,11 +171,21 @@ __device__ __forceinline__ void insert_top(float (&top)[NK], float t) {
     top[i] = hi;
   }
 }
-// Accumulator buffer b = n % 2 hosts chunk n of either pass: the number of earlier uses of b (its
+// Accumulator buffer b = n % 3 hosts chunk n of either pass: the number of earlier uses of b (its
 // mbarrier phase) at (tile li, pass, chunk n), for both sides.
 __device__ __forceinline__ uint32_t buf_uses(int b, uint32_t li, int pass, int n, int NCH) {
-  const uint32_t per_pass = (NCH - b + 1) / 2;
-  return (2 * li + pass) * per_pass + n / 2;
+  const uint32_t per_pass = (NCH - b + 2) / 3;
+  return (2 * li + pass) * per_pass + n / 3;
+}
+__device__ __forceinline__ uint32_t acc_col(int b) { return b == 2 ? 384u : (uint32_t)(b * NC); }
+
+__device__ __forceinline__ void cp_async4_f(float* smem, const float* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+template <typename T>
+__device__ __forceinline__ void cp_async4_f(float* smem, const T* gmem) {  // f64 input: unused path
+  *smem = (float)*gmem;
 }
 
 template <int G>
@@ -186,12 +210,13 @@ struct Pipe {  // B-ring geometry and back-off of the single-thread roles (tunab
 
 template <typename XT, int NK>
 __global__ void __launch_bounds__(NT, 1)
-    select_tc_kernel(const XT* __restrict__ x, int64_t T, int F, int C, int K, const float* __restrict__ blob,
-                     const float* __restrict__ maxes, const double* __restrict__ exact, float kappa, float kappa1,
+    select_tc_kernel(const XT* __restrict__ x, int64_t T, int F, int C, int K, const __half* __restrict__ blob,
+                     const float* __restrict__ maxes, const float* __restrict__ colscale,
+                     const double* __restrict__ exact, float kappa, float kappa1,
                      int group, int debug, Pipe pipe, int* __restrict__ flagged, int32_t* __restrict__ sel_out,
                      double* __restrict__ val_out) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int KP = kp(F), KS = KP / 8, NCH = nchunks(C);
+  const int KP = kp(F), KS = KP / 16, NCH = nchunks(C);
   uint8_t* ring = smem;                                             // [NST][STAGE]
   float* xs = reinterpret_cast<float*>(ring + RING);                // [TM][XS] frames of the tile (f32)
   const int STAGE = pipe.stage_bytes, NST = RING / STAGE;
@@ -202,8 +227,9 @@ __global__ void __launch_bounds__(NT, 1)
   double* ev = reinterpret_cast<double*>(mi + WMAX * TM);           // [WMAX][TM] exact scores
   float* kth1 = reinterpret_cast<float*>(ev + WMAX * TM);           // [TM] K-th of the second half
   int* cnt1 = reinterpret_cast<int*>(kth1 + TM);                    // [TM] window size of the second half
-  __shared__ uint64_t full[MAXST], empty[MAXST], tfull[2], tempty[2], afull, aempty;
+  __shared__ uint64_t full[MAXST], empty[MAXST], tfull[3], tempty[3], afull, aempty;
   __shared__ uint32_t tmem_base;
+  __shared__ float cs[128];  // colscale (feature column exponents of the f16 operands)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (T + TM - 1) / TM;
@@ -216,7 +242,7 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_init(&full[i], 1);
       tc::mbar_init(&empty[i], CL);
     }
-    for (int i = 0; i < 2; i++) {
+    for (int i = 0; i < 3; i++) {
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], NEPI / 32);
     }
@@ -225,12 +251,13 @@ __global__ void __launch_bounds__(NT, 1)
     tc::fence_mbar_init();
   }
   if (warp == 2) tc::tmem_alloc<512>(&tmem_base);
+  for (int k = tid; k < 128; k += NT) cs[k] = k < KP ? colscale[k] : 0.0f;
   tc::fence_before_sync();
   __syncthreads();
   tc::cluster_sync();  // barrier inits visible to the peers' multicast copies and commits
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const uint32_t tA_hi = tmem + 256, tA_lo = tmem + 384;
+  const uint32_t tA_hi = tmem + 256, tA_lo = tmem + 320;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -239,7 +266,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (lane == 0) {
       const uint32_t crank = tc::cluster_ctarank();
       const uint16_t mask = (uint16_t)((1u << CL) - 1u);
-      const float* blob_lo = blob + (size_t)NCH * KS * 1024;
+      const __half* blob_lo = blob + (size_t)NCH * KS * 2048;
       uint32_t q = 0;
       for (int64_t it = 0; it < iters; it++)
         for (int pass = 0; pass < 2; pass++) {
@@ -250,7 +277,7 @@ __global__ void __launch_bounds__(NT, 1)
               tc::mbar_wait_backoff(&empty[slot], ((q / NST) & 1) ^ 1, pipe.sleep_prod);
               const uint32_t piece = ns * 4096, share = piece / CL;  // hi (and lo) words of ns k-steps
               tc::mbar_arrive_expect_tx(&full[slot], pass == 0 ? piece : 2 * piece);
-              const size_t src = ((size_t)n * KS + s0) * 1024 + crank * (share / 4);
+              const size_t src = ((size_t)n * KS + s0) * 2048 + crank * (share / 2);
               uint8_t* dst = ring + slot * STAGE + crank * share;
               tc::bulk_g2s_mc(dst, blob + src, share, &full[slot], mask);
               if (pass == 1) tc::bulk_g2s_mc(dst + piece, blob_lo + src, share, &full[slot], mask);
@@ -260,7 +287,7 @@ __global__ void __launch_bounds__(NT, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM)
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_tf32(TM, NC);
+      const uint32_t idesc = tc::idesc_f16(TM, NC);
       const uint32_t rb = tc::smem_u32(ring);
       uint32_t q = 0, li = 0;
       const uint16_t mask = (uint16_t)((1u << CL) - 1u);
@@ -270,10 +297,10 @@ __global__ void __launch_bounds__(NT, 1)
         for (int pass = 0; pass < 2; pass++) {
           const int SP = pass == 0 ? pipe.sp0 : pipe.sp1;
           for (int n = 0; n < NCH; n++) {
-            const int b = n % 2;
+            const int b = n % 3;
             tc::mbar_wait_backoff(&tempty[b], (buf_uses(b, li, pass, n, NCH) & 1) ^ 1, pipe.sleep_mma);
             tc::fence_after_sync();
-            const uint32_t d = tmem + b * NC;
+            const uint32_t d = tmem + acc_col(b);
             for (int s0 = 0; s0 < KS; s0 += SP, q++) {
               const int slot = q % NST, ns = min(SP, KS - s0);
               tc::mbar_wait_backoff(&full[slot], (q / NST) & 1, pipe.sleep_mma);
@@ -282,11 +309,11 @@ __global__ void __launch_bounds__(NT, 1)
                 for (int i = 0; i < ns; i++) {
                   const int s = s0 + i;
                   const uint64_t bh = tc::smem_desc(rb + slot * STAGE + i * 4096, 128, 256);
-                  tc::mma_tf32_ts(d, tA_hi + 8 * s, bh, idesc, s > 0);
-                  if (pass == 1) {  // 3xTF32: a_hi b_hi + a_hi b_lo + a_lo b_hi
+                  tc::mma_f16_ts(d, tA_hi + 8 * s, bh, idesc, s > 0);
+                  if (pass == 1) {  // 3xFP16: a_hi b_hi + a_hi b_lo + a_lo b_hi
                     const uint64_t bl = tc::smem_desc(rb + slot * STAGE + (ns + i) * 4096, 128, 256);
-                    tc::mma_tf32_ts(d, tA_hi + 8 * s, bl, idesc, 1);
-                    tc::mma_tf32_ts(d, tA_lo + 8 * s, bh, idesc, 1);
+                    tc::mma_f16_ts(d, tA_hi + 8 * s, bl, idesc, 1);
+                    tc::mma_f16_ts(d, tA_lo + 8 * s, bh, idesc, 1);
                   }
                 }
               }
@@ -312,40 +339,62 @@ __global__ void __launch_bounds__(NT, 1)
     // Features [x^2, x, 1, 0...] of this thread's frame, TF32 hi (part 0, TMEM columns 256+) or lo
     // (part 1, columns 384+) words.  Each half writes the 64 columns it reads of every accumulator.
     const int FP = F | 1;  // odd row stride: conflict-free row-per-thread reads
-    // coalesced load of the tile's frames (as f32) into smem; all epilogue threads, then a barrier
+    // the tile's frames (as f32) into smem: f32 input by asynchronous 4-byte copies (waited for in
+    // build_A), f64 input converted by the threads; all epilogue threads take part
     auto load_x = [&](int64_t tile) {
       const int64_t base = tile * TM;
       for (int i = e; i < TM * F; i += NEPI) {
         const int rr = i / F, cc = i - rr * F;
-        xs[rr * FP + cc] = base + rr < T ? (float)x[(base + rr) * F + cc] : 0.0f;
+        if (sizeof(XT) == 4 && base + rr < T)
+          cp_async4_f(&xs[rr * FP + cc], x + (base + rr) * F + cc);
+        else
+          xs[rr * FP + cc] = base + rr < T ? (float)x[(base + rr) * F + cc] : 0.0f;
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
+      cp_async_commit();
     };
-    auto build_A = [&](int64_t tile) {
+    // Features v_k = [x^2, x, 1, 0...] scaled by colscale_k (table column exponents) and by a frame
+    // exponent 2^-E (max |v'| in [2^13, 2^14): no f16 overflow), split into f16 hi/lo and packed two
+    // per TMEM column: half h writes features [64h, 64h+64) (hi words at columns 256+, lo at 320+).
+    // Returns 2^-E: the tile's scores (and every threshold compared with them) are in units of 2^E.
+    auto build_A = [&](int64_t tile) -> float {
+      cp_async_wait<0>();
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // every thread's frame copies have landed
       const int64_t t = tile * TM + r;
       const bool ok = t < T;
       const float* xr = xs + r * FP;
-      for (int j = 2 * h; j < 2 * h + 2 && 32 * j < KP; j++) {
+      float mx = ok ? cs[2 * F] : 0.0f;  // max |v_k| over the row, analytically
+      if (ok)
+        for (int f = 0; f < F; f++) {
+          const float xv = xr[f];
+          mx = fmaxf(mx, fmaxf(xv * xv * cs[f], fabsf(xv) * cs[F + f]));
+        }
+      const int E = (mx > 0.0f && isfinite(mx)) ? ilogbf(mx) - 13 : 0;
+      const float inv = ldexpf(1.0f, -E);
+      if (64 * h < KP) {
         float wh[32], wl[32];
 #pragma unroll
-        for (int u = 0; u < 32; u++) {
-          const int k = 32 * j + u;
+        for (int u = 0; u < 64; u++) {
+          const int k = 64 * h + u;
           float v = 0.0f;
           if (ok && k == 2 * F) {
-            v = 1.0f;
+            v = cs[k] * inv;
           } else if (ok && k < 2 * F) {
             const float xv = xr[k < F ? k : k - F];
-            v = k < F ? xv * xv : xv;
+            v = (k < F ? xv * xv : xv) * cs[k] * inv;
           }
-          wh[u] = tc::tf32_round(v);
-          wl[u] = tc::tf32_round(v - wh[u]);
+          const __half hi = __float2half_rn(v), lo = __float2half_rn(v - __half2float(hi));
+          __half* ph = reinterpret_cast<__half*>(&wh[u >> 1]);
+          __half* pl = reinterpret_cast<__half*>(&wl[u >> 1]);
+          ph[u & 1] = hi;
+          pl[u & 1] = lo;
         }
-        tc::tmem_st32(lane_addr + 256 + 32 * j, wh);
-        tc::tmem_st32(lane_addr + 384 + 32 * j, wl);
+        tc::tmem_st32(lane_addr + 256 + 32 * h, wh);
+        tc::tmem_st32(lane_addr + 320 + 32 * h, wl);
       }
       tc::tmem_st_wait();
       tc::fence_before_sync();
       tc::mbar_arrive(&afull);
+      return inv;
     };
     // margin scale S_t = sum_f x_f^2 max|a_f| + |x_f| max|b_f| + max|c|
     auto scale = [&](int64_t tile) -> float {
@@ -361,9 +410,10 @@ __global__ void __launch_bounds__(NT, 1)
     };
 
     int64_t tile = blockIdx.x;
+    float inv = 1.0f;  // 2^-E of the current tile's frame (see build_A)
     if (iters > 0) {
       load_x(tile);
-      build_A(tile);
+      inv = build_A(tile);
     }
     float S = iters > 0 ? scale(tile) : 0.0f;
     uint32_t li = 0;
@@ -375,7 +425,7 @@ __global__ void __launch_bounds__(NT, 1)
     for (int64_t it = 0; it < iters; it++, tile += gridDim.x, li++) {
       mark(it, 0);
       const int64_t t = tile * TM + r;
-      const float m = kappa * S, m2 = 2.0f * m;
+      const float m = kappa * S * inv, m2 = 2.0f * m;  // in score units of the tile (2^E)
       const bool live = t < T && isfinite(S);  // rows past T (and non-finite frames) take nothing
 
       // ---- pass 0 (1xTF32): K-th largest of the group maxima, a lower bound of the K-th exact score
@@ -383,10 +433,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int i = 0; i < NK; i++) top[i] = i < NK - K ? INFINITY : -INFINITY;
       for (int n = 0; n < NCH; n++) {
-        const int b = n % 2;
+        const int b = n % 3;
         tc::mbar_wait(&tfull[b], buf_uses(b, li, 0, n, NCH) & 1);
         tc::fence_after_sync();
-        const uint32_t col = b * NC + h * (NC / H);
+        const uint32_t col = acc_col(b) + h * (NC / H);
         float v[2][32];
         tc::tmem_ld32(lane_addr + col, v[0]);
         tc::tmem_ld32(lane_addr + col + 32, v[1]);
@@ -421,7 +471,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int i = 0; i < NK; i++) insert_top<NK>(top, i >= NK - K ? mv[i * TM + r] : -INFINITY);
         // every exact score of the K group maxima is >= (their 1xTF32 score) - kappa1 S
-        kth1[r] = kth_of<NK>(top, K) - kappa1 * S - 3.0f * m;
+        kth1[r] = kth_of<NK>(top, K) - kappa1 * S * inv - 3.0f * m;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
       const float thr = live ? kth1[r] : INFINITY;
@@ -432,14 +482,14 @@ __global__ void __launch_bounds__(NT, 1)
       int cnt = 0;
       bool ovf = false;
       for (int n = 0; n < NCH; n++) {
-        const int b = n % 2;
+        const int b = n % 3;
         tc::mbar_wait(&tfull[b], buf_uses(b, li, 1, n, NCH) & 1);
         tc::fence_after_sync();
 #pragma unroll 1
         for (int j = 0; j < NC / 32 / H; j++) {
           const int col = h * (NC / H) + j * 32;
           float v[32];
-          tc::tmem_ld32(lane_addr + b * NC + col, v);
+          tc::tmem_ld32(lane_addr + acc_col(b) + col, v);
           tc::tmem_ld_wait();
           if (j == NC / 32 / H - 1) {
             tc::fence_before_sync();
@@ -464,10 +514,10 @@ __global__ void __launch_bounds__(NT, 1)
       // A operand of the next tile (all MMAs of this tile have completed: their last chunk was read)
       mark(it, 4);
       const int64_t next = tile + gridDim.x;
-      float S_next = 0.0f;
+      float S_next = 0.0f, inv_next = 1.0f;
       if (it + 1 < iters) {
         tc::mbar_wait(&aempty, li & 1);
-        build_A(next);
+        inv_next = build_A(next);
         S_next = scale(next);
       }
 
@@ -569,7 +619,7 @@ __global__ void __launch_bounds__(NT, 1)
           if (debug) {  // diagnostics: s~ - s of the s~-ordered window
             for (int i = 0; i < K; i++) {
               sel_out[t * K + i] = mi[i * TM + r];
-              if (val_out) val_out[t * K + i] = (double)mv[i * TM + r] - ev[i * TM + r];
+              if (val_out) val_out[t * K + i] = (double)mv[i * TM + r] / (double)inv - ev[i * TM + r];
             }
           } else {
             for (int p = 0; p < 32;) {  // re-sort each flagged cluster by the exact rank
@@ -602,6 +652,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
       mark(it, 7);
       S = S_next;
+      inv = inv_next;
     }
   }
   tc::fence_before_sync();
@@ -681,9 +732,10 @@ int diag_table_tc(const double* tab, int C, int F, cudaStream_t st) {
   uint8_t* base = (uint8_t*)tab;
   int64_t total = (int64_t)stc::nchunks(C) * stc::NC * stc::kp(F);
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-  stc::build_blob_kernel<<<blocks, 256, 0, st>>>(tab, C, F, (float*)(base + L.blob));
   stc::build_aux_kernel<<<2 * F + 1, 256, 0, st>>>(tab, C, F, (float*)(base + L.maxes),
                                                    (double*)(base + L.exact));
+  stc::build_blob_kernel<<<blocks, 256, 0, st>>>(tab, C, F, (const float*)(base + L.maxes),
+                                                 (__half*)(base + L.blob), (float*)(base + L.colscale));
   TVK_CHECK_LAUNCH("diag_table tensor-core part");
   return TVK_OK;
 }
@@ -720,7 +772,7 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   const float kappa1 = ek1 ? (float)atof(ek1) : stc::KAPPA1;
   // group maxima of 32 (or 8, or single scores) while at least 2K groups exist
   const int group = C >= 64 * K ? 32 : (C >= 16 * K ? 8 : 1);
-  stc::Pipe pipe{32768, 8, 4, 64, 0};  // 3 stages of 32 KB
+  stc::Pipe pipe{32768, 8, 4, 64, 0};  // 3 stages of 32 KB: pass 0 8 k16-steps (hi), pass 1 4 (hi + lo)
   if (const char* ep = getenv("TVK_SEL_PIPE"))  // stage_bytes,sp0,sp1,sleep_prod,sleep_mma
     sscanf(ep, "%d,%d,%d,%d,%d", &pipe.stage_bytes, &pipe.sp0, &pipe.sp1, &pipe.sleep_prod, &pipe.sleep_mma);
   TVK_REQUIRE(pipe.stage_bytes >= 8192 && stc::RING % pipe.stage_bytes == 0 && stc::RING / pipe.stage_bytes <= stc::MAXST &&
@@ -744,8 +796,9 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, x, T, F, C, K, (const float*)(base + L.blob),
-                                      (const float*)(base + L.maxes), (const double*)(base + L.exact), kappa, kappa1,
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, x, T, F, C, K, (const __half*)(base + L.blob),
+                                      (const float*)(base + L.maxes), (const float*)(base + L.colscale),
+                                      (const double*)(base + L.exact), kappa, kappa1,
                                       group, debug, pipe, flagged, sel, val);
   if (le != cudaSuccess) {
     set_error("select_tc launch: %s", cudaGetErrorString(le));
