@@ -42,7 +42,7 @@ constexpr int NC = 128;        // components per chunk = MMA N
 constexpr int RING = 98304;    // B ring bytes: NST stages of STAGE bytes (runtime split, see Pipe)
 constexpr int XS = 64;         // smem row stride (floats) of the staged frame tile, >= F + 1
 constexpr int MAXST = 12;
-constexpr int CL = 1;          // CTAs per cluster sharing every B stage by TMA multicast (4 measured slower)
+constexpr int CL = 2;          // CTAs per cluster sharing every B stage by TMA multicast
 constexpr int KSTEP = 8192;    // blob bytes per k16-step: 128 comps x 16 k x (hi, lo) x 2 B
 constexpr int H = 2;           // epilogue warps per TMEM lane quarter (each takes half of a chunk's columns)
 constexpr int NEPI = 128 * H;  // epilogue threads
