@@ -163,7 +163,6 @@ struct WhitenSmem {
   double cst[2];            // const, pad (one 16-byte copy)
   XT X[2][GROWS * GS];      // raw frame rows (columns F..63 stay zero)
   int pair[2][GROWS];
-  double part[GROWS][2];
 };
 
 template <int BYTES>  // 4 or 8: one frame element
@@ -172,28 +171,23 @@ __device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
 }
 
-// One warp's 32 x 32 block of Z = Y U: rows wm*32.., column blocks n = wn, wn+2, wn+4, wn+6 (8 wide,
-// interleaved so both warp columns get similar triangular work); k-step kk (4 wide) is needed by
-// column block n only when 4 kk <= 8 n + 7.
-template <int WN, typename XT>
-__device__ __forceinline__ void whiten_mma(const XT* X, const double* U, const double* mu, int wm, int g, int t4,
-                                           double (&acc)[4][4][2]) {
+// One warp's 16 rows of Z = Y U (all 8 column blocks of 8): column block n needs k-step kk
+// (4 wide) only when 4 kk <= 8 n + 7 (U upper triangular).
+template <typename XT>
+__device__ __forceinline__ void whiten_mma(const XT* X, const double* U, const double* mu, int w, int g, int t4,
+                                           double (&acc)[2][8][2]) {
 #pragma unroll
   for (int kk = 0; kk < GP / 4; kk++) {
     const int k = kk * 4 + t4;
     const double m = mu[k];
-    double a[4];
+    double a[2];
 #pragma unroll
-    for (int i = 0; i < 4; i++) a[i] = (double)X[(wm * 32 + i * 8 + g) * GS + k] - m;
+    for (int i = 0; i < 2; i++) a[i] = (double)X[(w * 16 + i * 8 + g) * GS + k] - m;
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      constexpr int dummy = 0;
-      (void)dummy;
-      if (kk <= 2 * (WN + 2 * j) + 1) {
-        const double b = U[k * GS + (WN + 2 * j) * 8 + g];
+    for (int n = kk / 2; n < 8; n++) {
+      const double b = U[k * GS + n * 8 + g];
 #pragma unroll
-        for (int i = 0; i < 4; i++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
-      }
+      for (int i = 0; i < 2; i++) dmma884(acc[i][n][0], acc[i][n][1], a[i], b);
     }
   }
 }
@@ -206,7 +200,6 @@ __global__ void __launch_bounds__(GT, 2)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WhitenSmem<XT>& S = *reinterpret_cast<WhitenSmem<XT>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t4 = lane & 3;
   const int ntiles = *ntile_p;
   const int per = (ntiles + gridDim.x - 1) / gridDim.x;
@@ -255,41 +248,34 @@ __global__ void __launch_bounds__(GT, 2)
   for (int ti = tb; ti < te; ti++) {
     const int xb = (ti - tb) & 1;
     const int4 d = tiles[ti];
-    if (d.z != comp) {  // new component: stage U (the previous tile's math is done)
+    if (d.z != comp) {  // new component: stage U once every warp is done with the previous tile
+      __syncthreads();
       stage_U(d.z);
       comp = d.z;
     }
-    // prefetch the next tile's frame rows into the other buffer
-    if (ti + 1 < te) {
-      issue(ti + 1, xb ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<0>();
     __syncthreads();
-    // rows past the tile's pairs hold stale frames: their (finite) results are never stored
-    double acc[4][4][2];
+    // prefetch the next tile's frame rows into the other buffer (its last readers passed the barrier)
+    if (ti + 1 < te) issue(ti + 1, xb ^ 1);
+    // warp w owns rows 16w..16w+15 of the tile: Z rows, q = rowsum(Z o Z), ll, store -- no more barriers
+    if (warp * 16 < d.y) {
+      double acc[2][8][2];
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+      for (int i = 0; i < 2; i++)
 #pragma unroll
-      for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-    if (wm * 32 < d.y) {
-      if (wn == 0) whiten_mma<0>(S.X[xb], S.U, S.mu, wm, g, t4, acc);
-      else whiten_mma<1>(S.X[xb], S.U, S.mu, wm, g, t4, acc);
+        for (int n = 0; n < 8; n++) acc[i][n][0] = acc[i][n][1] = 0.0;
+      whiten_mma(S.X[xb], S.U, S.mu, warp, g, t4, acc);
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        double s = 0.0;
+#pragma unroll
+        for (int n = 0; n < 8; n++) s += acc[i][n][0] * acc[i][n][0] + acc[i][n][1] * acc[i][n][1];
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        const int r = warp * 16 + i * 8 + g;
+        if (t4 == 0 && r < d.y) sel_ll[S.pair[xb][r]] = S.cst[0] - 0.5 * s;
+      }
     }
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < 4; j++) s += acc[i][j][0] * acc[i][j][0] + acc[i][j][1] * acc[i][j][1];
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      if (t4 == 0) S.part[wm * 32 + i * 8 + g][wn] = s;
-    }
-    __syncthreads();
-    for (int r = tid; r < d.y; r += GT) sel_ll[S.pair[xb][r]] = S.cst[0] - 0.5 * (S.part[r][0] + S.part[r][1]);
-    // the next iteration's prefetch overwrites this tile's buffers only after its own barrier
-    __syncthreads();
   }
 }
 
