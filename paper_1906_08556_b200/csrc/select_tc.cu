@@ -37,7 +37,8 @@ namespace stc {
 
 constexpr int TM = 128;        // frames per tile = MMA M = TMEM lanes
 constexpr int NC = 128;        // components per chunk = MMA N
-// TMEM columns: [0,128) acc 0 | [128,256) acc 1 | [256,320) A hi | [320,384) A lo | [384,512) acc 2
+// TMEM columns: [0,128) acc 0 | [128,256) acc 1 | [256,384) A buffer 0 | [384,512) A buffer 1, each A
+// buffer = 64 columns of hi words then 64 of lo words; the next tile's A is built during this tile
 // (A: two f16 per 32-bit column)
 constexpr int RING = 98304;    // B ring bytes: NST stages of STAGE bytes (runtime split, see Pipe)
 constexpr int XS = 64;         // smem row stride (floats) of the staged frame tile, >= F + 1
@@ -171,13 +172,14 @@ __device__ __forceinline__ void insert_top(float (&top)[NK], float t) {
     top[i] = hi;
   }
 }
-// Accumulator buffer b = n % 3 hosts chunk n of either pass: the number of earlier uses of b (its
+// Accumulator buffer b = n % 2 hosts chunk n of either pass: the number of earlier uses of b (its
 // mbarrier phase) at (tile li, pass, chunk n), for both sides.
 __device__ __forceinline__ uint32_t buf_uses(int b, uint32_t li, int pass, int n, int NCH) {
-  const uint32_t per_pass = (NCH - b + 2) / 3;
-  return (2 * li + pass) * per_pass + n / 3;
+  const uint32_t per_pass = (NCH - b + 1) / 2;
+  return (2 * li + pass) * per_pass + n / 2;
 }
-__device__ __forceinline__ uint32_t acc_col(int b) { return b == 2 ? 384u : (uint32_t)(b * NC); }
+__device__ __forceinline__ uint32_t acc_col(int b) { return (uint32_t)(b * NC); }
+__device__ __forceinline__ uint32_t a_col(uint32_t li) { return 256u + 128u * (li & 1u); }
 
 __device__ __forceinline__ void cp_async4_f(float* smem, const float* gmem) {
   unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(NT, 1)
   double* ev = reinterpret_cast<double*>(mi + WMAX * TM);           // [WMAX][TM] exact scores
   float* kth1 = reinterpret_cast<float*>(ev + WMAX * TM);           // [TM] K-th of the second half
   int* cnt1 = reinterpret_cast<int*>(kth1 + TM);                    // [TM] window size of the second half
-  __shared__ uint64_t full[MAXST], empty[MAXST], tfull[3], tempty[3], afull, aempty;
+  __shared__ uint64_t full[MAXST], empty[MAXST], tfull[2], tempty[2], afull[2], aempty[2];
   __shared__ uint32_t tmem_base;
   __shared__ float cs[128];  // colscale (feature column exponents of the f16 operands)
 
@@ -242,12 +244,14 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_init(&full[i], 1);
       tc::mbar_init(&empty[i], CL);
     }
-    for (int i = 0; i < 3; i++) {
+    for (int i = 0; i < 2; i++) {
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], NEPI / 32);
     }
-    tc::mbar_init(&afull, NEPI);
-    tc::mbar_init(&aempty, 1);
+    for (int i = 0; i < 2; i++) {
+      tc::mbar_init(&afull[i], NEPI);
+      tc::mbar_init(&aempty[i], 1);
+    }
     tc::fence_mbar_init();
   }
   if (warp == 2) tc::tmem_alloc<512>(&tmem_base);
@@ -257,7 +261,6 @@ __global__ void __launch_bounds__(NT, 1)
   tc::cluster_sync();  // barrier inits visible to the peers' multicast copies and commits
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const uint32_t tA_hi = tmem + 256, tA_lo = tmem + 320;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -292,12 +295,13 @@ __global__ void __launch_bounds__(NT, 1)
       uint32_t q = 0, li = 0;
       const uint16_t mask = (uint16_t)((1u << CL) - 1u);
       for (int64_t it = 0; it < iters; it++, li++) {
-        tc::mbar_wait_backoff(&afull, li & 1, 64);
+        tc::mbar_wait_backoff(&afull[li & 1], (li >> 1) & 1, 64);
+        const uint32_t tA_hi = tmem + a_col(li), tA_lo = tA_hi + 64;
         tc::fence_after_sync();
         for (int pass = 0; pass < 2; pass++) {
           const int SP = pass == 0 ? pipe.sp0 : pipe.sp1;
           for (int n = 0; n < NCH; n++) {
-            const int b = n % 3;
+            const int b = n % 2;
             tc::mbar_wait_backoff(&tempty[b], (buf_uses(b, li, pass, n, NCH) & 1) ^ 1, pipe.sleep_mma);
             tc::fence_after_sync();
             const uint32_t d = tmem + acc_col(b);
@@ -322,9 +326,10 @@ __global__ void __launch_bounds__(NT, 1)
             tc::mma_commit(&tfull[b]);
           }
         }
-        tc::mma_commit(&aempty);
+        tc::mma_commit(&aempty[li & 1]);
       }
-      if (li > 0) tc::mbar_wait(&aempty, (li - 1) & 1);  // no async arrive outlives the CTA
+      for (uint32_t l = li > 2 ? li - 2 : 0; l < li; l++)  // no async arrive outlives the CTA
+        tc::mbar_wait(&aempty[l & 1], (l >> 1) & 1);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
@@ -354,9 +359,9 @@ __global__ void __launch_bounds__(NT, 1)
     };
     // Features v_k = [x^2, x, 1, 0...] scaled by colscale_k (table column exponents) and by a frame
     // exponent 2^-E (max |v'| in [2^13, 2^14): no f16 overflow), split into f16 hi/lo and packed two
-    // per TMEM column: half h writes features [64h, 64h+64) (hi words at columns 256+, lo at 320+).
+    // per TMEM column: half h writes features [64h, 64h+64) (hi words at a_col + 32h, lo 64 further).
     // Returns 2^-E: the tile's scores (and every threshold compared with them) are in units of 2^E.
-    auto build_A = [&](int64_t tile) -> float {
+    auto build_A = [&](int64_t tile, uint32_t lt) -> float {
       cp_async_wait<0>();
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // every thread's frame copies have landed
       const int64_t t = tile * TM + r;
@@ -388,12 +393,12 @@ __global__ void __launch_bounds__(NT, 1)
           ph[u & 1] = hi;
           pl[u & 1] = lo;
         }
-        tc::tmem_st32(lane_addr + 256 + 32 * h, wh);
-        tc::tmem_st32(lane_addr + 320 + 32 * h, wl);
+        tc::tmem_st32(lane_addr + a_col(lt) + 32 * h, wh);
+        tc::tmem_st32(lane_addr + a_col(lt) + 64 + 32 * h, wl);
       }
       tc::tmem_st_wait();
       tc::fence_before_sync();
-      tc::mbar_arrive(&afull);
+      tc::mbar_arrive(&afull[lt & 1]);
       return inv;
     };
     // margin scale S_t = sum_f x_f^2 max|a_f| + |x_f| max|b_f| + max|c|
@@ -413,7 +418,7 @@ __global__ void __launch_bounds__(NT, 1)
     float inv = 1.0f;  // 2^-E of the current tile's frame (see build_A)
     if (iters > 0) {
       load_x(tile);
-      inv = build_A(tile);
+      inv = build_A(tile, 0);
     }
     float S = iters > 0 ? scale(tile) : 0.0f;
     uint32_t li = 0;
@@ -424,6 +429,7 @@ __global__ void __launch_bounds__(NT, 1)
     };
     for (int64_t it = 0; it < iters; it++, tile += gridDim.x, li++) {
       mark(it, 0);
+      if (it + 1 < iters) load_x(tile + gridDim.x);  // xs is free: this tile's A and scale are built
       const int64_t t = tile * TM + r;
       const float m = kappa * S * inv, m2 = 2.0f * m;  // in score units of the tile (2^E)
       const bool live = t < T && isfinite(S);  // rows past T (and non-finite frames) take nothing
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int i = 0; i < NK; i++) top[i] = i < NK - K ? INFINITY : -INFINITY;
       for (int n = 0; n < NCH; n++) {
-        const int b = n % 3;
+        const int b = n % 2;
         tc::mbar_wait(&tfull[b], buf_uses(b, li, 0, n, NCH) & 1);
         tc::fence_after_sync();
         const uint32_t col = acc_col(b) + h * (NC / H);
@@ -475,14 +481,20 @@ __global__ void __launch_bounds__(NT, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
       const float thr = live ? kth1[r] : INFINITY;
-      if (it + 1 < iters) load_x(tile + gridDim.x);  // frames of the next tile, read after its A is free
+      // A operand of the next tile into the other TMEM A buffer (its last reader, tile li-1, is done)
+      float S_next = 0.0f, inv_next = 1.0f;
+      if (it + 1 < iters) {
+        if (li >= 1) tc::mbar_wait(&aempty[(li + 1) & 1], ((li - 1) >> 1) & 1);
+        inv_next = build_A(tile + gridDim.x, li + 1);
+        S_next = scale(tile + gridDim.x);
+      }
       mark(it, 3);
 
       // ---- pass 1 (3xTF32): collect every score >= thr
       int cnt = 0;
       bool ovf = false;
       for (int n = 0; n < NCH; n++) {
-        const int b = n % 3;
+        const int b = n % 2;
         tc::mbar_wait(&tfull[b], buf_uses(b, li, 1, n, NCH) & 1);
         tc::fence_after_sync();
 #pragma unroll 1
@@ -513,13 +525,7 @@ __global__ void __launch_bounds__(NT, 1)
 
       // A operand of the next tile (all MMAs of this tile have completed: their last chunk was read)
       mark(it, 4);
-      const int64_t next = tile + gridDim.x;
-      float S_next = 0.0f, inv_next = 1.0f;
-      if (it + 1 < iters) {
-        tc::mbar_wait(&aempty, li & 1);
-        inv_next = build_A(next);
-        S_next = scale(next);
-      }
+
 
       mark(it, 5);
       // ---- half lists sorted by s~ desc (index asc on ties)
