@@ -194,7 +194,7 @@ __device__ __forceinline__ void whiten_mma(const XT* X, const double* U, const d
 
 template <typename XT, bool VEC>
 __global__ void __launch_bounds__(GT, 2)
-    whiten_ll_kernel(const XT* __restrict__ x, int F, const double* __restrict__ tab, int K,
+    whiten_ll_kernel(const XT* __restrict__ x, int F, const double* __restrict__ tab, int K, uint64_t kinv,
                      const int32_t* __restrict__ sorted, const int4* __restrict__ tiles, const int* __restrict__ ntile_p,
                      double* __restrict__ sel_ll) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -227,17 +227,31 @@ __global__ void __launch_bounds__(GT, 2)
     // frame rows: row r <- x[sorted / K], F elements; warp w copies rows w, w+8, ... (lanes over
     // 16-byte pieces), lane j first fetches the frame index of the warp's j-th row
     const int per_row = VEC ? (F * (int)sizeof(XT)) / 16 : F;
+    // frame = pair / K by a 40-bit reciprocal (exact for pair < 2^31, K <= 32)
     const int myrow = warp + (GT / 32) * lane;
-    const int myframe = (lane < GROWS / (GT / 32) && myrow < d.y) ? sorted[d.x + myrow] / K : 0;
-    for (int j = 0; j < GROWS / (GT / 32); j++) {
-      const int r = warp + (GT / 32) * j;
-      const int fr = __shfl_sync(0xffffffffu, myframe, j);
-      if (r >= d.y) break;
-      const XT* src = x + (int64_t)fr * F;
-      for (int c = lane; c < per_row; c += 32) {
-        if (VEC) cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
-                            reinterpret_cast<const uint8_t*>(src) + 16 * c, 16);
-        else cp_async_elem<(int)sizeof(XT)>(&S.X[b][r * GS + c], src + c);
+    const int myframe = (lane < GROWS / (GT / 32) && myrow < d.y)
+                            ? (int)(((uint64_t)(uint32_t)sorted[d.x + myrow] * kinv) >> 40) : 0;
+    if (VEC && per_row <= 16) {  // two rows per warp step: lanes 0-15 and 16-31
+      const int sub = lane >> 4, c = lane & 15;
+      for (int j = 0; j < GROWS / (GT / 32); j += 2) {
+        const int r = warp + (GT / 32) * (j + sub);
+        const int fr = __shfl_sync(0xffffffffu, myframe, j + sub);
+        if (warp + (GT / 32) * j >= d.y) break;
+        if (r < d.y && c < per_row)
+          cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
+                     reinterpret_cast<const uint8_t*>(x + (int64_t)fr * F) + 16 * c, 16);
+      }
+    } else {
+      for (int j = 0; j < GROWS / (GT / 32); j++) {
+        const int r = warp + (GT / 32) * j;
+        const int fr = __shfl_sync(0xffffffffu, myframe, j);
+        if (r >= d.y) break;
+        const XT* src = x + (int64_t)fr * F;
+        for (int c = lane; c < per_row; c += 32) {
+          if (VEC) cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
+                              reinterpret_cast<const uint8_t*>(src) + 16 * c, 16);
+          else cp_async_elem<(int)sizeof(XT)>(&S.X[b][r * GS + c], src + c);
+        }
       }
     }
     cp_async_commit();
@@ -321,7 +335,9 @@ static int launch_whiten(const XT* x, int F, const double* tab, int K, const Gro
                          cudaStream_t st) {
   const size_t smem = sizeof(WhitenSmem<XT>);
   cudaFuncSetAttribute(whiten_ll_kernel<XT, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  whiten_ll_kernel<XT, VEC><<<2 * sms, GT, smem, st>>>(x, F, tab, K, w.sorted, w.tiles, w.tile_start + 0, sel_ll);
+  const uint64_t kinv = ((1ull << 40) + K - 1) / K;
+  whiten_ll_kernel<XT, VEC><<<2 * sms, GT, smem, st>>>(x, F, tab, K, kinv, w.sorted, w.tiles, w.tile_start + 0,
+                                                       sel_ll);
   TVK_CHECK_LAUNCH("whiten_ll");
   return TVK_OK;
 }
@@ -330,6 +346,7 @@ template <typename XT>
 int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, int K, const int32_t* sel,
                     double* sel_ll, void* ws_base, int64_t ws_bytes, cudaStream_t st) {
   TVK_REQUIRE(F <= GP, "grouped full log-likelihood supports F <= 64");
+  TVK_REQUIRE(K >= 1 && K <= 32, "grouped full log-likelihood supports K <= 32");
   TVK_REQUIRE(C <= 8192, "grouped full log-likelihood supports C <= 8192");
   const int64_t n_pairs = T * K;
   TVK_REQUIRE(n_pairs < (1ll << 31) - 1, "too many (frame, component) pairs for one call");
