@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(NT, 1)
     float S = iters > 0 ? scale(tile) : 0.0f;
     uint32_t li = 0;
     // debug 6: per-phase clock64 timeline of CTA 0, epilogue thread 0 (into val_out)
-    const bool tl = debug == 6 && blockIdx.x == 0 && e == 0 && val_out;
+    const bool tl = (debug == 6 || debug == 7) && blockIdx.x == 0 && e == 0 && val_out;
     auto mark = [&](int it, int ph) {
       if (tl && it < 64) val_out[it * 8 + ph] = (double)clock64();
     };
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (lane == 0) tc::mbar_arrive(&tempty[b]);
 #pragma unroll
         for (int j = 0; j < 2; j++) {
-          if (debug >= 2) continue;  // diagnostics: MMA/producer pipeline only
+          if (debug >= 2 && debug != 6) continue;  // diagnostics: MMA/producer pipeline only (2, 3, 7)
           if (group == 32) {
             insert_top<NK>(top, group_max<32>(v[j], 0));
           } else if (group == 8) {
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(NT, 1)
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[b]);
           }
-          if (debug >= 2) continue;
+          if (debug >= 2 && debug != 6) continue;
           const int c0 = n * NC + col;
 #pragma unroll
           for (int u = 0; u < 32; u++) {
