@@ -421,6 +421,7 @@ __global__ void __launch_bounds__(NT, 1)
       inv = build_A(tile, 0);
     }
     float S = iters > 0 ? scale(tile) : 0.0f;
+    asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // every thread is done with xs before the next load_x
     uint32_t li = 0;
     // debug 6: per-phase clock64 timeline of CTA 0, epilogue thread 0 (into val_out)
     const bool tl = (debug == 6 || debug == 7) && blockIdx.x == 0 && e == 0 && val_out;
@@ -468,14 +469,19 @@ __global__ void __launch_bounds__(NT, 1)
       mark(it, 2);
 
       // union of both halves' lists: half 1 publishes, half 0 merges and publishes the threshold
+      // (published through half 1's own candidate columns: free until its pass 1; the merged-window
+      // arrays may still be in use by half 0 finishing the previous tile)
+      float* pub = cv + (e | 128);
+      float* pub2 = reinterpret_cast<float*>(ci + (e | 128));
       if (h == 1) {
 #pragma unroll
-        for (int i = 0; i < NK; i++) mv[i * TM + r] = top[i];
+        for (int i = 0; i < NK; i++) (i < CAP ? pub[i * NEPI] : pub2[(i - CAP) * NEPI]) = top[i];
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
       if (h == 0) {
 #pragma unroll
-        for (int i = 0; i < NK; i++) insert_top<NK>(top, i >= NK - K ? mv[i * TM + r] : -INFINITY);
+        for (int i = 0; i < NK; i++)
+          insert_top<NK>(top, i >= NK - K ? (i < CAP ? pub[i * NEPI] : pub2[(i - CAP) * NEPI]) : -INFINITY);
         // every exact score of the K group maxima is >= (their 1xTF32 score) - kappa1 S
         kth1[r] = kth_of<NK>(top, K) - kappa1 * S * inv - 3.0f * m;
       }
@@ -620,6 +626,12 @@ __global__ void __launch_bounds__(NT, 1)
             rest &= rest - 1u;
             if (i >= 0) ev[i * TM + r] = exact_score(xr, exact + (int64_t)mi[i * TM + r] * (2 * F + 2), F);
           }
+        }
+        if (debug == 8 && val_out && t < T) {  // diagnostics: the tile's per-frame scales
+          val_out[t * K + 0] = inv;
+          val_out[t * K + 1] = S;
+          val_out[t * K + 2] = m2;
+          val_out[t * K + 3] = (double)li;
         }
         if (good) {
           if (debug) {  // diagnostics: s~ - s of the s~-ordered window
