@@ -383,3 +383,33 @@ def test_tensor_core_preselection_stable_across_runs_and_tile_counts(gpu, monkey
     for t in bad:  # same multiset of scores up to ties at the 1e-9 level
         np.testing.assert_allclose(np.sort(ll[t, first[t]]), np.sort(ll[t, ref[t]]), rtol=1e-9, atol=0)
     assert bad.size <= max(1, T // 1000)
+
+
+@pytest.mark.parametrize("C,T,xf64", [(64, 60000, False), (300, 20000, True)], ids=["c64_many_tiles", "c300_f64"])
+def test_whitening_kernel_many_tiles_matches_oracle_and_is_reproducible(gpu, C, T, xf64):
+    """whiten_ll_kernel (selected-pair full-covariance LLs, FP64 DMMA): many tiles per CTA with
+    component switches; values equal the oracle's Cholesky/solve LLs to 1e-11 and are bit-identical
+    between runs."""
+    import torch
+    from paper_1906_08556_b200 import _lib
+    (w, mu, var), full, x = orc.posterior_ubm(C, 20, 0.5, seed=C, n_frames=T)
+    if xf64:
+        x = x.astype(np.float64)
+    fm = gpu.gmm.GmmFull(*full)
+    tab = fm.device_table()
+    rng = np.random.default_rng(1)
+    sel = np.stack([rng.permutation(C)[:20] for _ in range(T)]).astype(np.int32)
+    xd = gpu._device.frames_to_device(x)
+    seld = torch.from_numpy(sel).cuda()
+    outs = []
+    for _ in range(2):
+        out = _lib.empty((T, 20))
+        nbytes = int(_lib.load().tvk_full_loglik_workspace_bytes(T, 20, C))
+        ws = _lib.empty((nbytes,), torch.uint8)
+        xp, xfl = _lib.x_args(xd)
+        _lib.call("tvk_full_loglik_selected", xp, xfl, T, 20, None, _lib.ptr(tab.prec), C, 20, 0, _lib.ptr(seld),
+                  _lib.ptr(out), _lib.ptr(ws), nbytes, _lib.stream())
+        outs.append(out.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    ll = orc.full_loglik(*full, x[:2000].astype(np.float64))
+    np.testing.assert_allclose(outs[0][:2000], np.take_along_axis(ll, sel[:2000], 1), rtol=1e-11, atol=1e-9)
