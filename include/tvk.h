@@ -97,8 +97,11 @@ int tvk_diag_table(const double* weights, const double* means, const double* var
 int tvk_full_table(const double* weights, const double* means, const double* covariances, int C, int F,
                    double* table, int32_t* status, void* stream);
 
-/* Per-component precision table for the grouped path, stride tvk_precision_table_stride(F):
- * [Sigma_c^-1 (F x F) | mu_c (F) | log w_c - (F log 2pi + log|Sigma_c|)/2 | 0].  status as above. */
+/* Per-component whitening table for the grouped (default) path, stride tvk_precision_table_stride(F)
+ * = 64*64 + 64 + 4 doubles: [U_c = L_c^-T (Sigma_c = L_c L_c^T; upper triangular, zero padded to
+ * 64 x 64) | mu_c (zero padded to 64) | log w_c - (F log 2pi + log|Sigma_c|)/2 | 0 0 0], so that
+ * ll_c(x) = const_c - ||(x - mu_c) U_c||^2 / 2 (gmm.py:111-118's Cholesky + triangular solve).
+ * F <= 64.  status as above. */
 int tvk_precision_table(const double* weights, const double* means, const double* covariances, int C, int F,
                         double* table, int32_t* status, void* stream);
 int64_t tvk_precision_table_stride(int F);
