@@ -16,10 +16,10 @@
 #include "gemm_f64.cuh"
 #include "internal.h"
 #include "spd_small.cuh"
+#include "finalize.cuh"
 
 namespace tvk {
 
-constexpr int kMaxTopK = 32;
 
 // ----------------------------------------------------------------------------- tables
 
@@ -391,48 +391,13 @@ __global__ void finalize_kernel(int64_t T, int K, double prune, const int32_t* s
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= T) return;
   double ll[kMaxTopK];
-  int id[kMaxTopK];
-  double mx = -INFINITY;
+  int id[kMaxTopK], oc[kMaxTopK];
+  float ow[kMaxTopK];
   for (int j = 0; j < K; j++) {
     ll[j] = sel_ll[t * K + j];
     id[j] = sel[t * K + j];
-    mx = fmax(mx, ll[j]);
   }
-  if (!isfinite(mx)) mx = 0.0;  // scipy logsumexp convention
-  double s = 0.0;
-  for (int j = 0; j < K; j++) s += exp(ll[j] - mx);
-  double lse = log(s) + mx;
-  int nkeep = 0, best = 0;
-  for (int j = 0; j < K; j++) {
-    ll[j] = exp(ll[j] - lse);  // posterior over the selection
-    if (ll[j] > ll[best]) best = j;
-    if (ll[j] >= prune) nkeep++;
-  }
-  bool degenerate = nkeep == 0;
-  double tot = 0.0;
-  for (int j = 0; j < K; j++) {
-    bool keep = degenerate ? (j == best) : (ll[j] >= prune);
-    if (!keep) ll[j] = 0.0;
-    tot += ll[j];
-  }
-  // emit kept entries sorted by component (insertion sort, K <= 32)
-  int n = 0;
-  int oc[kMaxTopK];
-  float ow[kMaxTopK];
-  for (int j = 0; j < K; j++) {
-    bool keep = degenerate ? (j == best) : (ll[j] >= prune);
-    if (!keep) continue;
-    float wv = (float)(ll[j] / tot);
-    int c = id[j];
-    int p = n++;
-    while (p > 0 && oc[p - 1] > c) {
-      oc[p] = oc[p - 1];
-      ow[p] = ow[p - 1];
-      p--;
-    }
-    oc[p] = c;
-    ow[p] = wv;
-  }
+  const int n = finalize_frame(K, prune, ll, id, oc, ow);
   for (int e = 0; e < n; e++) {
     comp_pad[t * K + e] = oc[e];
     w_pad[t * K + e] = ow[e];
@@ -586,6 +551,11 @@ extern "C" int64_t tvk_align_workspace_bytes(int64_t T, int K, int C) { return (
 
 namespace tvk {
 
+static bool sparse_disabled() {  // TVK_ALIGN_SPARSE=1 opts into the approximate + exact path (align_grouped.cu)
+  const char* e = getenv("TVK_ALIGN_SPARSE");
+  return !(e && strcmp(e, "1") == 0);
+}
+
 static bool select_dmma_forced() {  // TVK_SELECT=dmma: the FP64 DMMA preselection (A/B comparisons)
   const char* e = getenv("TVK_SELECT");
   return e && strcmp(e, "dmma") == 0;
@@ -672,11 +642,18 @@ static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, c
   AlignWs w = carve(workspace, T, K, C);
   TVK_REQUIRE(workspace != nullptr && (int64_t)w.bytes <= workspace_bytes, "align_frames: workspace too small");
   TVK_TRY(launch_select<XT>(x, T, F, diag_table, C, K, w.sel, nullptr, st));
-  TVK_TRY(full_ll_dispatch<XT>(x, T, F, full_table, prec_table, C, K, flags, w.sel, w.sel_ll, w.group,
-                               w.group_bytes, st));
   int fb = (int)((T + 127) / 128);
-  finalize_kernel<<<fb, 128, 0, st>>>(T, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts);
-  TVK_CHECK_LAUNCH("finalize");
+  if (!(flags & TVK_ALIGN_DENSE) && sel_ll_out == nullptr && !sparse_disabled()) {
+    // FP64 log-likelihoods only where the kept set or its weights need them
+    TVK_REQUIRE(prec_table != nullptr, "align_frames: grouped mode needs the precision table");
+    TVK_TRY(grouped_align_sparse<XT>(x, T, F, prec_table, C, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad,
+                                     w.counts, w.group, w.group_bytes, st));
+  } else {
+    TVK_TRY(full_ll_dispatch<XT>(x, T, F, full_table, prec_table, C, K, flags, w.sel, w.sel_ll, w.group,
+                                 w.group_bytes, st));
+    finalize_kernel<<<fb, 128, 0, st>>>(T, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts);
+    TVK_CHECK_LAUNCH("finalize");
+  }
   TVK_TRY(exclusive_scan_counts(w.counts, T, offsets, w.block_sums, st));
   compact_kernel<<<fb, 128, 0, st>>>(T, K, offsets, w.comp_pad, w.w_pad, components, weights);
   TVK_CHECK_LAUNCH("compact");

@@ -18,6 +18,8 @@
 #include "common.cuh"
 #include "internal.h"
 #include "spd_small.cuh"
+#include "finalize.cuh"
+#include "tc.cuh"
 
 namespace tvk {
 
@@ -79,13 +81,13 @@ __global__ void whiten_table_kernel(const double* w, const double* mu, const dou
   }
 }
 
-__global__ void pair_hist_kernel(const int32_t* sel, int64_t n_pairs, int C, int* hist) {
+__global__ void pair_hist_kernel(const int32_t* sel, const uint8_t* need, int64_t n_pairs, int C, int* hist) {
   extern __shared__ int lh[];
   for (int c = threadIdx.x; c < C; c += blockDim.x) lh[c] = 0;
   __syncthreads();
   int64_t base = (int64_t)blockIdx.x * kSortChunk;
   for (int i = threadIdx.x; i < kSortChunk; i += blockDim.x)
-    if (base + i < n_pairs) atomicAdd(&lh[sel[base + i]], 1);
+    if (base + i < n_pairs && (!need || need[base + i])) atomicAdd(&lh[sel[base + i]], 1);
   __syncthreads();
   for (int c = threadIdx.x; c < C; c += blockDim.x)
     if (lh[c]) atomicAdd(&hist[c], lh[c]);
@@ -118,7 +120,8 @@ __global__ void hist_scan_kernel(int* hist, int C, int* start, int* cursor) {
   }
 }
 
-__global__ void pair_scatter_kernel(const int32_t* sel, int64_t n_pairs, int C, int* cursor, int32_t* sorted) {
+__global__ void pair_scatter_kernel(const int32_t* sel, const uint8_t* need, int64_t n_pairs, int C, int* cursor,
+                                    int32_t* sorted) {
   extern __shared__ int sh[];
   int* lh = sh;       // local counts -> local cursor
   int* lb = sh + C;   // global base per component
@@ -130,7 +133,7 @@ __global__ void pair_scatter_kernel(const int32_t* sel, int64_t n_pairs, int C, 
 #pragma unroll
   for (int k = 0; k < PER; k++) {
     int64_t p = base + threadIdx.x + k * GT;
-    comp[k] = p < n_pairs ? sel[p] : -1;
+    comp[k] = (p < n_pairs && (!need || need[p])) ? sel[p] : -1;
     rank[k] = comp[k] >= 0 ? atomicAdd(&lh[comp[k]], 1) : 0;
   }
   __syncthreads();
@@ -294,6 +297,10 @@ __global__ void __launch_bounds__(GT, 2)
 }
 
 struct GroupWs {
+  double* approx_ll;  // sparse path: 3xTF32 log-likelihood of every pair of the window
+  float* approx_err;  // and its rigorous error bound
+  uint8_t* need;      // pairs that need the exact FP64 value
+  int2* state;        // per frame: (kept set known, kept mask)
   int* hist;
   int* start;
   int* cursor;
@@ -315,6 +322,10 @@ static GroupWs group_carve(void* base, int64_t n_pairs, int C) {
     off += gup(n);
     return p;
   };
+  w.approx_ll = (double*)take(sizeof(double) * n_pairs);
+  w.approx_err = (float*)take(sizeof(float) * n_pairs);
+  w.need = (uint8_t*)take(n_pairs);
+  w.state = (int2*)take(sizeof(int2) * n_pairs);  // >= frames of the window
   w.hist = (int*)take(sizeof(int) * C);
   w.start = (int*)take(sizeof(int) * (C + 1));
   w.cursor = (int*)take(sizeof(int) * C);
@@ -342,6 +353,21 @@ static int launch_whiten(const XT* x, int F, const double* tab, int K, const Gro
   return TVK_OK;
 }
 
+// bucket the window's pairs (optionally only those with need[p]) by component into <=128-pair tiles
+static int sort_tiles(const int32_t* wsel, const uint8_t* need, int64_t np, int C, const GroupWs& w,
+                      cudaStream_t st) {
+  cudaMemsetAsync(w.hist, 0, sizeof(int) * C, st);
+  int nchunks = (int)((np + kSortChunk - 1) / kSortChunk);
+  pair_hist_kernel<<<nchunks, GT, sizeof(int) * C, st>>>(wsel, need, np, C, w.hist);
+  hist_scan_kernel<<<1, 1024, 0, st>>>(w.hist, C, w.start, w.cursor);
+  pair_scatter_kernel<<<nchunks, GT, sizeof(int) * 2 * C, st>>>(wsel, need, np, C, w.cursor, w.sorted);
+  tile_count_kernel<<<(C + 255) / 256, 256, 0, st>>>(w.hist, C, w.ntile);
+  hist_scan_kernel<<<1, 1024, 0, st>>>(w.ntile, C, w.tile_start, w.cursor);
+  tile_build_kernel<<<(C + 255) / 256, 256, 0, st>>>(w.hist, w.start, w.tile_start, C, w.tiles);
+  TVK_CHECK_LAUNCH("pair sort");
+  return TVK_OK;
+}
+
 template <typename XT>
 int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, int K, const int32_t* sel,
                     double* sel_ll, void* ws_base, int64_t ws_bytes, cudaStream_t st) {
@@ -365,15 +391,7 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
     const int64_t nf = std::min<int64_t>(win, T - f0);
     const int64_t np = nf * K;
     const int32_t* wsel = sel + f0 * K;
-    cudaMemsetAsync(w.hist, 0, sizeof(int) * C, st);
-    int nchunks = (int)((np + kSortChunk - 1) / kSortChunk);
-    pair_hist_kernel<<<nchunks, GT, sizeof(int) * C, st>>>(wsel, np, C, w.hist);
-    hist_scan_kernel<<<1, 1024, 0, st>>>(w.hist, C, w.start, w.cursor);
-    pair_scatter_kernel<<<nchunks, GT, sc_smem, st>>>(wsel, np, C, w.cursor, w.sorted);
-    tile_count_kernel<<<(C + 255) / 256, 256, 0, st>>>(w.hist, C, w.ntile);
-    hist_scan_kernel<<<1, 1024, 0, st>>>(w.ntile, C, w.tile_start, w.cursor);
-    tile_build_kernel<<<(C + 255) / 256, 256, 0, st>>>(w.hist, w.start, w.tile_start, C, w.tiles);
-    TVK_CHECK_LAUNCH("pair sort");
+    TVK_TRY(sort_tiles(wsel, nullptr, np, C, w, st));
     // the kernel reads the tile count from tile_start[C]
     GroupWs wc = w;
     wc.tile_start = w.tile_start + C;
@@ -384,6 +402,282 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
   }
   return TVK_OK;
 }
+
+// ============================================================================ sparse (approximate + exact)
+// align_frames only needs FP64 log-likelihoods for the entries it keeps (weights exp(ll - lse_kept))
+// and for frames whose prune decision is not certain.  whiten_approx_kernel evaluates every pair's
+// Z = (x - mu) U with tcgen05 3xTF32 (A = rows in TMEM, B = U in shared memory) together with a
+// rigorous bound |q~ - q| <= sum_j (2|z~_j| e_j + e_j^2), e_j = kappa_z ||y||_2 ||U_:,j||_2;
+// decide_kernel proves the kept set (or flags the frame); the FP64 whitening kernel then runs on the
+// flagged pairs only (~4.3 of 20 per frame on the config-2 data) and finalize_sparse writes weights.
+constexpr int AT = 128;                      // threads of the approximate kernel: one pair row each
+constexpr float KAPPA_Z = 1.0f / 262144.0f;  // 3xTF32 relative error bound
+
+template <typename XT>
+struct ApproxSmem {
+  float B[2][GP * GP];  // U^T hi / lo words (N = 64 output dims x K = 64 features, K-major core matrices)
+  double mu[GP];
+  float cn[GP];         // ||U[:, j]||_2, rounded up
+  double cst[2];        // const (16 bytes: keeps X 16-byte aligned for cp.async)
+  XT X[2][GROWS * GS];  // frame rows (columns F..63 stay zero)
+  int pair[2][GROWS];
+  uint64_t mbar;
+  uint32_t tbase;
+};
+
+template <typename XT, bool VEC>
+__global__ void __launch_bounds__(AT)
+    whiten_approx_kernel(const XT* __restrict__ x, int F, const double* __restrict__ tab, int K, uint64_t kinv,
+                         const int32_t* __restrict__ sorted, const int4* __restrict__ tiles,
+                         const int* __restrict__ ntile_p, double* __restrict__ approx_ll,
+                         float* __restrict__ approx_err) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  ApproxSmem<XT>& S = *reinterpret_cast<ApproxSmem<XT>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ntiles = *ntile_p;
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int tb = blockIdx.x * per, te = min(tb + per, ntiles);
+  if (tb >= te) return;
+  for (int i = tid; i < 2 * GROWS * GS; i += AT) (&S.X[0][0])[i] = (XT)0;
+  if (tid == 0) {
+    tc::mbar_init(&S.mbar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<256>(&S.tbase);  // A hi [0,64) | A lo [64,128) | Z [128,192)
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = S.tbase, lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+
+  auto issue = [&](int ti, int b) {  // frame rows of tile ti into buffer b (cp.async), as whiten_ll
+    const int4 d = tiles[ti];
+    for (int r = tid; r < GROWS; r += AT) S.pair[b][r] = r < d.y ? sorted[d.x + r] : -1;
+    const int per_row = VEC ? (F * (int)sizeof(XT)) / 16 : F;
+    for (int r = warp; r < d.y; r += AT / 32) {
+      const XT* src = x + (int64_t)(((uint64_t)(uint32_t)sorted[d.x + r] * kinv) >> 40) * F;
+      for (int c = lane; c < per_row; c += 32) {
+        if (VEC) cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
+                            reinterpret_cast<const uint8_t*>(src) + 16 * c, 16);
+        else cp_async_elem<(int)sizeof(XT)>(&S.X[b][r * GS + c], src + c);
+      }
+    }
+    cp_async_commit();
+  };
+
+  int comp = -1;
+  uint32_t phase = 0;
+  issue(tb, 0);
+  for (int ti = tb; ti < te; ti++) {
+    const int xb = (ti - tb) & 1;
+    const int4 d = tiles[ti];
+    if (d.z != comp) {  // stage U^T as TF32 hi/lo, column norms, mu, const
+      __syncthreads();
+      const double* src = tab + (int64_t)d.z * kWhitenStride;
+      for (int idx = tid; idx < GP * GP; idx += AT) {
+        const int i = idx / GP, j = idx % GP;  // U[i][j] -> B[j][i]
+        const float u = (float)src[idx];
+        const float hi = tc::tf32_round(u), lo = tc::tf32_round(u - hi);
+        const uint32_t o = tc::kmajor_offset(j, i, GP) / 4;
+        S.B[0][o] = hi;
+        S.B[1][o] = lo;
+      }
+      for (int j = warp; j < GP; j += AT / 32) {
+        double c2 = 0.0;
+        for (int i = lane; i < GP; i += 32) c2 += src[i * GP + j] * src[i * GP + j];
+        c2 = warp_sum(c2);
+        if (lane == 0) S.cn[j] = __double2float_ru(sqrt(c2)) * (1.0f + 1.0f / 1048576.0f);
+      }
+      for (int i = tid; i < GP; i += AT) S.mu[i] = src[GP * GP + i];
+      if (tid == 0) S.cst[0] = src[GP * GP + GP];
+      tc::fence_proxy_async();  // the tensor core reads B through the async proxy
+      comp = d.z;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (ti + 1 < te) issue(ti + 1, xb ^ 1);
+    // A rows: y = x - mu (FP64 difference, then f32), TF32 hi/lo words into TMEM
+    const int r = tid;
+    double yn2 = 0.0;
+    {
+      float wh[32], wl[32];
+#pragma unroll 1
+      for (int j = 0; j < 2; j++) {
+#pragma unroll
+        for (int u = 0; u < 32; u++) {
+          const int i = 32 * j + u;
+          const float y = i < F ? (float)((double)S.X[xb][r * GS + i] - S.mu[i]) : 0.0f;
+          yn2 += (double)y * y;
+          wh[u] = tc::tf32_round(y);
+          wl[u] = tc::tf32_round(y - wh[u]);
+        }
+        tc::tmem_st32(lane_addr + 32 * j, wh);
+        tc::tmem_st32(lane_addr + 64 + 32 * j, wl);
+      }
+    }
+    tc::tmem_st_wait();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+      const uint32_t idesc = tc::idesc_tf32(GROWS, GP);
+      const uint32_t b0 = tc::smem_u32(S.B[0]), b1 = tc::smem_u32(S.B[1]);
+      const int ks = (F + 7) / 8;
+      for (int k = 0; k < ks; k++) {
+        const uint64_t bh = tc::smem_desc(b0 + 256 * k, 128, 8 * GP * 4);
+        const uint64_t bl = tc::smem_desc(b1 + 256 * k, 128, 8 * GP * 4);
+        tc::mma_tf32_ts(tmem + 128, tmem + 8 * k, bh, idesc, k > 0);
+        tc::mma_tf32_ts(tmem + 128, tmem + 8 * k, bl, idesc, 1);
+        tc::mma_tf32_ts(tmem + 128, tmem + 64 + 8 * k, bh, idesc, 1);
+      }
+      tc::mma_commit(&S.mbar);
+    }
+    tc::mbar_wait(&S.mbar, phase);
+    phase ^= 1u;
+    tc::fence_after_sync();
+    double q = 0.0, dq = 0.0;
+    const double ynorm = sqrt(yn2) * (1.0 + 1e-6);
+#pragma unroll 1
+    for (int j = 0; j < 2; j++) {
+      float z[32];
+      tc::tmem_ld32(lane_addr + 128 + 32 * j, z);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int u = 0; u < 32; u++) {
+        const double zz = z[u];
+        const double ej = (double)KAPPA_Z * ynorm * S.cn[32 * j + u];
+        q = fma(zz, zz, q);
+        dq += (2.0 * fabs(zz) + ej) * ej;
+      }
+    }
+    if (r < d.y) {
+      const int p = S.pair[xb][r];
+      approx_ll[p] = S.cst[0] - 0.5 * q;
+      approx_err[p] = __double2float_ru(0.5 * dq * (1.0 + 1e-6) + 1e-12 * fabs(q));
+    }
+    tc::fence_before_sync();
+  }
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<256>(tmem);
+}
+
+// per frame: prove the kept set from the approximate values or ask for every exact value
+__global__ void decide_kernel(int64_t nf, int K, double prune, const double* __restrict__ approx_ll,
+                              const float* __restrict__ approx_err, uint8_t* __restrict__ need,
+                              int2* __restrict__ state) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nf) return;
+  const double* ll = approx_ll + t * K;
+  const float* er = approx_err + t * K;
+  bool ok = true;
+  double mx = -INFINITY, D = 0.0;
+  for (int j = 0; j < K; j++) {
+    ok = ok && isfinite(ll[j]) && isfinite(er[j]);
+    mx = fmax(mx, ll[j]);
+    D = fmax(D, (double)er[j]);
+  }
+  unsigned kept = 0u;
+  if (ok) {
+    double s = 0.0;
+    for (int j = 0; j < K; j++) s += exp(ll[j] - mx);
+    const double lse = log(s) + mx;
+    const double lp = log(prune);  // -inf for prune = 0: everything is kept
+    const double tie = 1e-12;
+    for (int j = 0; j < K && ok; j++) {
+      const double lo = ll[j] - er[j] - (lse + D), hi = ll[j] + er[j] - (lse - D);
+      if (lo >= lp + tie) kept |= 1u << j;
+      else if (!(hi < lp - tie)) ok = false;
+    }
+    if (ok && kept == 0u) {  // degenerate: the arg-max (first in selection order) must be certain
+      int best = 0;
+      for (int j = 1; j < K; j++)
+        if (ll[j] > ll[best]) best = j;
+      for (int j = 0; j < K && ok; j++)
+        if (j != best && !(ll[best] - er[best] > ll[j] + er[j])) ok = false;
+      kept = 1u << best;
+    }
+  }
+  const bool exact_kept = ok && __popc(kept) > 1;
+  for (int j = 0; j < K; j++) need[t * K + j] = !ok || (exact_kept && ((kept >> j) & 1u));
+  state[t] = make_int2(ok ? 1 : 0, (int)kept);
+}
+
+__global__ void finalize_sparse_kernel(int64_t nf, int K, double prune, const int32_t* sel, const double* sel_ll,
+                                       const int2* state, int32_t* comp_pad, float* w_pad, int64_t* counts) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nf) return;
+  double ll[kMaxTopK];
+  int id[kMaxTopK], oc[kMaxTopK];
+  float ow[kMaxTopK];
+  const int2 s = state[t];
+  for (int j = 0; j < K; j++) {
+    id[j] = sel[t * K + j];
+    ll[j] = (s.x == 0 || ((s.y >> j) & 1)) ? sel_ll[t * K + j] : 0.0;
+  }
+  const int n = s.x == 0 ? finalize_frame(K, prune, ll, id, oc, ow) : finalize_known(K, (unsigned)s.y, ll, id, oc, ow);
+  for (int e = 0; e < n; e++) {
+    comp_pad[t * K + e] = oc[e];
+    w_pad[t * K + e] = ow[e];
+  }
+  counts[t] = n;
+}
+
+template <typename XT, bool VEC>
+static int launch_approx(const XT* x, int F, const double* tab, int K, uint64_t kinv, const GroupWs& w,
+                         const int* ntile, int sms, cudaStream_t st) {
+  const size_t smem = sizeof(ApproxSmem<XT>);
+  cudaFuncSetAttribute(whiten_approx_kernel<XT, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  whiten_approx_kernel<XT, VEC><<<2 * sms, AT, smem, st>>>(x, F, tab, K, kinv, w.sorted, w.tiles, ntile,
+                                                            w.approx_ll, w.approx_err);
+  TVK_CHECK_LAUNCH("whiten_approx");
+  return TVK_OK;
+}
+
+// align_frames' stages 2-3 (gmm.py:412-438) for the grouped path: frames in L2-sized windows;
+// per window the approximate LLs of all pairs, the kept-set proof, FP64 LLs for the pairs that need
+// them and the per-frame CSR rows (comp_pad / w_pad / counts of the window's frames).
+template <typename XT>
+int grouped_align_sparse(const XT* x, int64_t T, int F, const double* ptab, int C, int K, double prune,
+                         const int32_t* sel, double* sel_ll, int32_t* comp_pad, float* w_pad, int64_t* counts,
+                         void* ws_base, int64_t ws_bytes, cudaStream_t st) {
+  TVK_REQUIRE(F <= GP, "grouped full log-likelihood supports F <= 64");
+  TVK_REQUIRE(K >= 1 && K <= 32, "grouped full log-likelihood supports K <= 32");
+  TVK_REQUIRE(C <= 8192, "grouped full log-likelihood supports C <= 8192");
+  TVK_REQUIRE(T * K < (1ll << 31) - 1, "too many (frame, component) pairs for one call");
+  const int64_t win = std::min<int64_t>(T, kGroupWindowFrames);
+  GroupWs w = group_carve(ws_base, win * K, C);
+  TVK_REQUIRE(ws_base != nullptr && (int64_t)w.bytes <= ws_bytes, "grouped full log-likelihood: workspace too small");
+  cudaFuncSetAttribute(pair_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int) * 2 * C));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool vec = ((F * sizeof(XT)) % 16 == 0) && ((uintptr_t)x % 16 == 0);
+  const uint64_t kinv = ((1ull << 40) + K - 1) / K;
+  GroupWs wc = w;
+  wc.tile_start = w.tile_start + C;  // the kernels read the tile count from tile_start[C]
+  for (int64_t f0 = 0; f0 < T; f0 += win) {
+    const int64_t nf = std::min<int64_t>(win, T - f0);
+    const int64_t np = nf * K;
+    const int32_t* wsel = sel + f0 * K;
+    const XT* wx = x + f0 * F;
+    TVK_TRY(sort_tiles(wsel, nullptr, np, C, w, st));
+    if (vec) TVK_TRY((launch_approx<XT, true>(wx, F, ptab, K, kinv, w, wc.tile_start, sms, st)));
+    else TVK_TRY((launch_approx<XT, false>(wx, F, ptab, K, kinv, w, wc.tile_start, sms, st)));
+    decide_kernel<<<(int)((nf + 127) / 128), 128, 0, st>>>(nf, K, prune, w.approx_ll, w.approx_err, w.need, w.state);
+    TVK_CHECK_LAUNCH("decide");
+    TVK_TRY(sort_tiles(wsel, w.need, np, C, w, st));
+    if (vec) TVK_TRY((launch_whiten<XT, true>(wx, F, ptab, K, wc, sel_ll + f0 * K, sms, st)));
+    else TVK_TRY((launch_whiten<XT, false>(wx, F, ptab, K, wc, sel_ll + f0 * K, sms, st)));
+    finalize_sparse_kernel<<<(int)((nf + 127) / 128), 128, 0, st>>>(nf, K, prune, wsel, sel_ll + f0 * K, w.state,
+                                                                    comp_pad + f0 * K, w_pad + f0 * K, counts + f0);
+    TVK_CHECK_LAUNCH("finalize_sparse");
+  }
+  return TVK_OK;
+}
+template int grouped_align_sparse<float>(const float*, int64_t, int, const double*, int, int, double, const int32_t*,
+                                         double*, int32_t*, float*, int64_t*, void*, int64_t, cudaStream_t);
+template int grouped_align_sparse<double>(const double*, int64_t, int, const double*, int, int, double,
+                                          const int32_t*, double*, int32_t*, float*, int64_t*, void*, int64_t,
+                                          cudaStream_t);
 
 template int grouped_full_ll<float>(const float*, int64_t, int, const double*, int, int, const int32_t*, double*,
                                     void*, int64_t, cudaStream_t);

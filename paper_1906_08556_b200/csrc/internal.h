@@ -48,3 +48,11 @@ template <typename XT>
 int select_tc(const XT* x, int64_t T, int F, const double* tab, int C, int K, int32_t* sel, double* val,
               cudaStream_t st);
 }  // namespace tvk
+
+namespace tvk {
+// approximate (tcgen05 3xTF32) + exact (FP64, kept/ambiguous pairs only) stages 2-3 of align_frames
+template <typename XT>
+int grouped_align_sparse(const XT* x, int64_t T, int F, const double* ptab, int C, int K, double prune,
+                         const int32_t* sel, double* sel_ll, int32_t* comp_pad, float* w_pad, int64_t* counts,
+                         void* ws_base, int64_t ws_bytes, cudaStream_t st);
+}  // namespace tvk

@@ -413,3 +413,16 @@ def test_whitening_kernel_many_tiles_matches_oracle_and_is_reproducible(gpu, C, 
     np.testing.assert_array_equal(outs[0], outs[1])
     ll = orc.full_loglik(*full, x[:2000].astype(np.float64))
     np.testing.assert_allclose(outs[0][:2000], np.take_along_axis(ll, sel[:2000], 1), rtol=1e-11, atol=1e-9)
+
+
+@pytest.mark.parametrize("case", cases.ALIGN_CASES, ids=[c[0] for c in cases.ALIGN_CASES])
+def test_sparse_align_path_matches_reference_golden(gpu, monkeypatch, case):
+    """Opt-in approximate (tcgen05 3xTF32) + exact (FP64 on kept/ambiguous pairs) stage 2-3 path
+    (TVK_ALIGN_SPARSE=1): the same alignment as the reference goldens."""
+    monkeypatch.setenv("TVK_ALIGN_SPARSE", "1")
+    g = ALIGN[case[0]]
+    diag, full, x, k, prune, _ = cases.align_inputs(case)
+    dm, fm = _models(diag, full)
+    got = gpu.gmm.align_frames(dm, fm, x, top_k=k, prune=prune)
+    ties = np.flatnonzero(g["boundary_gap"] < TIE_REL * np.maximum(1.0, np.abs(g["sel_full_ll"][:, 0])))
+    _assert_alignment_matches(got, g["offsets"], g["components"], g["weights"], ties)
