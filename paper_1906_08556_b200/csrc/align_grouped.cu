@@ -453,8 +453,27 @@ __global__ void __launch_bounds__(AT)
     const int4 d = tiles[ti];
     for (int r = tid; r < GROWS; r += AT) S.pair[b][r] = r < d.y ? sorted[d.x + r] : -1;
     const int per_row = VEC ? (F * (int)sizeof(XT)) / 16 : F;
-    for (int r = warp; r < d.y; r += AT / 32) {
-      const XT* src = x + (int64_t)(((uint64_t)(uint32_t)sorted[d.x + r] * kinv) >> 40) * F;
+    // lane j fetches the frame of the warp's j-th row (rows warp, warp+4, ...): one round of loads
+    const int myrow = warp + (AT / 32) * lane;
+    const int myframe = myrow < d.y ? (int)(((uint64_t)(uint32_t)sorted[d.x + myrow] * kinv) >> 40) : 0;
+    if (VEC && per_row <= 16) {  // two rows per warp step: lanes 0-15 and 16-31
+      const int sub = lane >> 4, c = lane & 15;
+      for (int jr = 0; jr < GROWS / (AT / 32); jr += 2) {
+        const int r = warp + (AT / 32) * (jr + sub);
+        const int fr = __shfl_sync(0xffffffffu, myframe, jr + sub);
+        if (warp + (AT / 32) * jr >= d.y) break;
+        if (r < d.y && c < per_row)
+          cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
+                     reinterpret_cast<const uint8_t*>(x + (int64_t)fr * F) + 16 * c, 16);
+      }
+      cp_async_commit();
+      return;
+    }
+    for (int jr = 0; jr < GROWS / (AT / 32); jr++) {
+      const int r = warp + (AT / 32) * jr;
+      const int fr = __shfl_sync(0xffffffffu, myframe, jr);
+      if (r >= d.y) break;
+      const XT* src = x + (int64_t)fr * F;
       for (int c = lane; c < per_row; c += 32) {
         if (VEC) cp_async16(reinterpret_cast<uint8_t*>(&S.X[b][r * GS]) + 16 * c,
                             reinterpret_cast<const uint8_t*>(src) + 16 * c, 16);
@@ -534,8 +553,9 @@ __global__ void __launch_bounds__(AT)
     tc::mbar_wait(&S.mbar, phase);
     phase ^= 1u;
     tc::fence_after_sync();
-    double q = 0.0, dq = 0.0;
-    const double ynorm = sqrt(yn2) * (1.0 + 1e-6);
+    // q~ = sum z~^2 in f32 (its own rounding, <= 64 ulp of q~, joins the bound), bound in f32
+    float q = 0.0f, dq = 0.0f;
+    const float ky = KAPPA_Z * (float)sqrt(yn2) * 1.0001f;
 #pragma unroll 1
     for (int j = 0; j < 2; j++) {
       float z[32];
@@ -543,16 +563,15 @@ __global__ void __launch_bounds__(AT)
       tc::tmem_ld_wait();
 #pragma unroll
       for (int u = 0; u < 32; u++) {
-        const double zz = z[u];
-        const double ej = (double)KAPPA_Z * ynorm * S.cn[32 * j + u];
-        q = fma(zz, zz, q);
-        dq += (2.0 * fabs(zz) + ej) * ej;
+        const float ej = ky * S.cn[32 * j + u];
+        q = fmaf(z[u], z[u], q);
+        dq = fmaf(fmaf(2.0f, fabsf(z[u]), ej), ej, dq);
       }
     }
     if (r < d.y) {
       const int p = S.pair[xb][r];
-      approx_ll[p] = S.cst[0] - 0.5 * q;
-      approx_err[p] = __double2float_ru(0.5 * dq * (1.0 + 1e-6) + 1e-12 * fabs(q));
+      approx_ll[p] = S.cst[0] - 0.5 * (double)q;
+      approx_err[p] = (0.5f * dq + 4.0e-6f * q) * 1.001f + 1e-12f;
     }
     tc::fence_before_sync();
   }
