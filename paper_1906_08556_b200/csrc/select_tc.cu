@@ -361,66 +361,65 @@ __global__ void __launch_bounds__(NT, 1)
     // exponent 2^-E (max |v'| in [2^13, 2^14): no f16 overflow), split into f16 hi/lo and packed two
     // per TMEM column: half h writes features [64h, 64h+64) (hi words at a_col + 32h, lo 64 further).
     // Returns 2^-E: the tile's scores (and every threshold compared with them) are in units of 2^E.
-    auto build_A = [&](int64_t tile, uint32_t lt) -> float {
+    // A operand of a tile in three parts so that most of it overlaps the pass-1 chunk loop:
+    //  prep_A: frames landed (cp.async + barrier); frame exponent 2^-E and margin scale S_t;
+    //  piece_A(p): features [64h + 8p, +8) -> f16 hi/lo pairs -> 4 TMEM columns each (p = 0..7);
+    //  finish_A: make the stores visible to the MMA issuer.
+    struct Prep {
+      float inv, S;
+    };
+    auto prep_A = [&](int64_t tile) -> Prep {
       cp_async_wait<0>();
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // every thread's frame copies have landed
       const int64_t t = tile * TM + r;
+      if (t >= T) return Prep{1.0f, INFINITY};
+      const float* xr = xs + r * FP;
+      float mx = cs[2 * F], S = cmax;  // max |v_k| over the row (analytically) and S_t
+      for (int f = 0; f < F; f++) {
+        const float xv = xr[f];
+        mx = fmaxf(mx, fmaxf(xv * xv * cs[f], fabsf(xv) * cs[F + f]));
+        S += xv * xv * amax[f] + fabsf(xv) * bmax[f];
+      }
+      const int E = (mx > 0.0f && isfinite(mx)) ? ilogbf(mx) - 13 : 0;
+      return Prep{ldexpf(1.0f, -E), S};
+    };
+    auto piece_A = [&](int64_t tile, uint32_t lt, float inv, int pc) {
+      const int64_t t = tile * TM + r;
       const bool ok = t < T;
       const float* xr = xs + r * FP;
-      float mx = ok ? cs[2 * F] : 0.0f;  // max |v_k| over the row, analytically
-      if (ok)
-        for (int f = 0; f < F; f++) {
-          const float xv = xr[f];
-          mx = fmaxf(mx, fmaxf(xv * xv * cs[f], fabsf(xv) * cs[F + f]));
-        }
-      const int E = (mx > 0.0f && isfinite(mx)) ? ilogbf(mx) - 13 : 0;
-      const float inv = ldexpf(1.0f, -E);
-      if (64 * h < KP) {
-        float wh[32], wl[32];
+      float wh[4], wl[4];
 #pragma unroll
-        for (int u = 0; u < 64; u++) {
-          const int k = 64 * h + u;
-          float v = 0.0f;
-          if (ok && k == 2 * F) {
-            v = cs[k] * inv;
-          } else if (ok && k < 2 * F) {
-            const float xv = xr[k < F ? k : k - F];
-            v = (k < F ? xv * xv : xv) * cs[k] * inv;
-          }
-          const __half hi = __float2half_rn(v), lo = __float2half_rn(v - __half2float(hi));
-          __half* ph = reinterpret_cast<__half*>(&wh[u >> 1]);
-          __half* pl = reinterpret_cast<__half*>(&wl[u >> 1]);
-          ph[u & 1] = hi;
-          pl[u & 1] = lo;
+      for (int u = 0; u < 8; u++) {
+        const int k = 64 * h + 8 * pc + u;
+        float v = 0.0f;
+        if (ok && k == 2 * F) {
+          v = cs[k] * inv;
+        } else if (ok && k < 2 * F) {
+          const float xv = xr[k < F ? k : k - F];
+          v = (k < F ? xv * xv : xv) * cs[k] * inv;
         }
-        tc::tmem_st32(lane_addr + a_col(lt) + 32 * h, wh);
-        tc::tmem_st32(lane_addr + a_col(lt) + 64 + 32 * h, wl);
+        const __half hi = __float2half_rn(v), lo = __float2half_rn(v - __half2float(hi));
+        reinterpret_cast<__half*>(&wh[u >> 1])[u & 1] = hi;
+        reinterpret_cast<__half*>(&wl[u >> 1])[u & 1] = lo;
       }
+      tc::tmem_st4(lane_addr + a_col(lt) + 32 * h + 4 * pc, wh);
+      tc::tmem_st4(lane_addr + a_col(lt) + 64 + 32 * h + 4 * pc, wl);
+    };
+    auto finish_A = [&](uint32_t lt) {
       tc::tmem_st_wait();
       tc::fence_before_sync();
       tc::mbar_arrive(&afull[lt & 1]);
-      return inv;
     };
-    // margin scale S_t = sum_f x_f^2 max|a_f| + |x_f| max|b_f| + max|c|
-    auto scale = [&](int64_t tile) -> float {
-      const int64_t t = tile * TM + r;
-      if (t >= T) return INFINITY;
-      const float* xr = xs + r * FP;
-      float S = cmax;
-      for (int f = 0; f < F; f++) {
-        const float xv = (float)xr[f];
-        S += xv * xv * amax[f] + fabsf(xv) * bmax[f];
-      }
-      return S;
-    };
-
     int64_t tile = blockIdx.x;
-    float inv = 1.0f;  // 2^-E of the current tile's frame (see build_A)
+    float inv = 1.0f, S = 0.0f;  // 2^-E and S_t of the current tile's frame (see prep_A)
     if (iters > 0) {
       load_x(tile);
-      inv = build_A(tile, 0);
+      const Prep p0 = prep_A(tile);
+      inv = p0.inv;
+      S = p0.S;
+      for (int pc = 0; pc < 8; pc++) piece_A(tile, 0, inv, pc);
+      finish_A(0);
     }
-    float S = iters > 0 ? scale(tile) : 0.0f;
     asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // every thread is done with xs before the next load_x
     uint32_t li = 0;
     // debug 6: per-phase clock64 timeline of CTA 0, epilogue thread 0 (into val_out)
@@ -466,7 +465,6 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       mark(it, 1);
-      mark(it, 2);
 
       // union of both halves' lists: half 1 publishes, half 0 merges and publishes the threshold
       // (published through half 1's own candidate columns: free until its pass 1; the merged-window
@@ -487,12 +485,16 @@ __global__ void __launch_bounds__(NT, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
       const float thr = live ? kth1[r] : INFINITY;
-      // A operand of the next tile into the other TMEM A buffer (its last reader, tile li-1, is done)
+      mark(it, 2);
+      // A operand of the next tile into the other TMEM A buffer (its last reader, tile li-1, is
+      // done): scales now, the feature pieces between the pass-1 chunks below
       float S_next = 0.0f, inv_next = 1.0f;
-      if (it + 1 < iters) {
+      const bool has_next = it + 1 < iters;
+      if (has_next) {
         if (li >= 1) tc::mbar_wait(&aempty[(li + 1) & 1], ((li - 1) >> 1) & 1);
-        inv_next = build_A(tile + gridDim.x, li + 1);
-        S_next = scale(tile + gridDim.x);
+        const Prep pn = prep_A(tile + gridDim.x);
+        inv_next = pn.inv;
+        S_next = pn.S;
       }
       mark(it, 3);
 
@@ -527,6 +529,11 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
         }
+        if (has_next && n < 8) piece_A(tile + gridDim.x, li + 1, inv_next, n);
+      }
+      if (has_next) {
+        for (int pc = NCH; pc < 8; pc++) piece_A(tile + gridDim.x, li + 1, inv_next, pc);
+        finish_A(li + 1);
       }
 
       // A operand of the next tile (all MMAs of this tile have completed: their last chunk was read)
