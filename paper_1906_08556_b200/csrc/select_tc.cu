@@ -490,12 +490,12 @@ __global__ void __launch_bounds__(NT, 1)
       // done): scales now, the feature pieces between the pass-1 chunks below
       float S_next = 0.0f, inv_next = 1.0f;
       const bool has_next = it + 1 < iters;
-      if (has_next) {
+      auto prep_next = [&]() {
         if (li >= 1) tc::mbar_wait(&aempty[(li + 1) & 1], ((li - 1) >> 1) & 1);
         const Prep pn = prep_A(tile + gridDim.x);
         inv_next = pn.inv;
         S_next = pn.S;
-      }
+      };
       mark(it, 3);
 
       // ---- pass 1 (3xTF32): collect every score >= thr
@@ -529,10 +529,11 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
         }
-        if (has_next && n < 8) piece_A(tile + gridDim.x, li + 1, inv_next, n);
+        if (has_next && n == 0) prep_next();
+        if (has_next && n >= 1 && n <= 8) piece_A(tile + gridDim.x, li + 1, inv_next, n - 1);
       }
       if (has_next) {
-        for (int pc = NCH; pc < 8; pc++) piece_A(tile + gridDim.x, li + 1, inv_next, pc);
+        for (int pc = NCH > 1 ? NCH - 1 : 0; pc < 8; pc++) piece_A(tile + gridDim.x, li + 1, inv_next, pc);
         finish_A(li + 1);
       }
 
