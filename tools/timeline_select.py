@@ -16,7 +16,7 @@ for dbg in ("6", "7"):
     sel, val = _device.select_topk(x, tab, 20, values=True)
     torch.cuda.synchronize()
     v = val.view(-1)[:64 * 8].cpu().numpy().reshape(64, 8)
-    names = ["start", "pass0 done", "A_lo built", "thr ready", "pass1 done", "nextA built", "merge done", "tile end"]
+    names = ["start", "pass0 done", "thr ready", "next A built", "pass1 done", "-", "merge done", "tile end"]
     d = np.diff(v[2:12], axis=1)
     print("debug", dbg, "mean cycles per phase (tiles 2-11):")
     for i in range(7):
