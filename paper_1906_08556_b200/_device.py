@@ -141,7 +141,7 @@ def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True, den
     return res
 
 
-STREAM_CHUNK = 1 << 20  # frames per chunk of the host-input alignment pipeline
+STREAM_CHUNK = 1 << 19  # frames per chunk of the host-input alignment pipeline
 _staging = {}             # (chunk, k) -> pinned host staging slots, reused across calls
 _copier = None
 
@@ -218,9 +218,25 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
         slot_busy[slot] = _copier.submit(unstage, lo, n, e, base, st, ev)
         return base + e
 
+    # piece sizes ramp up and down (chunk/4, chunk/2, chunk, ..., chunk/2, chunk/4) so that the first
+    # host->device copy and the last copy-out, which cannot overlap anything, are short
+    sizes, rest, q = [], T, max(1, chunk // 4)
+    for c in (q, 2 * q):
+        if rest > 0:
+            sizes.append(min(c, rest))
+            rest -= sizes[-1]
+    tail = []
+    for c in (q, 2 * q):
+        if rest > 4 * chunk:
+            tail.insert(0, c)
+            rest -= c
+    while rest > 0:
+        sizes.append(min(chunk, rest))
+        rest -= sizes[-1]
+    sizes += tail
     nd = 0
-    for i, lo in enumerate(range(0, T, chunk)):
-        n = min(chunk, T - lo)
+    lo = 0
+    for i, n in enumerate(sizes):
         buf = bufs[i % 2][:n]
         with torch.cuda.stream(copy_stream):
             if free[i % 2] is not None:
@@ -237,6 +253,7 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
             base = drain(pending, base, nd % 2)
             nd += 1
         pending = (lo, n, res, done)
+        lo += n
     if pending is not None:
         base = drain(pending, base, nd % 2)
     for f in slot_busy:
