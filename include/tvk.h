@@ -21,6 +21,9 @@
  *   tvk_posterior           _posterior_terms                   tvm.py:183-215 (chol, Phi, phi, logdet)
  *   tvk_spd_solve_rows      update_T                           tvm.py:317-334
  *   tvk_sigma_floor         update_sigma + floor_eigenvalues   tvm.py:337-358, _linalg.py:15-24
+ *   tvk_row_softmax         UBM EM responsibilities            gmm.py:284-287, 345-348
+ *   tvk_seed_dist2          _seed_means distance update        gmm.py:228-243
+ *   tvk_full_moments        train_gmm_full M-step moments      gmm.py:350-366
  */
 #ifndef TVK_H_
 #define TVK_H_
@@ -68,6 +71,9 @@ int tvk_dgemm(int trans_a, int trans_b, int m, int n, int k, double alpha, const
 int tvk_colsum(const double* a, int64_t rows, int64_t cols, int64_t lda, double alpha, double beta, double* out,
                void* stream);
 int64_t tvk_ddot_workspace_bytes(void);
+/* Row log-sum-exp and softmax in place (GMM E-step responsibilities, gmm.py:284-287, 345-348):
+ * norm[r] = logsumexp(a[r, :]), a[r, :] <- exp(a[r, :] - norm[r]); rows x cols row-major. */
+int tvk_row_softmax(double* a, int64_t rows, int cols, double* norm, void* stream);
 int tvk_ddot(const double* x, const double* y, int64_t n, double alpha, double beta, double* out, double* workspace,
              void* stream);
 
@@ -193,6 +199,22 @@ int tvk_spd_solve_rows(const double* apk, const double* b, int batch, int D, int
  * reports an applied floor; TVK_ITEM_NOT_SPD reports a non-positive floor (collapse). */
 int tvk_sigma_floor(const double* ssum, const double* tb, const double* N, const double* sigma_old, int C, int F,
                     double floor_scale, double* sigma_out, int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------- UBM EM training */
+
+/* k-means++ seeding distances (_seed_means, gmm.py:228-243): d_t = sum_i (x_ti - center_i)^2 summed
+ * in numpy's pairwise order (bit-identical to np.sum(..., axis=1)); dist2[t] = d_t when init, else
+ * min(dist2[t], d_t).  F <= 128. */
+int tvk_seed_dist2(const void* x, int x_f64, int64_t T, int F, const double* center, double* dist2, int init,
+                   void* stream);
+
+/* Full-covariance M-step moments (train_gmm_full, gmm.py:350-366).  stats is C x Q, Q = 1+F+F(F+1)/2,
+ * row c = sum_t r_tc [1, x_i, x_i x_j (i<=j)] (responsibilities^T x tvk_frame_features kind 1).
+ * Writes mean_c = s1/occ (mean_old_c when starved), s2_c (full F x F), tb_c = s1 s1^T / occ, n_out[c] = occ (0 when
+ * occ < occ_min: starved, tvk_sigma_floor keeps the old covariance) and trace[c] =
+ * tr(s2_c - tb_c)/occ (NaN when starved), ready for tvk_sigma_floor(s2, tb, n_out, ...). */
+int tvk_full_moments(const double* stats, int C, int F, double occ_min, const double* mean_old, double* mean,
+                     double* s2, double* tb, double* n_out, double* trace, void* stream);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,8 @@ from .gmm import (
     accumulate_bw_stats,
     align_frames,
     select_top_k,
+    train_gmm_diag,
+    train_gmm_full,
 )
 from .tvm import (
     AUGMENTED,

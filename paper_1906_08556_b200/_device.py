@@ -283,3 +283,111 @@ def bw_stats(x, utt_frames, ali_offsets, comps, wts, C, center=None, want_S=Fals
     call("tvk_bw_stats", xp, xf, F, ptr(utt_frames), U, ptr(ali_offsets), ptr(comps), ptr(wts), C, ptr(center),
          ptr(n), ptr(f), ptr(S), ptr(ssum_acc), int(entry_capacity), ptr(ws), ws_bytes, stream())
     return n, f, S
+
+
+# ---------------------------------------------------------------------------- UBM EM training
+
+EM_CHUNK_ELEMS = 1 << 27  # doubles in each per-chunk T x max(C, Q) buffer (1 GiB)
+
+
+def seed_means(x, frames, n_components, rng):
+    """k-means++-style seeding (_seed_means, gmm.py:228-243).
+
+    The O(T F) distance update per seeded mean runs on device (``tvk_seed_dist2``, numpy's
+    summation order, so the distances are bit-identical); the O(T) draw ``rng.choice`` stays
+    with the caller's numpy Generator so the selected frames are exactly the reference's.
+    """
+    T, F = x.shape
+    chosen = np.empty((n_components, F))
+    chosen[0] = frames[rng.integers(T)]
+    if n_components == 1:
+        return chosen
+    xp, xf = _lib.x_args(x)
+    center = _lib.empty((F,))
+    dist2 = _lib.empty((T,))
+    host = torch.empty((T,), dtype=torch.float64, pin_memory=True)
+    center.copy_(torch.from_numpy(chosen[0]))
+    call("tvk_seed_dist2", xp, xf, T, F, ptr(center), ptr(dist2), 1, stream())
+    for c in range(1, n_components):
+        host.copy_(dist2)
+        d = host.numpy()
+        total = d.sum()
+        if total <= 0:
+            chosen[c] = frames[rng.integers(T)]
+            continue
+        idx = rng.choice(T, p=d / total)
+        chosen[c] = frames[idx]
+        center.copy_(torch.from_numpy(chosen[c]))
+        call("tvk_seed_dist2", xp, xf, T, F, ptr(center), ptr(dist2), 0, stream())
+    return chosen
+
+
+class EmEStep:
+    """GMM E-step over a device frame matrix (gmm.py:283-292 diagonal, 344-349 full).
+
+    Per chunk of frames: features (kind 0 ``[x^2, x, 1]``, kind 1 ``[1, x_i, x_i x_j]``) ->
+    log-likelihoods as one DMMA GEMM against the model's coefficient table -> row softmax
+    (responsibilities in place, log-normalisers out) -> one ``resp^T x features`` GEMM that
+    accumulates every sufficient statistic at once (C x Q: occupancy, first and second
+    moments).  The total log-likelihood is a fixed-order device reduction of the normalisers.
+    """
+
+    def __init__(self, x, kind, C):
+        self.x = x
+        self.T, self.F = x.shape
+        F = self.F
+        self.kind, self.C = kind, C
+        self.q = 2 * F + 1 if kind == 0 else 1 + F + F * (F + 1) // 2
+        self.rows = int(max(256, min(self.T, EM_CHUNK_ELEMS // max(C, self.q))))
+        self.feats = _lib.empty((self.rows, self.q))
+        self.ll = _lib.empty((self.rows, C))
+        self.norm = _lib.empty((self.rows,))
+        self.stats = _lib.empty((C, self.q))
+        self.total = _lib.empty((1,))
+        self.dot_ws = _lib.empty((max(int(_lib.load().tvk_ddot_workspace_bytes()) // 8, 1),))
+        tiles = -(-C // 128) * -(-self.q // 128)
+        self.splits = int(max(1, min(32, (2 * 148) // tiles, self.rows // 1024)))
+        self.work = _lib.empty((self.splits * C * self.q,)) if self.splits > 1 else None
+
+    def run(self, table):
+        """Accumulate the statistics for the model whose table is ``table``; returns (stats, total)."""
+        T, F, C, q = self.T, self.F, self.C, self.q
+        for lo in range(0, T, self.rows):
+            n = min(self.rows, T - lo)
+            xp, xf = _lib.x_args(self.x[lo:lo + n])
+            feats, ll = self.feats[:n], self.ll[:n]
+            call("tvk_frame_features", xp, xf, n, F, self.kind, ptr(feats), stream())
+            _lib.dgemm(feats, table, ll, n, C, q)
+            call("tvk_row_softmax", ptr(ll), n, C, ptr(self.norm), stream())
+            beta = 0.0 if lo == 0 else 1.0
+            call("tvk_ddot", ptr(self.norm), None, n, 1.0, beta, ptr(self.total), ptr(self.dot_ws), stream())
+            splits = self.splits if n >= 1024 * self.splits else 1
+            _lib.dgemm(ll, feats, self.stats, C, q, n, trans_a=True, beta=beta, splits=splits,
+                       work=self.work if splits > 1 else None)
+        return self.stats, self.total
+
+
+def full_moments(stats, mean_old, C, F, occ_min=1.0):
+    """(mean, S2, s1 s1^T/occ, N (0 when starved), trace) from a kind-1 statistics matrix."""
+    mean = _lib.empty((C, F))
+    s2 = _lib.empty((C, F, F))
+    tb = _lib.empty((C, F, F))
+    n = _lib.empty((C,))
+    tr = _lib.empty((C,))
+    call("tvk_full_moments", ptr(stats), C, F, float(occ_min), ptr(mean_old), ptr(mean), ptr(s2), ptr(tb), ptr(n),
+         ptr(tr), stream())
+    return mean, s2, tb, n, tr
+
+
+def sigma_floor(s2, tb, n, sigma_old, C, F, floor_scale):
+    out = _lib.empty((C, F, F))
+    status = _lib.empty((C,), torch.int32)
+    call("tvk_sigma_floor", ptr(s2), ptr(tb), ptr(n), ptr(sigma_old), C, F, float(floor_scale), ptr(out),
+         ptr(status), stream())
+    return out, status
+
+
+def spd_status(a, C, F):
+    status = _lib.empty((C,), torch.int32)
+    call("tvk_spd_small", ptr(a), C, F, None, None, None, ptr(status), stream())
+    return status

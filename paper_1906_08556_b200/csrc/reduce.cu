@@ -55,6 +55,25 @@ __global__ void dot_final_kernel(const double* partial, double alpha, double bet
   if (threadIdx.x == 0) out[0] = (beta != 0.0 ? beta * out[0] : 0.0) + alpha * red[0];
 }
 
+// One warp per row: norm[r] = log sum_j exp(a[r, j]) (max-shifted), a[r, j] <- exp(a[r, j] - norm[r]).
+// The GMM E-step responsibilities (gmm.py:284-287, 345-348).  Fixed order per row.
+__global__ void row_softmax_kernel(double* a, int64_t rows, int cols, double* norm) {
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  double* row = a + r * cols;
+  double mx = -INFINITY;
+  for (int j = lane; j < cols; j += 32) mx = fmax(mx, row[j]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const double sh = isfinite(mx) ? mx : 0.0;  // scipy logsumexp convention
+  double s = 0.0;
+  for (int j = lane; j < cols; j += 32) s += exp(row[j] - sh);
+  s = warp_sum(s);
+  const double lse = log(s) + sh;
+  for (int j = lane; j < cols; j += 32) row[j] = exp(row[j] - lse);
+  if (lane == 0) norm[r] = lse;
+}
+
 }  // namespace tvk
 
 extern "C" int tvk_colsum(const double* a, int64_t rows, int64_t cols, int64_t lda, double alpha, double beta,
@@ -76,5 +95,14 @@ extern "C" int tvk_ddot(const double* x, const double* y, int64_t n, double alph
   tvk::dot_partial_kernel<<<tvk::kDotBlocks, tvk::kDotThreads, 0, st>>>(x, y, n, workspace);
   tvk::dot_final_kernel<<<1, tvk::kDotThreads, 0, st>>>(workspace, alpha, beta, out);
   TVK_CHECK_LAUNCH("ddot");
+  return TVK_OK;
+}
+
+extern "C" int tvk_row_softmax(double* a, int64_t rows, int cols, double* norm, void* stream) {
+  TVK_REQUIRE(rows >= 0 && cols >= 1, "row_softmax: bad shape");
+  if (rows == 0) return TVK_OK;
+  const int64_t blocks = (rows * 32 + 255) / 256;
+  tvk::row_softmax_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a, rows, cols, norm);
+  TVK_CHECK_LAUNCH("row_softmax");
   return TVK_OK;
 }

@@ -46,6 +46,37 @@ CONFIG1 = dict(n_comp=64, dim=20, rank=100, speakers=50, upc=4, frames=(300, 300
                within=0.3, iterations=5)
 
 
+UBM_CASES = [
+    # name, frame seed, frames per cluster, dim, clusters, spread, C, diag iters, full iters, diag seed
+    ("ubm_c4f3", 70, 400, 3, 4, 6.0, 4, 8, 5, 0),
+    ("ubm_c16f8", 71, 300, 8, 6, 4.0, 16, 6, 4, 3),
+]
+
+
+def ubm_frames(case):
+    """Gaussian clusters around seeded centres (UBM training inputs)."""
+    _, fs, per, f, k, spread = case[:6]
+    rng = np.random.default_rng(fs)
+    centres = rng.normal(0.0, spread, (k, f))
+    x = np.concatenate([c + rng.normal(0.0, 1.0, (per, f)) for c in centres])
+    return x[rng.permutation(x.shape[0])]
+
+
+# Outlier-laden inputs (name, seed): starved components (re-seeded in the diagonal EM, frozen in
+# the full EM) and a single-frame component whose covariance collapses (NumericError).
+UBM_EDGE_CASES = [("ubm_starve7", 7), ("ubm_starve21", 21), ("ubm_collapse0", 0)]
+UBM_EDGE_ITERS = (8, 5)
+
+
+def ubm_edge_frames(seed):
+    """(frames, C): a unit cluster of 10*C frames plus 1-5 scattered outliers."""
+    rng = np.random.default_rng(seed)
+    F, C = 2, int(rng.integers(6, 14))
+    nout = int(rng.integers(1, 6))
+    x = np.concatenate([rng.normal(0, 1, (10 * C, F)), rng.normal(0, 1, (nout, F)) * rng.uniform(5, 40)])
+    return x[rng.permutation(len(x))], C
+
+
 def digest(*arrays):
     h = hashlib.sha256()
     for a in arrays:

@@ -14,6 +14,7 @@ tests rebuild them on any box and check the checksum first.
 from __future__ import annotations
 
 import os
+import warnings
 import sys
 
 import numpy as np
@@ -28,7 +29,8 @@ from tvkit import gmm as rgmm, pipeline as rpipe, synth as rsynth, tvm as rtvm  
 
 from oracle import tvkit_oracle as orc  # noqa: E402
 sys.path.insert(0, HERE)
-from cases import ALIGN_CASES, TRAIN_CASES, TVM_CASES, digest  # noqa: E402
+from cases import (ALIGN_CASES, TRAIN_CASES, TVM_CASES, UBM_CASES, UBM_EDGE_CASES, UBM_EDGE_ITERS,  # noqa: E402
+                   digest, ubm_edge_frames, ubm_frames)
 
 
 def save(name, **arrays):
@@ -183,7 +185,44 @@ def make_config1():
          aux=np.array([r.aux for r in metrics.records]), ivectors=emb)
 
 
+def make_ubm():
+    """Reference UBM EM training (gmm.py:246-373) on seeded cluster data."""
+    out = {}
+    for case in UBM_CASES:
+        name, c, di, fi, seed = case[0], case[6], case[7], case[8], case[9]
+        x = ubm_frames(case)
+        diag = rgmm.train_gmm_diag(x, c, n_iters=di, seed=seed)
+        full = rgmm.train_gmm_full(x, diag, n_iters=fi)
+        od = orc.train_gmm_diag(x, c, n_iters=di, seed=seed)
+        of = orc.train_gmm_full(x, od.weights, od.means, od.variances, n_iters=fi)
+        assert np.allclose(od.means, diag.means, rtol=1e-10, atol=1e-10), name
+        assert np.allclose(of.covariances, full.covariances, rtol=1e-10, atol=1e-10), name
+        out[f"{name}__x_digest"] = np.array([digest(x)])
+        out[f"{name}__diag_w"], out[f"{name}__diag_mu"], out[f"{name}__diag_var"] = diag.weights, diag.means, diag.variances
+        out[f"{name}__diag_ll"] = np.array(diag.training_loglik)
+        out[f"{name}__full_w"], out[f"{name}__full_mu"], out[f"{name}__full_cov"] = full.weights, full.means, full.covariances
+        out[f"{name}__full_ll"] = np.array(full.training_loglik)
+    di, fi = UBM_EDGE_ITERS
+    for name, seed in UBM_EDGE_CASES:
+        x, c = ubm_edge_frames(seed)
+        out[f"{name}__x_digest"] = np.array([digest(x)])
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            diag = rgmm.train_gmm_diag(x, c, n_iters=di, seed=seed)
+            nd = len(w)
+            out[f"{name}__diag_w"], out[f"{name}__diag_mu"] = diag.weights, diag.means
+            out[f"{name}__diag_var"], out[f"{name}__diag_ll"] = diag.variances, np.array(diag.training_loglik)
+            try:
+                full = rgmm.train_gmm_full(x, diag, n_iters=fi)
+                out[f"{name}__full_w"], out[f"{name}__full_mu"] = full.weights, full.means
+                out[f"{name}__full_cov"], out[f"{name}__full_ll"] = full.covariances, np.array(full.training_loglik)
+            except Exception as exc:  # the reference's own error is the golden output
+                out[f"{name}__error"] = np.array([f"{type(exc).__name__}: {exc}"])
+        out[f"{name}__warnings"] = np.array([nd, len(w) - nd])
+    save("ubm", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["align", "tvm", "train", "config1"]
+    which = sys.argv[1:] or ["align", "tvm", "train", "config1", "ubm"]
     for w in which:
         globals()[f"make_{w}"]()

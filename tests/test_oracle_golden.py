@@ -115,3 +115,49 @@ def test_householder_and_min_div_properties():
         np.testing.assert_allclose(p2 @ p2, np.eye(d), atol=1e-10)
         np.testing.assert_allclose((p2 @ v)[1:], 0.0, atol=1e-10 * max(1, np.linalg.norm(v)))
     np.testing.assert_array_equal(orc.householder(np.array([2.5, 0.0, 0.0])), np.eye(3))
+
+
+UBM = cases.load("ubm")
+
+
+@pytest.mark.parametrize("case", cases.UBM_CASES, ids=[c[0] for c in cases.UBM_CASES])
+def test_ubm_training_matches_reference(case):
+    """Oracle UBM EM (gmm.py:246-373) against the reference's own run."""
+    name, c, di, fi, seed = case[0], case[6], case[7], case[8], case[9]
+    x = cases.ubm_frames(case)
+    assert UBM[name]["x_digest"][0] == cases.digest(x)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        d = orc.train_gmm_diag(x, c, n_iters=di, seed=seed)
+        f = orc.train_gmm_full(x, d.weights, d.means, d.variances, n_iters=fi)
+    np.testing.assert_allclose(d.weights, UBM[name]["diag_w"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(d.means, UBM[name]["diag_mu"], rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(d.variances, UBM[name]["diag_var"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(d.training_loglik, UBM[name]["diag_ll"], rtol=1e-12)
+    np.testing.assert_allclose(f.weights, UBM[name]["full_w"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(f.means, UBM[name]["full_mu"], rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(f.covariances, UBM[name]["full_cov"], rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(f.training_loglik, UBM[name]["full_ll"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("name,seed", cases.UBM_EDGE_CASES, ids=[c[0] for c in cases.UBM_EDGE_CASES])
+def test_ubm_edge_cases_match_reference(name, seed):
+    """Starved components and collapsed covariances: warnings, re-seeding and errors as the reference."""
+    g = UBM[name]
+    x, c = cases.ubm_edge_frames(seed)
+    assert g["x_digest"][0] == cases.digest(x)
+    di, fi = cases.UBM_EDGE_ITERS
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        d = orc.train_gmm_diag(x, c, n_iters=di, seed=seed)
+        nd = len(w)
+        np.testing.assert_allclose(d.means, g["diag_mu"], rtol=1e-10, atol=1e-10)
+        np.testing.assert_allclose(d.variances, g["diag_var"], rtol=1e-10, atol=1e-12)
+        if "error" in g:
+            with pytest.raises(orc.OracleNumericError) as exc:
+                orc.train_gmm_full(x, d.weights, d.means, d.variances, n_iters=fi)
+            assert str(exc.value) in str(g["error"][0])
+        else:
+            f = orc.train_gmm_full(x, d.weights, d.means, d.variances, n_iters=fi)
+            np.testing.assert_allclose(f.covariances, g["full_cov"], rtol=1e-9, atol=1e-10)
+    assert [nd, len(w) - nd] == list(g["warnings"])
