@@ -23,6 +23,7 @@
  *   tvk_sigma_floor         update_sigma + floor_eigenvalues   tvm.py:337-358, _linalg.py:15-24
  *   tvk_row_softmax         UBM EM responsibilities            gmm.py:284-287, 345-348
  *   tvk_seed_dist2          _seed_means distance update        gmm.py:228-243
+ *   tvk_seed_means          _seed_means draw loop              gmm.py:228-243
  *   tvk_full_moments        train_gmm_full M-step moments      gmm.py:350-366
  */
 #ifndef TVK_H_
@@ -207,6 +208,17 @@ int tvk_sigma_floor(const double* ssum, const double* tb, const double* N, const
  * min(dist2[t], d_t).  F <= 128. */
 int tvk_seed_dist2(const void* x, int x_f64, int64_t T, int F, const double* center, double* dist2, int init,
                    void* stream);
+
+/* Whole k-means++ seeding loop on the device (_seed_means, gmm.py:228-243), no host round trips.
+ * idx[0] (set by the caller) is the first seeded frame; u[0..C-2] are the caller's rng.random()
+ * draws, one per rng.choice.  Step c folds the distance to frame idx[c-1] into dist2 (as
+ * tvk_seed_dist2) and sets idx[c] = first frame whose dist2 prefix sum exceeds u[c-1] * sum(dist2)
+ * (rng.choice's inverse-CDF draw).  If the total at step c is <= 0 or non-finite the loop stops:
+ * stop[0] = c, stop[1] = 1 (total <= 0) or 2 (non-finite); dist2 then holds the distances the host
+ * needs to continue.  Workspace: tvk_seed_workspace_bytes(T).  F <= 128. */
+int64_t tvk_seed_workspace_bytes(int64_t T);
+int tvk_seed_means(const void* x, int x_f64, int64_t T, int F, int C, const double* u, int64_t* idx, double* dist2,
+                   int32_t* stop, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Full-covariance M-step moments (train_gmm_full, gmm.py:350-366).  stats is C x Q, Q = 1+F+F(F+1)/2,
  * row c = sum_t r_tc [1, x_i, x_i x_j (i<=j)] (responsibilities^T x tvk_frame_features kind 1).

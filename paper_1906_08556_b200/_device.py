@@ -293,33 +293,59 @@ EM_CHUNK_ELEMS = 1 << 27  # doubles in each per-chunk T x max(C, Q) buffer (1 Gi
 def seed_means(x, frames, n_components, rng):
     """k-means++-style seeding (_seed_means, gmm.py:228-243).
 
-    The O(T F) distance update per seeded mean runs on device (``tvk_seed_dist2``, numpy's
-    summation order, so the distances are bit-identical); the O(T) draw ``rng.choice`` stays
-    with the caller's numpy Generator so the selected frames are exactly the reference's.
+    The whole draw loop runs on the device (``tvk_seed_means``): distance updates bit-identical
+    to numpy, inverse-CDF draws against uniforms taken from the caller's Generator up front (one
+    ``rng.random()`` per ``rng.choice``, exactly what the reference consumes).  If the device
+    stops early (all distances zero -> the reference's ``rng.integers`` branch, or non-finite
+    distances -> ``rng.choice``'s ValueError) the random stream is rewound and the remaining
+    draws follow the reference step by step on the host.
     """
     T, F = x.shape
-    chosen = np.empty((n_components, F))
-    chosen[0] = frames[rng.integers(T)]
-    if n_components == 1:
+    C = n_components
+    chosen = np.empty((C, F))
+    first = int(rng.integers(T))
+    chosen[0] = frames[first]
+    if C == 1:
         return chosen
+    state = rng.bit_generator.state
+    u = _lib.to_dev(rng.random(C - 1))
+    idx = _lib.empty((C,), torch.int64)
+    idx[:1].fill_(first)
+    dist2 = _lib.empty((T,))
+    stop = _lib.empty((2,), torch.int32)
+    ws_bytes = int(_lib.load().tvk_seed_workspace_bytes(T))
+    ws = _lib.empty((ws_bytes // 8,))
+    xp, xf = _lib.x_args(x)
+    call("tvk_seed_means", xp, xf, T, F, C, ptr(u), ptr(idx), ptr(dist2), ptr(stop), ptr(ws), ws_bytes, stream())
+    idx_h, stop_h = _lib.to_host(idx), _lib.to_host(stop)
+    s = int(stop_h[0])
+    if s == 0:
+        chosen[1:] = frames[idx_h[1:]]
+        return chosen
+    chosen[1:s] = frames[idx_h[1:s]]
+    rng.bit_generator.state = state
+    if s > 1:
+        rng.random(s - 1)
+    _seed_host_steps(x, frames, chosen, dist2, s, rng)
+    return chosen
+
+
+def _seed_host_steps(x, frames, chosen, dist2, start, rng):
+    """Steps ``start..C-1`` of _seed_means with the draws on the host (gmm.py:235-242)."""
+    T, F = x.shape
     xp, xf = _lib.x_args(x)
     center = _lib.empty((F,))
-    dist2 = _lib.empty((T,))
     host = torch.empty((T,), dtype=torch.float64, pin_memory=True)
-    center.copy_(torch.from_numpy(chosen[0]))
-    call("tvk_seed_dist2", xp, xf, T, F, ptr(center), ptr(dist2), 1, stream())
-    for c in range(1, n_components):
+    for c in range(start, chosen.shape[0]):
         host.copy_(dist2)
         d = host.numpy()
         total = d.sum()
         if total <= 0:
             chosen[c] = frames[rng.integers(T)]
             continue
-        idx = rng.choice(T, p=d / total)
-        chosen[c] = frames[idx]
+        chosen[c] = frames[rng.choice(T, p=d / total)]
         center.copy_(torch.from_numpy(chosen[c]))
         call("tvk_seed_dist2", xp, xf, T, F, ptr(center), ptr(dist2), 0, stream())
-    return chosen
 
 
 class EmEStep:

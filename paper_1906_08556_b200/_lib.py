@@ -45,6 +45,8 @@ SIGNATURES = {
     "tvk_diag_table_bytes": (_i64, [_i, _i]),
     "tvk_row_softmax": (_i, [_p, _i64, _i, _p, _p]),
     "tvk_seed_dist2": (_i, [_p, _i, _i64, _i, _p, _p, _i, _p]),
+    "tvk_seed_workspace_bytes": (_i64, [_i64]),
+    "tvk_seed_means": (_i, [_p, _i, _i64, _i, _i, _p, _p, _p, _p, _p, _i64, _p]),
     "tvk_full_moments": (_i, [_p, _i, _i, _d, _p, _p, _p, _p, _p, _p, _p]),
     "tvk_full_table": (_i, [_p, _p, _p, _i, _i, _p, _p, _p]),
     "tvk_precision_table": (_i, [_p, _p, _p, _i, _i, _p, _p, _p]),

@@ -57,6 +57,115 @@ __global__ void seed_dist2_kernel(const XT* __restrict__ x, int64_t T, int F, co
   }
 }
 
+// ---------------------------------------------------------------- device-resident seeding loop
+//
+// All C-1 draws of _seed_means run on the device without a host round trip.  The caller draws the
+// C-1 uniforms u_c up front (rng.choice(T, p) consumes exactly one rng.random() per call), so the
+// random stream is the reference's.  Step c: (1) fold the distance to mean c-1 (frame idx[c-1]) into
+// dist2 (bit-identical to numpy) and write per-block partial sums in a fixed order; (2) one warp
+// finds the first frame whose prefix sum of dist2 exceeds u_c * total -- numpy's
+// cdf.searchsorted(u, 'right') over cumsum(dist2 / total) / cdf[-1] up to the rounding of the
+// prefix sums, i.e. the same frame unless u_c lands within a few ulps of a CDF step.
+// A non-positive total (every frame coincides with a chosen mean; the reference then draws with
+// rng.integers) or a non-finite one (rng.choice raises) stops the loop and is reported to the
+// host, which replays the random stream and finishes the remaining draws itself.
+
+constexpr int kSeedThreads = 256;
+
+template <typename XT>
+__global__ void __launch_bounds__(kSeedThreads)
+    seed_step_kernel(const XT* __restrict__ x, int64_t T, int F, int64_t per, const int64_t* __restrict__ idx, int c,
+                     double* __restrict__ dist2, double* __restrict__ bsum, const int32_t* __restrict__ stop) {
+  if (stop[0]) return;
+  __shared__ double cen[kSeedMaxF];
+  __shared__ double red[kSeedThreads / 32];
+  const XT* crow = x + idx[c - 1] * F;
+  for (int i = threadIdx.x; i < F; i += blockDim.x) cen[i] = (double)crow[i];
+  __syncthreads();
+  const int64_t lo = blockIdx.x * per, hi = min(T, lo + per);
+  double acc = 0.0;
+  for (int64_t t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+    double s = np_pairwise_sq(x + t * F, cen, F);
+    double v = c == 1 ? s : fmin(dist2[t], s);
+    dist2[t] = v;
+    acc += v;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < kSeedThreads / 32; w++) b += red[w];
+    bsum[blockIdx.x] = b;
+  }
+}
+
+// Walk v[0..n) from running sum `acc`; first j with acc + v[j] > thr (else the last j with v[j] > 0).
+__device__ __forceinline__ int64_t seed_walk(const double* v, int64_t n, double& acc, double thr) {
+  int64_t last = -1;
+  for (int64_t j = 0; j < n; j++) {
+    double nxt = acc + v[j];
+    if (v[j] > 0.0) last = j;
+    if (nxt > thr && v[j] > 0.0) return j;
+    acc = nxt;
+  }
+  return last;
+}
+
+// One warp: lane chunks of the block sums -> crossing block -> lane chunks of that block's
+// frames -> crossing frame.
+__global__ void seed_draw_kernel(const double* __restrict__ dist2, int64_t T, int64_t per, const double* __restrict__ bsum,
+                                 int nb, const double* __restrict__ u, int c, int64_t* __restrict__ idx,
+                                 int32_t* __restrict__ stop) {
+  if (stop[0]) return;
+  const int lane = threadIdx.x;
+  // level 1: block sums
+  int64_t cb = (nb + 31) / 32, b0 = min((int64_t)nb, lane * cb), b1 = min((int64_t)nb, b0 + cb);
+  double ls = 0.0;
+  for (int64_t b = b0; b < b1; b++) ls += bsum[b];
+  double inc = ls;
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const double total = __shfl_sync(0xffffffffu, inc, 31);
+  if (!(total > 0.0) || !isfinite(total)) {
+    if (lane == 0) {
+      stop[0] = c;
+      stop[1] = isfinite(total) ? 1 : 2;
+    }
+    return;
+  }
+  const double thr = u[c - 1] * total;
+  unsigned hit = __ballot_sync(0xffffffffu, inc > thr && ls > 0.0);
+  int l = hit ? __ffs(hit) - 1 : 31 - __clz(__ballot_sync(0xffffffffu, ls > 0.0));
+  double acc = __shfl_sync(0xffffffffu, inc - ls, l);
+  int64_t blk = 0;
+  if (lane == l) {
+    int64_t lb0 = min((int64_t)nb, l * cb), lb1 = min((int64_t)nb, lb0 + cb);
+    blk = lb0 + seed_walk(bsum + lb0, lb1 - lb0, acc, thr);
+  }
+  blk = __shfl_sync(0xffffffffu, blk, l);
+  acc = __shfl_sync(0xffffffffu, acc, l);
+  // level 2: frames of the crossing block; acc = sum of all earlier blocks
+  const int64_t f0 = blk * per, f1 = min(T, f0 + per);
+  int64_t cf = (f1 - f0 + 31) / 32, e0 = min(f1, f0 + lane * cf), e1 = min(f1, e0 + cf);
+  double fs = 0.0;
+  for (int64_t t = e0; t < e1; t++) fs += dist2[t];
+  double finc = fs;
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(0xffffffffu, finc, o);
+    if (lane >= o) finc += y;
+  }
+  hit = __ballot_sync(0xffffffffu, acc + finc > thr && fs > 0.0);
+  l = hit ? __ffs(hit) - 1 : 31 - __clz(__ballot_sync(0xffffffffu, fs > 0.0));
+  if (lane == l) {
+    double a2 = acc + (finc - fs);
+    int64_t le0 = min(f1, f0 + l * cf), le1 = min(f1, le0 + cf);
+    idx[c] = le0 + seed_walk(dist2 + le0, le1 - le0, a2, thr);
+  }
+}
+
 // One CTA per component.  stats row c: [occ, s1 (F), s2 packed upper (F(F+1)/2)].
 __global__ void full_moments_kernel(const double* __restrict__ stats, int F, double occ_min,
                                     const double* __restrict__ mean_old, double* __restrict__ mean,
@@ -114,5 +223,34 @@ extern "C" int tvk_full_moments(const double* stats, int C, int F, double occ_mi
   tvk::full_moments_kernel<<<C, 256, 0, (cudaStream_t)stream>>>(stats, F, occ_min, mean_old, mean, s2, tb, n_out,
                                                                  trace);
   TVK_CHECK_LAUNCH("full_moments");
+  return TVK_OK;
+}
+
+extern "C" int64_t tvk_seed_workspace_bytes(int64_t T) {
+  int64_t nb = (T + tvk::kSeedThreads - 1) / tvk::kSeedThreads;
+  if (nb > 148 * 8) nb = 148 * 8;
+  return (nb < 1 ? 1 : nb) * (int64_t)sizeof(double);
+}
+
+extern "C" int tvk_seed_means(const void* x, int x_f64, int64_t T, int F, int C, const double* u, int64_t* idx,
+                              double* dist2, int32_t* stop, void* workspace, int64_t workspace_bytes, void* stream) {
+  TVK_REQUIRE(T >= 1 && F >= 1 && F <= tvk::kSeedMaxF && C >= 1, "seed_means: bad shape (F must be <= 128)");
+  TVK_REQUIRE(workspace_bytes >= tvk_seed_workspace_bytes(T), "seed_means: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nb = tvk_seed_workspace_bytes(T) / (int64_t)sizeof(double);
+  int64_t per = (T + nb - 1) / nb;
+  nb = (T + per - 1) / per;
+  double* bsum = (double*)workspace;
+  cudaMemsetAsync(stop, 0, 2 * sizeof(int32_t), st);
+  for (int c = 1; c < C; c++) {
+    if (x_f64)
+      tvk::seed_step_kernel<double><<<(unsigned)nb, tvk::kSeedThreads, 0, st>>>((const double*)x, T, F, per, idx, c,
+                                                                                 dist2, bsum, stop);
+    else
+      tvk::seed_step_kernel<float><<<(unsigned)nb, tvk::kSeedThreads, 0, st>>>((const float*)x, T, F, per, idx, c,
+                                                                                dist2, bsum, stop);
+    tvk::seed_draw_kernel<<<1, 32, 0, st>>>(dist2, T, per, bsum, (int)nb, u, c, idx, stop);
+  }
+  TVK_CHECK_LAUNCH("seed_means");
   return TVK_OK;
 }

@@ -98,6 +98,13 @@ def test_seeding_is_bit_exact(gpu, T, F, C):
     ours = _device.seed_means(_lib.to_dev(x), x, C, np.random.default_rng(9))
     ref = orc.seed_means(x, C, np.random.default_rng(9))
     np.testing.assert_array_equal(ours, ref)
+    # the host-draw fallback steps agree too (dist2 after the first device step)
+    rng = np.random.default_rng(9)
+    chosen = np.empty((C, F))
+    chosen[0] = x[rng.integers(T)]
+    dist2 = _lib.to_dev(np.sum((x - chosen[0]) ** 2, axis=1))
+    _device._seed_host_steps(_lib.to_dev(x), x, chosen, dist2, 1, rng)
+    np.testing.assert_array_equal(chosen, ref)
 
 
 @pytest.mark.parametrize("chunk", [None, 1 << 14])
@@ -124,3 +131,26 @@ def test_larger_training_matches_oracle(gpu, chunk, monkeypatch):
     # EM never decreases the likelihood
     assert np.all(np.diff(d.training_loglik) > -1e-6 * abs(d.training_loglik[0]))
     assert np.all(np.diff(f.training_loglik) > -1e-6 * abs(f.training_loglik[0]))
+
+
+def test_seeding_degenerate_inputs(gpu):
+    """All distances zero mid-loop (the reference's rng.integers branch) and NaN frames
+    (rng.choice's ValueError): the device loop stops and the host finishes like the reference."""
+    from paper_1906_08556_b200 import _device, _lib
+    pts = np.array([[0.0, 1.0], [3.0, -2.0], [5.0, 5.0]])
+    x = np.repeat(pts, 20, axis=0)[np.random.default_rng(0).permutation(60)]
+    for C in (3, 4, 6):
+        ours = _device.seed_means(_lib.to_dev(x), x, C, np.random.default_rng(4))
+        ref = orc.seed_means(x, C, np.random.default_rng(4))
+        np.testing.assert_array_equal(ours, ref)
+    # the random stream after seeding is where the reference leaves it
+    r1, r2 = np.random.default_rng(4), np.random.default_rng(4)
+    _device.seed_means(_lib.to_dev(x), x, 6, r1)
+    orc.seed_means(x, 6, r2)
+    assert r1.random() == r2.random()
+    xn = x.copy()
+    xn[7, 1] = np.nan
+    with pytest.raises(ValueError, match="Probabilities contain NaN"):
+        orc.seed_means(xn, 4, np.random.default_rng(1))
+    with pytest.raises(ValueError, match="Probabilities contain NaN"):
+        _device.seed_means(_lib.to_dev(xn), xn, 4, np.random.default_rng(1))
