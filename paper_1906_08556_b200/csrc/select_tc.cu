@@ -11,9 +11,10 @@
 //    scores of its frame out of TMEM (tcgen05.ld 32x32b): a value-only top-K list gives the running
 //    K-th largest s~_(K); every score >= s~_(K) - 2m is appended to a per-thread smem buffer.  Any
 //    component below that window is strictly below K others in exact arithmetic.
-// 3. Exact order.  The window is sorted by s~; runs whose consecutive gaps are <= 2m ("clusters")
-//    are rescored in FP64 from the exact table and re-sorted by (exact value desc, index asc) — the
-//    stable-argsort rule of the reference.  Pairs further apart than 2m are ordered by s~ already.
+// 3. Exact order (select_post_kernel, one warp per frame, off the tensor-core pipeline).  The window
+//    is sorted by s~; runs whose consecutive gaps are <= 2m ("clusters") are rescored in FP64 from
+//    the exact table and re-sorted by (exact value desc, index asc) — the stable-argsort rule of the
+//    reference.  Pairs further apart than 2m are ordered by s~ already.
 // Frames whose window overflows the buffer, has fewer than K finite entries, or holds non-finite
 // values are flagged (sel[t*K] = -1) and recomputed by select_exact_kernel in plain FP64.
 //
@@ -21,7 +22,8 @@
 //   warp 0 lane 0: bulk-copy (TMA) producer streaming the pre-split W blob through a 4-stage ring;
 //   warp 1 lane 0: tcgen05.mma issuer (M=128 frames, N=128 components, K=8 per instruction);
 //   warp 2: TMEM allocator (512 columns = 4 accumulator buffers of 128 components);
-//   warps 4-7: epilogue (A-operand producer, candidate window, exact clusters, output).
+//   warps 4-11: epilogue (A-operand producer, pass-0 bound, pass-1 candidate collection); the
+//   candidate runs go to global scratch so the tensor-core pipeline never waits for step 3.
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -40,16 +42,15 @@ constexpr int NC = 128;        // components per chunk = MMA N
 // TMEM columns: [0,128) acc 0 | [128,256) acc 1 | [256,384) A buffer 0 | [384,512) A buffer 1, each A
 // buffer = 64 columns of hi words then 64 of lo words; the next tile's A is built during this tile
 // (A: two f16 per 32-bit column)
-constexpr int RING = 98304;    // B ring bytes: NST stages of STAGE bytes (runtime split, see Pipe)
+constexpr int RING = 131072;   // B ring bytes: NST stages of STAGE bytes (runtime split, see Pipe)
 constexpr int XS = 64;         // smem row stride (floats) of the staged frame tile, >= F + 1
-constexpr int MAXST = 12;
+constexpr int MAXST = 16;
 constexpr int CL = 2;          // CTAs per cluster sharing every B stage by TMA multicast
 constexpr int KSTEP = 8192;    // blob bytes per k16-step: 128 comps x 16 k x (hi, lo) x 2 B
 constexpr int H = 2;           // epilogue warps per TMEM lane quarter (each takes half of a chunk's columns)
 constexpr int NEPI = 128 * H;  // epilogue threads
 constexpr int NT = 128 + NEPI;
 constexpr int CAP = 24;        // candidate buffer entries per (frame, half)
-constexpr int WMAX = 24;       // merged window entries per frame
 constexpr float KAPPA = 1.0f / 65536.0f;  // 3xTF32 bound: 28x the max observed error
 constexpr float KAPPA1 = 1.0f / 4096.0f;   // pass-0 slack (heuristic: the window check below is exact)
 constexpr int MAX_F = 63;      // A hi/lo (2F+1 f16, padded to 16, two per column) in TMEM columns 256-383
@@ -78,8 +79,7 @@ __host__ __device__ inline Layout layout(int C, int F) {
 }
 
 inline size_t smem_bytes(int) {
-  return (size_t)RING + (size_t)TM * XS * 4 + (size_t)CAP * NEPI * 8 + (size_t)WMAX * TM * 16 +
-         (size_t)TM * 8 + 256;
+  return (size_t)RING + (size_t)TM * XS * 4 + (size_t)(CAP + 1) * NEPI * 8 + (size_t)TM * 4 + 256;
 }
 
 // ---------------------------------------------------------------- table construction
@@ -215,20 +215,17 @@ __global__ void __launch_bounds__(NT, 1)
     select_tc_kernel(const XT* __restrict__ x, int64_t T, int F, int C, int K, const __half* __restrict__ blob,
                      const float* __restrict__ maxes, const float* __restrict__ colscale,
                      const double* __restrict__ exact, float kappa, float kappa1,
-                     int group, int debug, Pipe pipe, int* __restrict__ flagged, int32_t* __restrict__ sel_out,
-                     double* __restrict__ val_out) {
+                     int group, int debug, Pipe pipe, float2* __restrict__ cand, int* __restrict__ cand_n,
+                     float4* __restrict__ fpar, double* __restrict__ val_arg) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  // debug 6/7 (timeline) take val_arg as the clock buffer and otherwise run like production
+  double* const tlbuf = (debug == 6 || debug == 7 || debug >= 12) ? val_arg : nullptr;  // 12-14: ablations
   const int KP = kp(F), KS = KP / 16, NCH = nchunks(C);
   uint8_t* ring = smem;                                             // [NST][STAGE]
   float* xs = reinterpret_cast<float*>(ring + RING);                // [TM][XS] frames of the tile (f32)
   const int STAGE = pipe.stage_bytes, NST = RING / STAGE;
-  float* cv = xs + TM * XS;                                         // [CAP][NEPI] approx scores
-  int* ci = reinterpret_cast<int*>(cv + CAP * NEPI);                // [CAP][NEPI] components
-  float* mv = reinterpret_cast<float*>(ci + CAP * NEPI);            // [WMAX][TM] merged window
-  int* mi = reinterpret_cast<int*>(mv + WMAX * TM);                 // [WMAX][TM]
-  double* ev = reinterpret_cast<double*>(mi + WMAX * TM);           // [WMAX][TM] exact scores
-  float* kth1 = reinterpret_cast<float*>(ev + WMAX * TM);           // [TM] K-th of the second half
-  int* cnt1 = reinterpret_cast<int*>(kth1 + TM);                    // [TM] window size of the second half
+  float2* cc = reinterpret_cast<float2*>(xs + TM * XS);             // [CAP+1][NEPI] (s~, component); row CAP: dump
+  float* kth1 = reinterpret_cast<float*>(cc + (CAP + 1) * NEPI);    // [TM] collection threshold per frame
   __shared__ uint64_t full[MAXST], empty[MAXST], tfull[2], tempty[2], afull[2], aempty[2];
   __shared__ uint32_t tmem_base;
   __shared__ float cs[128];  // colscale (feature column exponents of the f16 operands)
@@ -423,9 +420,9 @@ __global__ void __launch_bounds__(NT, 1)
     asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // every thread is done with xs before the next load_x
     uint32_t li = 0;
     // debug 6: per-phase clock64 timeline of CTA 0, epilogue thread 0 (into val_out)
-    const bool tl = (debug == 6 || debug == 7) && blockIdx.x == 0 && e == 0 && val_out;
+    const bool tl = tlbuf && blockIdx.x == 0 && e == 0;
     auto mark = [&](int it, int ph) {
-      if (tl && it < 64) val_out[it * 8 + ph] = (double)clock64();
+      if (tl && it < 64) tlbuf[it * 8 + ph] = (double)clock64();
     };
     for (int64_t it = 0; it < iters; it++, tile += gridDim.x, li++) {
       mark(it, 0);
@@ -452,7 +449,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (lane == 0) tc::mbar_arrive(&tempty[b]);
 #pragma unroll
         for (int j = 0; j < 2; j++) {
-          if (debug >= 2 && debug != 6) continue;  // diagnostics: MMA/producer pipeline only (2, 3, 7)
+          if ((debug >= 2 && debug <= 7 && debug != 6) || debug == 14) continue;  // diagnostics (2, 3, 7, 14)
           if (group == 32) {
             insert_top<NK>(top, group_max<32>(v[j], 0));
           } else if (group == 8) {
@@ -469,17 +466,16 @@ __global__ void __launch_bounds__(NT, 1)
       // union of both halves' lists: half 1 publishes, half 0 merges and publishes the threshold
       // (published through half 1's own candidate columns: free until its pass 1; the merged-window
       // arrays may still be in use by half 0 finishing the previous tile)
-      float* pub = cv + (e | 128);
-      float* pub2 = reinterpret_cast<float*>(ci + (e | 128));
+      auto pub = [&](int i) -> float& { return reinterpret_cast<float*>(cc + (i >> 1) * NEPI + (e | 128))[i & 1]; };
       if (h == 1) {
 #pragma unroll
-        for (int i = 0; i < NK; i++) (i < CAP ? pub[i * NEPI] : pub2[(i - CAP) * NEPI]) = top[i];
+        for (int i = 0; i < NK; i++) pub(i) = top[i];
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
       if (h == 0) {
 #pragma unroll
         for (int i = 0; i < NK; i++)
-          insert_top<NK>(top, i >= NK - K ? (i < CAP ? pub[i * NEPI] : pub2[(i - CAP) * NEPI]) : -INFINITY);
+          insert_top<NK>(top, i >= NK - K ? pub(i) : -INFINITY);
         // every exact score of the K group maxima is >= (their 1xTF32 score) - kappa1 S
         kth1[r] = kth_of<NK>(top, K) - kappa1 * S * inv - 3.0f * m;
       }
@@ -500,7 +496,7 @@ __global__ void __launch_bounds__(NT, 1)
 
       // ---- pass 1 (3xTF32): collect every score >= thr
       int cnt = 0;
-      bool ovf = false;
+      const uint32_t cbase = tc::smem_u32(cc + e);
       for (int n = 0; n < NCH; n++) {
         const int b = n % 2;
         tc::mbar_wait(&tfull[b], buf_uses(b, li, 1, n, NCH) & 1);
@@ -516,166 +512,40 @@ __global__ void __launch_bounds__(NT, 1)
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[b]);
           }
-          if (debug >= 2 && debug != 6) continue;
+          if ((debug >= 2 && debug <= 7 && debug != 6) || debug == 12) continue;
           const int c0 = n * NC + col;
+          // branch-free append: predicated 8-byte store into row min(cnt, CAP) (row CAP is a dump)
 #pragma unroll
           for (int u = 0; u < 32; u++) {
-            if (v[u] >= thr) {
-              if (cnt < CAP) {
-                cv[cnt * NEPI + e] = v[u];
-                ci[cnt * NEPI + e] = c0 + u;
-              }
-              cnt++;
-            }
+            const uint32_t addr = cbase + (uint32_t)min(cnt, CAP) * (uint32_t)(NEPI * sizeof(float2));
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ge.f32 p, %0, %1;\n @p st.shared.v2.b32 [%2], {%3, %4};\n}\n" ::"f"(v[u]),
+                "f"(thr), "r"(addr), "r"(__float_as_uint(v[u])), "r"(c0 + u)
+                : "memory");
+            cnt += v[u] >= thr ? 1 : 0;
           }
         }
         if (has_next && n == 0) prep_next();
-        if (has_next && n >= 1 && n <= 8) piece_A(tile + gridDim.x, li + 1, inv_next, n - 1);
+        if (has_next && n >= 1 && n <= 8 && debug != 13) piece_A(tile + gridDim.x, li + 1, inv_next, n - 1);
       }
       if (has_next) {
         for (int pc = NCH > 1 ? NCH - 1 : 0; pc < 8; pc++) piece_A(tile + gridDim.x, li + 1, inv_next, pc);
         finish_A(li + 1);
       }
 
-      // A operand of the next tile (all MMAs of this tile have completed: their last chunk was read)
       mark(it, 4);
-
-
       mark(it, 5);
-      // ---- half lists sorted by s~ desc (index asc on ties)
-      ovf = cnt > CAP;
-      const int W = (t < T && !ovf) ? cnt : 0;
-      {
-        for (int p = 0; p < W; p++) {
-          int bi = p;
-          float bv = cv[p * NEPI + e];
-          int bc = ci[p * NEPI + e];
-          for (int i = p + 1; i < W; i++) {
-            const float vv = cv[i * NEPI + e];
-            const int cc = ci[i * NEPI + e];
-            if (vv > bv || (vv == bv && cc < bc)) {
-              bv = vv;
-              bc = cc;
-              bi = i;
-            }
-          }
-          if (bi != p) {
-            cv[bi * NEPI + e] = cv[p * NEPI + e];
-            ci[bi * NEPI + e] = ci[p * NEPI + e];
-            cv[p * NEPI + e] = bv;
-            ci[p * NEPI + e] = bc;
-          }
-        }
-      }
-      if (h == 1) cnt1[r] = ovf ? -1 : W;
-      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
-
-      // ---- half 0 merges both halves into the frame window and flags the entries needing FP64
-      bool good = false;
-      unsigned need = 0u;
-      if (h == 0 && t < T) {
-        const int W1 = cnt1[r];
-        good = live && !ovf && W1 >= 0 && W + W1 >= K;
-        if (good) {
-          const float lb = thr;
-          const int o1 = e + 128;
-          int i0 = 0, i1 = 0, Wm = 0;
-          while (Wm < WMAX) {
-            const bool a0 = i0 < W && cv[i0 * NEPI + e] >= lb;
-            const bool a1 = i1 < W1 && cv[i1 * NEPI + o1] >= lb;
-            if (!a0 && !a1) break;
-            bool take0 = a0;
-            if (a0 && a1) {
-              const float v0 = cv[i0 * NEPI + e], v1 = cv[i1 * NEPI + o1];
-              take0 = v0 > v1 || (v0 == v1 && ci[i0 * NEPI + e] < ci[i1 * NEPI + o1]);
-            }
-            if (take0) {
-              mv[Wm * TM + r] = cv[i0 * NEPI + e];
-              mi[Wm * TM + r] = ci[i0 * NEPI + e];
-              i0++;
-            } else {
-              mv[Wm * TM + r] = cv[i1 * NEPI + o1];
-              mi[Wm * TM + r] = ci[i1 * NEPI + o1];
-              i1++;
-            }
-            Wm++;
-          }
-          // the collected K-th (a lower bound of the true K-th) must clear the collection threshold,
-          // otherwise window entries may have been skipped (pass-0 slack too small): exact path
-          if (Wm < K || mv[(K - 1) * TM + r] - m2 < thr) {
-            good = false;
-          } else {
-            const float lim = mv[(K - 1) * TM + r] - m2;  // the exact frame window
-            int We = K;
-            while (We < Wm && mv[We * TM + r] >= lim) We++;
-            const bool more = (i0 < W && cv[i0 * NEPI + e] >= lim) || (i1 < W1 && cv[i1 * NEPI + o1] >= lim);
-            if (We == WMAX && more) good = false;  // window larger than the merge buffer
-            for (int p = 0; good && p < K;) {
-              int q = p + 1;
-              while (q < We && mv[(q - 1) * TM + r] - mv[q * TM + r] <= m2) q++;
-              if (q - p > 1 || val_out || debug) need |= (q - p >= 32 ? 0xffffffffu : ((1u << (q - p)) - 1u)) << p;
-              p = q;
-            }
-          }
-        }
-        if (!good) {  // recomputed by select_exact_kernel
-          sel_out[t * K] = -1;
-          flagged[1 + atomicAdd(flagged, 1)] = (int)t;
-        }
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // half 1 may now reuse its candidate buffer
       mark(it, 6);
-      if (h == 0) {
-        {  // exact FP64 scores of the flagged entries: one converged pass over the warp
-          const XT* xr = x + (t < T ? t : 0) * F;
-          unsigned rest = need;
-          while (__any_sync(0xffffffffu, rest != 0u)) {
-            const int i = rest ? __ffs(rest) - 1 : -1;
-            rest &= rest - 1u;
-            if (i >= 0) ev[i * TM + r] = exact_score(xr, exact + (int64_t)mi[i * TM + r] * (2 * F + 2), F);
-          }
-        }
-        if (debug == 8 && val_out && t < T) {  // diagnostics: the tile's per-frame scales
-          val_out[t * K + 0] = inv;
-          val_out[t * K + 1] = S;
-          val_out[t * K + 2] = m2;
-          val_out[t * K + 3] = (double)li;
-        }
-        if (good) {
-          if (debug) {  // diagnostics: s~ - s of the s~-ordered window
-            for (int i = 0; i < K; i++) {
-              sel_out[t * K + i] = mi[i * TM + r];
-              if (val_out) val_out[t * K + i] = (double)mv[i * TM + r] / (double)inv - ev[i * TM + r];
-            }
-          } else {
-            for (int p = 0; p < 32;) {  // re-sort each flagged cluster by the exact rank
-              if (!((need >> p) & 1u)) {
-                p++;
-                continue;
-              }
-              int q = p + 1;
-              while (q < 32 && ((need >> q) & 1u) && mv[(q - 1) * TM + r] - mv[q * TM + r] <= m2) q++;
-              for (int i = p + 1; i < q; i++) {
-                const double vv = ev[i * TM + r];
-                const int cc = mi[i * TM + r];
-                int k = i;
-                while (k > p && better(vv, cc, ev[(k - 1) * TM + r], mi[(k - 1) * TM + r])) {
-                  ev[k * TM + r] = ev[(k - 1) * TM + r];
-                  mi[k * TM + r] = mi[(k - 1) * TM + r];
-                  k--;
-                }
-                ev[k * TM + r] = vv;
-                mi[k * TM + r] = cc;
-              }
-              p = q;
-            }
-            for (int i = 0; i < K; i++) {
-              sel_out[t * K + i] = mi[i * TM + r];
-              if (val_out) val_out[t * K + i] = ev[i * TM + r];
-            }
-          }
-        }
+      // ---- hand the window candidates to select_post_kernel: frame-major runs of CAP per half,
+      // count (-1: overflow) and the frame's threshold / margin / scale
+      if (t < T) {
+        const bool ovf = cnt > CAP;
+        float2* dst = cand + ((size_t)t * 2 + h) * CAP;
+        for (int j = 0; j < (ovf ? 0 : cnt); j++) dst[j] = cc[j * NEPI + e];
+        cand_n[t * 2 + h] = ovf ? -1 : cnt;
+        if (h == 0) fpar[t] = make_float4(thr, m2, inv, 0.0f);
       }
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // every thread is done with xs before the next load_x
       mark(it, 7);
       S = S_next;
       inv = inv_next;
@@ -748,6 +618,174 @@ __global__ void __launch_bounds__(XT_THREADS) select_exact_kernel(const XT* __re
   }
 }
 
+// ---------------------------------------------------------------- window merge, exact order, output
+// One warp per frame.  The two half lists (<= CAP each, every entry >= the collection threshold)
+// are bitonic-sorted together (one slot per lane when they fit 32 entries, else two) on 64-bit keys
+// that order (s~ desc, index asc).  The exact frame window is every entry >= s~_(K) - 2m; runs whose
+// consecutive gaps are <= 2m ("clusters") and that start inside the top K are rescored in FP64 — the
+// warp computes one 2F+1-term dot product at a time, F/32 terms per lane and a fixed shuffle tree —
+// and each member's final position is its cluster start plus the number of members that rank before
+// it under the stable-argsort rule.  Frames that cannot be decided (overflow, collected K-th below
+// the threshold, window wider than a warp) go to select_exact_kernel.
+__device__ __forceinline__ uint64_t sel_key(float v, int c) {  // larger key = earlier (s~ desc, index asc)
+  uint32_t u = __float_as_uint(v);
+  u ^= (u >> 31) ? 0xffffffffu : 0x80000000u;
+  return ((uint64_t)u << 32) | (uint32_t)(0x7fffffff - c);
+}
+__device__ __forceinline__ float key_v(uint64_t k) {
+  uint32_t u = (uint32_t)(k >> 32);
+  u ^= (u >> 31) ? 0x80000000u : 0xffffffffu;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ int key_c(uint64_t k) { return 0x7fffffff - (int)(uint32_t)k; }
+
+// descending bitonic sort of 32*NS keys, key index = 32 * slot + lane
+template <int NS>
+__device__ __forceinline__ void warp_sort_desc(uint64_t (&k)[2], int lane) {
+#pragma unroll
+  for (int w = 2; w <= 32 * NS; w <<= 1) {
+#pragma unroll
+    for (int j = w >> 1; j > 0; j >>= 1) {
+      if (j == 32) {
+        const uint64_t a = k[0], b = k[1];
+        k[0] = a > b ? a : b;
+        k[1] = a > b ? b : a;
+      } else {
+#pragma unroll
+        for (int sl = 0; sl < NS; sl++) {
+          const int i = 32 * sl + lane;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, k[sl], j);
+          // the lower index of a descending pair keeps the larger key
+          const bool keep_max = ((i & j) == 0) == ((i & w) == 0);
+          k[sl] = keep_max ? (o > k[sl] ? o : k[sl]) : (o < k[sl] ? o : k[sl]);
+        }
+      }
+    }
+  }
+}
+
+template <typename XT>
+__device__ __forceinline__ double warp_exact_score(double x0, double x1, const double* __restrict__ row, int F,
+                                                   int lane) {
+  double p = 0.0;
+  if (lane < F) p = x0 * fma(__ldg(row + lane), x0, __ldg(row + F + lane));
+  if (lane + 32 < F) p = fma(x1, fma(__ldg(row + lane + 32), x1, __ldg(row + F + lane + 32)), p);
+  if (lane == 0) p += __ldg(row + 2 * F);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+  return p;
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__ x, int64_t T, int F, int K,
+                                                          const double* __restrict__ exact,
+                                                          const float2* __restrict__ cand,
+                                                          const int* __restrict__ cand_n,
+                                                          const float4* __restrict__ fpar, int dbg_vals,
+                                                          int* __restrict__ flagged, int32_t* __restrict__ sel_out,
+                                                          double* __restrict__ val_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t pad = sel_key(-INFINITY, 0x7fffffff);
+  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += nw) {
+    const int n0 = cand_n[2 * t], n1 = cand_n[2 * t + 1];
+    const float4 par = fpar[t];
+    const float thr = par.x, m2 = par.y;
+    if (dbg_vals == 9) {  // diagnostics: candidate counts per half
+      if (lane == 0 && val_out) {
+        val_out[t * K] = n0;
+        val_out[t * K + 1] = n1;
+      }
+      continue;
+    }
+    bool good = n0 >= 0 && n1 >= 0 && n0 + n1 >= K;
+    uint64_t k[2] = {pad, pad};
+    float lim = INFINITY, v = -INFINITY;
+    int c = 0x7fffffff;
+    if (good) {
+      const float2* base = cand + (size_t)t * 2 * CAP;
+      const int n = n0 + n1;
+      // entries 0..n-1: half 0 then half 1 (lane-contiguous), then padding
+      if (lane < n) {
+        const float2 q = lane < n0 ? base[lane] : base[CAP + lane - n0];
+        k[0] = sel_key(q.x, __float_as_int(q.y));
+      }
+      if (n > 32) {
+        if (lane + 32 < n) {
+          const float2 q = base[CAP + lane + 32 - n0];
+          k[1] = sel_key(q.x, __float_as_int(q.y));
+        }
+        warp_sort_desc<2>(k, lane);
+      } else {
+        warp_sort_desc<1>(k, lane);
+      }
+      v = key_v(k[0]);
+      c = key_c(k[0]);
+      const float kv = __shfl_sync(0xffffffffu, v, K - 1);
+      lim = kv - m2;
+      // the collected K-th (a lower bound of the true K-th) must clear the collection threshold,
+      // and the exact window (all entries >= lim: a prefix) must fit one warp
+      if (kv - m2 < thr || key_v(k[1]) >= lim) good = false;
+      good = __all_sync(0xffffffffu, good);
+    }
+    if (!good) {
+      if (lane == 0) {
+        sel_out[t * K] = -1;
+        flagged[1 + atomicAdd(flagged, 1)] = (int)t;
+      }
+      continue;
+    }
+    const unsigned win = __ballot_sync(0xffffffffu, v >= lim);
+    const int We = __popc(win);
+    const float prev = __shfl_up_sync(0xffffffffu, v, 1);
+    const unsigned joined = __ballot_sync(0xffffffffu, lane >= 1 && lane < We && prev - v <= m2) & win;
+    const unsigned starts = win & ~joined;
+    const unsigned below = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);  // bits 0..lane
+    const int st = 31 - __clz(starts & below);                               // my cluster start
+    const unsigned after = starts & ~below;
+    const int en = after ? __ffs(after) - 1 : We;                            // my cluster end
+    const bool clustered = lane < We && en - st > 1 && st < K;
+    const bool want_all = val_out != nullptr || dbg_vals;
+    unsigned need = __ballot_sync(0xffffffffu, clustered || (want_all && lane < K));
+    double ev = 0.0;
+    if (need) {
+      const XT* xr = x + t * F;
+      const double x0 = lane < F ? (double)xr[lane] : 0.0, x1 = lane + 32 < F ? (double)xr[lane + 32] : 0.0;
+      while (need) {
+        const int j = __ffs(need) - 1;
+        need &= need - 1u;
+        const int cj = __shfl_sync(0xffffffffu, c, j);
+        const double s = warp_exact_score<XT>(x0, x1, exact + (int64_t)cj * (2 * F + 2), F, lane);
+        if (lane == j) ev = s;
+      }
+    }
+    if (dbg_vals) {  // diagnostics: s~ - s of the s~-ordered window
+      if (lane < K) {
+        sel_out[t * K + lane] = c;
+        if (val_out) val_out[t * K + lane] = (double)v / (double)par.z - ev;
+      }
+      continue;
+    }
+    // final position: cluster start + members ranked before me by (exact desc, index asc)
+    int pos = lane;
+    const unsigned cl_mask = __ballot_sync(0xffffffffu, clustered);
+    if (cl_mask) {
+      int cntb = 0;
+      const int hi = 32 - __clz(cl_mask);
+      for (int j = __ffs(cl_mask) - 1; j < hi; j++) {
+        const double ov = __shfl_sync(0xffffffffu, ev, j);
+        const int oc = __shfl_sync(0xffffffffu, c, j);
+        if (clustered && j >= st && j < en && j != lane && better(ov, oc, ev, c)) cntb++;
+      }
+      if (clustered) pos = st + cntb;
+    }
+    if (lane < We && pos < K) {
+      sel_out[t * K + pos] = c;
+      if (val_out) val_out[t * K + pos] = ev;
+    }
+  }
+}
+
 }  // namespace stc
 
 // ---------------------------------------------------------------- host side
@@ -804,11 +842,30 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   TVK_REQUIRE(pipe.stage_bytes >= 8192 && stc::RING % pipe.stage_bytes == 0 && stc::RING / pipe.stage_bytes <= stc::MAXST &&
                   pipe.sp0 * 4096 <= pipe.stage_bytes && pipe.sp1 * 8192 <= pipe.stage_bytes && pipe.sp0 > 0 && pipe.sp1 > 0,
               "select_tc: bad TVK_SEL_PIPE");
-  int* flagged = nullptr;  // [count | frame indices], stream-ordered scratch
-  if (cudaMallocAsync((void**)&flagged, sizeof(int) * (T + 1), st) != cudaSuccess) {
-    set_error("select_tc: cannot allocate %lld bytes of scratch", (long long)(sizeof(int) * (T + 1)));
+  // stream-ordered scratch: [flagged count | frame indices], candidate runs, counts, frame params
+  const size_t b_flag = stc::al(sizeof(int) * (T + 1), 256);
+  const size_t b_cand = stc::al(sizeof(float2) * 2 * stc::CAP * (size_t)T, 256);
+  const size_t b_n = stc::al(sizeof(int) * 2 * (size_t)T, 256);
+  const size_t b_par = sizeof(float4) * (size_t)T;
+  static bool pool_ready = false;
+  if (!pool_ready) {  // keep freed scratch mapped in the stream-ordered pool between calls
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_ready = true;
+  }
+  uint8_t* scratch = nullptr;
+  if (cudaMallocAsync((void**)&scratch, b_flag + b_cand + b_n + b_par, st) != cudaSuccess) {
+    set_error("select_tc: cannot allocate %lld bytes of scratch", (long long)(b_flag + b_cand + b_n + b_par));
     return TVK_ERR_CUDA;
   }
+  int* flagged = (int*)scratch;
+  float2* cand = (float2*)(scratch + b_flag);
+  int* cand_n = (int*)(scratch + b_flag + b_cand);
+  float4* fpar = (float4*)(scratch + b_flag + b_cand + b_n);
   cudaMemsetAsync(flagged, 0, sizeof(int), st);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -825,15 +882,22 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   cudaError_t le = cudaLaunchKernelEx(&cfg, kern, x, T, F, C, K, (const __half*)(base + L.blob),
                                       (const float*)(base + L.maxes), (const float*)(base + L.colscale),
                                       (const double*)(base + L.exact), kappa, kappa1,
-                                      group, debug, pipe, flagged, sel, val);
+                                      group, debug, pipe, cand, cand_n, fpar, val);
   if (le != cudaSuccess) {
     set_error("select_tc launch: %s", cudaGetErrorString(le));
     return TVK_ERR_CUDA;
   }
   TVK_CHECK_LAUNCH("select_tc");
+  if (debug < 2 || (debug > 7 && debug < 12)) {  // 2, 3, 6, 7, 12-14: tensor-core pipeline diagnostics only
+    const int64_t want_post = (T + 7) / 8;
+    const int post_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want_post, (int64_t)num_sms() * 8));
+    stc::select_post_kernel<XT><<<post_grid, 256, 0, st>>>(x, T, F, K, (const double*)(base + L.exact), cand, cand_n,
+                                                           fpar, debug, flagged, sel, val);
+    TVK_CHECK_LAUNCH("select_post");
+  }
   const char* dbg = getenv("TVK_SELECT");
   if (dbg && strcmp(dbg, "tc_noexact") == 0) {  // diagnostics: leave flagged frames at -1
-    cudaFreeAsync(flagged, st);
+    cudaFreeAsync(scratch, st);
     return TVK_OK;
   }
   const size_t xsm = sizeof(double) * C + sizeof(unsigned) * ((C + 31) / 32);
@@ -841,7 +905,7 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   stc::select_exact_kernel<XT><<<num_sms() * 2, stc::XT_THREADS, xsm, st>>>(x, F, C, K, (const double*)(base + L.exact),
                                                                              flagged, sel, val);
   TVK_CHECK_LAUNCH("select_exact");
-  cudaFreeAsync(flagged, st);
+  cudaFreeAsync(scratch, st);
   return TVK_OK;
 }
 

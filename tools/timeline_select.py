@@ -9,7 +9,7 @@ n = 2_000_000
 w, mu, cov = bench.make_ubm(0)
 x = bench.sample_frames(w, mu, cov, n, 5, torch.device("cuda"))
 tab = pkg.GmmDiag(w, mu, np.ascontiguousarray(np.diagonal(cov, axis1=1, axis2=2))).device_table()
-for dbg in ("6", "7"):
+for dbg in (sys.argv[1:] or ["6", "7"]):
     os.environ["TVK_SELECT_DEBUG"] = dbg
     os.environ["TVK_SELECT"] = "tc_noexact"
     sel, val = _device.select_topk(x, tab, 20, values=True)
