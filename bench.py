@@ -37,19 +37,19 @@ FLOP_FULL_PER_FRAME = 2 * C * Q            # dominant kernel (quadratic-feature 
 FLOP_DIAG_PER_FRAME = 2 * C * (2 * F + 1)   # preselection GEMM [x^2, x, 1] . Wdiag
 FLOP_PER_FRAME = FLOP_DIAG_PER_FRAME + FLOP_FULL_PER_FRAME   # 8,241,152 (dense)
 FLOP_GROUPED_PER_FRAME = 2 * K_TOP * F * F                   # (x-mu)' P (x-mu) for the K selected
-KP_TC = (2 * F + 1 + 7) // 8 * 8                             # [x^2, x, 1] padded to the MMA K step
-TF32_EXEC_PER_FRAME = 4 * 2 * KP_TC * C                      # 1xTF32 bound pass + 3xTF32 collection pass
+KP_TC = (2 * F + 1 + 15) // 16 * 16                          # [x^2, x, 1] padded to the f16 MMA K step
+F16_EXEC_PER_FRAME = 4 * 2 * KP_TC * C                       # 1xFP16 bound pass + 3xFP16 collection pass
 DMMA_EXEC_PER_FRAME = K_TOP * 1152 * 512 // 128              # whiten_ll: 1152 DMMA.8x8x4 per 128 pairs
 WINDOW_FRAMES = 131072                                       # grouped full-LL frame window (align_grouped.cu)
 
 
-def tf32_peak():
-    """TF32 dense peak: MEASURED_PEAKS.json's cuBLAS bf16 figure / 2 (tf32 issues at half the bf16 rate)."""
+def f16_peak():
+    """Dense f16/bf16 tensor peak (tcgen05 kind::f16): MEASURED_PEAKS.json's cuBLAS bf16 figure."""
     try:
         m = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
-        return m["bf16_tflops"] / 2.0, "measured bf16 (MEASURED_PEAKS.json) / 2"
+        return m["bf16_tflops"], "measured bf16 (MEASURED_PEAKS.json)"
     except Exception:
-        return 1590.0 / 2.0, "fallback bf16 1.59 PF / 2"
+        return 1590.0, "fallback bf16 1.59 PF (B200_PROFILING.md)"
 FP64_PEAK_FILE = os.path.join(REPO, "profiles", "r01_fp64_pipe_peak.txt")
 
 
@@ -296,9 +296,9 @@ def bench_ours(args):
     stage2()
     s2_ms = timed(stage2, 3)
     peak, peak_src = fp64_peak()
-    tpeak, tpeak_src = tf32_peak()
+    tpeak, tpeak_src = f16_peak()
     s1_tf = FLOP_DIAG_PER_FRAME * n / (s1_ms / 1e3) / 1e12
-    s1_exec = TF32_EXEC_PER_FRAME * n / (s1_ms / 1e3) / 1e12
+    s1_exec = F16_EXEC_PER_FRAME * n / (s1_ms / 1e3) / 1e12
     s2_tf = FLOP_GROUPED_PER_FRAME * n / (s2_ms / 1e3) / 1e12
     s2_exec = DMMA_EXEC_PER_FRAME * n / (s2_ms / 1e3) / 1e12
     # dense north-star variant: quadratic-feature GEMM over all C components (the reference's own work)
@@ -316,13 +316,13 @@ def bench_ours(args):
                  "full_ll_kernel": {"launch_ms": d2_ms, "flop_per_frame": FLOP_FULL_PER_FRAME,
                                     "achieved_tflops": FLOP_FULL_PER_FRAME * n / (d2_ms / 1e3) / 1e12,
                                     "frac_of_peak": FLOP_FULL_PER_FRAME * n / (d2_ms / 1e3) / 1e12 / peak}}
-    prof = os.path.join(REPO, "profiles", "r01_ncu_summary_v2.json")
+    prof = os.path.join(REPO, "profiles", "r01_ncu_summary_v3.json")
     traffic = None
     if os.path.exists(prof):
         try:  # DRAM bytes/frame of the dominant kernel from the committed ncu --set full capture
             reps = json.load(open(prof))["reports"]
             per_frame = [k["dram_bytes_per_frame"] for r in reps.values() for k in r
-                         if k["kernel"].startswith("tvk::stc::select_tc") and "dram_bytes_per_frame" in k][0]
+                         if k["kernel"].startswith("whiten_ll_kernel") and "dram_bytes_per_frame" in k][0]
             traffic = per_frame * n
         except Exception:
             traffic = None
@@ -364,25 +364,30 @@ def bench_ours(args):
                        "l2": "inputs (2.4 GB/GPU) larger than L2"},
             "x_realtime": value / 100.0,
             "entries_per_frame": entries / n,
-            # per step: select_tc + select_exact, 8 per grouped-LL frame window (hist memset/count/scan/
-            # scatter, tile count/scan/build, whiten_ll), finalize + 3 scan kernels + compact
-            "gpu_launches": args.steps * (2 + 8 * ((n + WINDOW_FRAMES - 1) // WINDOW_FRAMES) + 5),
+            # per step: select_tc + select_post + select_exact, 8 per grouped-LL frame window (hist
+            # memset/count/scan/scatter, tile count/scan/build, whiten_ll), finalize + 3 scans + compact
+            "gpu_launches": args.steps * (3 + 8 * ((n + WINDOW_FRAMES - 1) // WINDOW_FRAMES) + 5),
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": n * F * 4,
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                     "path": "paper_1906_08556_b200.align_frames(pinned host f32 frames) -> SparseAlignment"},
-            "roofline": {"bound": "tensor", "kernel": "select_tc_kernel (tcgen05 3xTF32 diag LL + exact top-20)",
-                         "achieved": s1_tf, "peak": tpeak, "unit": "TFLOP/s", "frac": s1_tf / tpeak,
-                         "peak_source": tpeak_src, "flop_per_frame": FLOP_DIAG_PER_FRAME, "launch_ms": s1_ms,
-                         "share_of_step": s1_ms / ms, "traffic": traffic,
-                         "executed_tf32_tflops": s1_exec, "executed_frac": s1_exec / tpeak,
-                         "executed_flop_per_frame": TF32_EXEC_PER_FRAME,
-                         "note": "achieved = algorithmic diag-LL flop (2C(2F+1)/frame); the kernel executes 4x "
-                                 "that on the TF32 pipe (1xTF32 bound pass + 3xTF32 pass) to be exact in FP64"},
-            "stages": {"select_tc_ms": s1_ms, "whiten_ll_ms": s2_ms,
-                       "whiten_ll": {"bound": "tensor (FP64 DMMA)", "achieved": s2_tf, "peak": peak,
-                                     "unit": "TFLOP/s", "frac": s2_tf / peak, "peak_source": peak_src,
-                                     "flop_per_frame": FLOP_GROUPED_PER_FRAME,
-                                     "executed_tflops": s2_exec, "executed_frac": s2_exec / peak},
+            # dominant kernel: whiten_ll (FP64 DMMA); the preselection stage is reported beside it
+            "roofline": {"bound": "tensor", "kernel": "whiten_ll_kernel (FP64 DMMA full-cov LL of the top-20 pairs)",
+                         "achieved": s2_tf, "peak": peak, "unit": "TFLOP/s", "frac": s2_tf / peak,
+                         "peak_source": peak_src, "flop_per_frame": FLOP_GROUPED_PER_FRAME, "launch_ms": s2_ms,
+                         "share_of_step": s2_ms / ms, "traffic": traffic,
+                         "executed_tflops": s2_exec, "executed_frac": s2_exec / peak,
+                         "executed_flop_per_frame": DMMA_EXEC_PER_FRAME,
+                         "note": "achieved = algorithmic 2*K*F^2 flop/frame (dense (x-mu)'P(x-mu) count); the "
+                                 "kernel executes the triangular U = L^-T product in 8x8x4 DMMA blocks"},
+            "stages": {"select_ms": s1_ms, "whiten_ll_ms": s2_ms,
+                       "select": {"bound": "tensor (tcgen05 kind::f16)",
+                                  "kernels": "select_tc_kernel (3xFP16 scores, candidate windows) + "
+                                             "select_post_kernel (window merge, FP64 cluster order) + "
+                                             "select_exact_kernel (flagged frames)",
+                                  "achieved": s1_tf, "peak": tpeak, "unit": "TFLOP/s", "frac": s1_tf / tpeak,
+                                  "peak_source": tpeak_src, "flop_per_frame": FLOP_DIAG_PER_FRAME,
+                                  "executed_f16_tflops": s1_exec, "executed_frac": s1_exec / tpeak,
+                                  "executed_flop_per_frame": F16_EXEC_PER_FRAME},
                        "rest_ms": ms - s1_ms - s2_ms},
             "dense_variant": dense,
             "clocks": clk,

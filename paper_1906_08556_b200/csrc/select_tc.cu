@@ -664,16 +664,29 @@ __device__ __forceinline__ void warp_sort_desc(uint64_t (&k)[2], int lane) {
   }
 }
 
-template <typename XT>
-__device__ __forceinline__ double warp_exact_score(double x0, double x1, const double* __restrict__ row, int F,
-                                                   int lane) {
-  double p = 0.0;
-  if (lane < F) p = x0 * fma(__ldg(row + lane), x0, __ldg(row + F + lane));
-  if (lane + 32 < F) p = fma(x1, fma(__ldg(row + lane + 32), x1, __ldg(row + F + lane + 32)), p);
-  if (lane == 0) p += __ldg(row + 2 * F);
+__device__ __forceinline__ void warp_exact_score2(double x0, double x1, const double* __restrict__ r0,
+                                                  const double* __restrict__ r1, int F, int lane, double& s0,
+                                                  double& s1) {
+  double p = 0.0, q = 0.0;
+  if (lane < F) {
+    p = x0 * fma(__ldg(r0 + lane), x0, __ldg(r0 + F + lane));
+    q = x0 * fma(__ldg(r1 + lane), x0, __ldg(r1 + F + lane));
+  }
+  if (lane + 32 < F) {
+    p = fma(x1, fma(__ldg(r0 + lane + 32), x1, __ldg(r0 + F + lane + 32)), p);
+    q = fma(x1, fma(__ldg(r1 + lane + 32), x1, __ldg(r1 + F + lane + 32)), q);
+  }
+  if (lane == 0) {
+    p += __ldg(r0 + 2 * F);
+    q += __ldg(r1 + 2 * F);
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-  return p;
+  for (int o = 16; o > 0; o >>= 1) {
+    p += __shfl_xor_sync(0xffffffffu, p, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+  s0 = p;
+  s1 = q;
 }
 
 template <typename XT>
@@ -705,16 +718,22 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
     if (good) {
       const float2* base = cand + (size_t)t * 2 * CAP;
       const int n = n0 + n1;
-      // entries 0..n-1: half 0 then half 1 (lane-contiguous), then padding
-      if (lane < n) {
-        const float2 q = lane < n0 ? base[lane] : base[CAP + lane - n0];
-        k[0] = sel_key(q.x, __float_as_int(q.y));
+      // entries 0..n-1: half 0 then half 1, then padding; the rows are loaded whole so the loads do
+      // not wait for the counts
+      float2 q0 = make_float2(-INFINITY, __int_as_float(0x7fffffff)), q1 = q0;
+      if (lane < CAP) {
+        q0 = base[lane];
+        q1 = base[CAP + lane];
       }
+      auto shfl2 = [](float2 q, int src) {
+        return make_float2(__shfl_sync(0xffffffffu, q.x, src), __shfl_sync(0xffffffffu, q.y, src));
+      };
+      const float2 a = shfl2(q1, (lane - n0) & 31);        // half-1 entry lane - n0
+      const float2 b2 = shfl2(q1, (lane + 32 - n0) & 31);  // half-1 entry lane + 32 - n0
+      const float2 e0 = lane < n0 ? q0 : a;
+      if (lane < n) k[0] = sel_key(e0.x, __float_as_int(e0.y));
       if (n > 32) {
-        if (lane + 32 < n) {
-          const float2 q = base[CAP + lane + 32 - n0];
-          k[1] = sel_key(q.x, __float_as_int(q.y));
-        }
+        if (lane + 32 < n) k[1] = sel_key(b2.x, __float_as_int(b2.y));
         warp_sort_desc<2>(k, lane);
       } else {
         warp_sort_desc<1>(k, lane);
@@ -751,12 +770,17 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
     if (need) {
       const XT* xr = x + t * F;
       const double x0 = lane < F ? (double)xr[lane] : 0.0, x1 = lane + 32 < F ? (double)xr[lane + 32] : 0.0;
-      while (need) {
-        const int j = __ffs(need) - 1;
+      while (need) {  // two entries per step: independent loads and shuffle trees
+        const int j0 = __ffs(need) - 1;
         need &= need - 1u;
-        const int cj = __shfl_sync(0xffffffffu, c, j);
-        const double s = warp_exact_score<XT>(x0, x1, exact + (int64_t)cj * (2 * F + 2), F, lane);
-        if (lane == j) ev = s;
+        const int j1 = need ? __ffs(need) - 1 : j0;
+        need &= need - 1u;
+        const int c0 = __shfl_sync(0xffffffffu, c, j0), c1 = __shfl_sync(0xffffffffu, c, j1);
+        double s0, s1;
+        warp_exact_score2(x0, x1, exact + (int64_t)c0 * (2 * F + 2), exact + (int64_t)c1 * (2 * F + 2), F, lane,
+                          s0, s1);
+        if (lane == j0) ev = s0;
+        if (lane == j1) ev = s1;
       }
     }
     if (dbg_vals) {  // diagnostics: s~ - s of the s~-ordered window
