@@ -860,7 +860,7 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   const float kappa1 = ek1 ? (float)atof(ek1) : stc::KAPPA1;
   // group maxima of 32 (or 8, or single scores) while at least 2K groups exist
   const int group = C >= 64 * K ? 32 : (C >= 16 * K ? 8 : 1);
-  stc::Pipe pipe{32768, 8, 4, 64, 0};  // 3 stages of 32 KB: pass 0 8 k16-steps (hi), pass 1 4 (hi + lo)
+  stc::Pipe pipe{65536, 8, 8, 64, 0};  // 2 stages of 64 KB: pass 0 8 k16-steps (hi), pass 1 8 (hi + lo)
   if (const char* ep = getenv("TVK_SEL_PIPE"))  // stage_bytes,sp0,sp1,sleep_prod,sleep_mma
     sscanf(ep, "%d,%d,%d,%d,%d", &pipe.stage_bytes, &pipe.sp0, &pipe.sp1, &pipe.sleep_prod, &pipe.sleep_mma);
   TVK_REQUIRE(pipe.stage_bytes >= 8192 && stc::RING % pipe.stage_bytes == 0 && stc::RING / pipe.stage_bytes <= stc::MAXST &&
