@@ -68,7 +68,7 @@ __global__ void lat(int n, int rounds, unsigned long long* cycles) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   int tid = threadIdx.x, warp = tid / 32;
-  for (int i = tid; i < (128 + 256) * 32; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.001f * (i % 7);
+  for (int i = tid; i < 80 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.001f * (i % 7);
   if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
   if (warp == 0) tc::tmem_alloc<512>(&tbase);
   tc::fence_proxy_async();
@@ -96,13 +96,13 @@ __global__ void lat(int n, int rounds, unsigned long long* cycles) {
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
-template <int MODE, int N>  // MODE 0: tf32 SS, 1: tf32 TS, 2: f16 SS
+template <int MODE, int N>  // MODE 0: tf32 SS, 1: tf32 TS, 2: f16 SS, 3: f16 TS, 4: f16 TS 2 acc, 5: f16 SS 2 acc
 __global__ void rate(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   int tid = threadIdx.x, warp = tid / 32;
-  for (int i = tid; i < (128 + 256) * 32; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.001f * (i % 7);
+  for (int i = tid; i < 80 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.001f * (i % 7);
   if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
   if (warp == 0) tc::tmem_alloc<512>(&tbase);
   tc::fence_proxy_async();
@@ -112,7 +112,7 @@ __global__ void rate(int iters, unsigned long long* cycles) {
   uint32_t tmem = tbase;
   if (tid == 0) {
     uint32_t a = tc::smem_u32(smem), b = a + 128 * 32 * 4;
-    uint32_t idesc = MODE == 2 ? ((1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24))
+    uint32_t idesc = MODE >= 2 ? ((1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24))
                                : tc::idesc_tf32(128, N);
     unsigned long long t0 = clock64();
     for (int i = 0; i < iters; i++) {
@@ -121,7 +121,17 @@ __global__ void rate(int iters, unsigned long long* cycles) {
         uint64_t bd = tc::smem_desc(b + 256 * s, 128, 8 * 32 * 4);
         if (MODE == 0) tc::mma_tf32(tmem, ad, bd, idesc, 1);
         else if (MODE == 1) tc::mma_tf32_ts(tmem, tmem + 256 + 8 * s, bd, idesc, 1);
-        else mma_f16(tmem, ad, bd, idesc, 1);
+        else if (MODE == 2) mma_f16(tmem, ad, bd, idesc, 1);
+        else if (MODE == 3) tc::mma_f16_ts(tmem, tmem + 256 + 8 * s, bd, idesc, 1);
+        else if (MODE == 4) tc::mma_f16_ts(tmem + (s & 1) * 128, tmem + 256 + 8 * s, bd, idesc, 1);
+        else if (MODE == 6) {  // f16 TS, fresh 4 KB K-major B tile (LBO 128, SBO 256) every MMA over 64 KB
+          const uint64_t bf = tc::smem_desc(a + 4096 * ((i * 4 + s) & 15), 128, 256);
+          tc::mma_f16_ts(tmem, tmem + 256 + 8 * s, bf, idesc, 1);
+        } else if (MODE == 7) {  // same tile every MMA, same layout
+          const uint64_t bf = tc::smem_desc(a, 128, 256);
+          tc::mma_f16_ts(tmem, tmem + 256 + 8 * s, bf, idesc, 1);
+        }
+        else if (MODE == 5) mma_f16(tmem + (s & 1) * 128, ad, bd, idesc, 1);
       }
     }
     tc::mma_commit(&bar);
@@ -139,7 +149,7 @@ void run(const char* name) {
   int iters = 4000;
   unsigned long long* dc;
   cudaMalloc(&dc, 8);
-  size_t sm = (128 + 256) * 32 * 4;
+  size_t sm = 80 * 1024;
   cudaFuncSetAttribute(rate<MODE, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   rate<MODE, N><<<148, 128, sm>>>(10, dc);
   cudaEvent_t e0, e1;
@@ -151,7 +161,7 @@ void run(const char* name) {
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long cyc; cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost);
   double nmma = 4.0 * iters;
-  double kk = MODE == 2 ? 16 : 8;
+  double kk = MODE >= 2 ? 16 : 8;
   double flops = nmma * 148 * 2.0 * 128 * N * kk;
   printf("%-14s N=%3d: %s %.1f cycles/MMA, %.0f TFLOP/s\n", name, N, err ? cudaGetErrorString(err) : "", cyc / nmma,
          flops / ms / 1e9);
@@ -164,6 +174,14 @@ int main() {
   run<1, 256>("tf32 TS");
   run<2, 128>("f16 SS");
   run<2, 256>("f16 SS");
+  run<3, 128>("f16 TS");
+  run<3, 64>("f16 TS");
+  run<4, 128>("f16 TS 2acc");
+  run<5, 128>("f16 SS 2acc");
+  run<2, 64>("f16 SS");
+  run<6, 128>("f16 TS fresh B");
+  run<7, 128>("f16 TS same B");
+  if (getenv("RATE_ONLY")) return 0;
   {
     unsigned long long* dc;
     cudaMalloc(&dc, 8);
