@@ -45,7 +45,7 @@ constexpr int NC = 128;        // components per chunk = MMA N
 constexpr int RING = 131072;   // B ring bytes: NST stages of STAGE bytes (runtime split, see Pipe)
 constexpr int XS = 64;         // smem row stride (floats) of the staged frame tile, >= F + 1
 constexpr int MAXST = 16;
-constexpr int CL = 2;          // CTAs per cluster sharing every B stage by TMA multicast
+constexpr int CL = 2;          // CTAs per cluster sharing every B stage by TMA multicast (pass 0: one chunk each)
 constexpr int KSTEP = 8192;    // blob bytes per k16-step: 128 comps x 16 k x (hi, lo) x 2 B
 constexpr int H = 2;           // epilogue warps per TMEM lane quarter (each takes half of a chunk's columns)
 constexpr int NEPI = 128 * H;  // epilogue threads
@@ -56,7 +56,7 @@ constexpr float KAPPA1 = 1.0f / 4096.0f;   // pass-0 slack (heuristic: the windo
 constexpr int MAX_F = 63;      // A hi/lo (2F+1 f16, padded to 16, two per column) in TMEM columns 256-383
 
 __host__ __device__ inline int kp(int F) { return (2 * F + 1 + 15) / 16 * 16; }  // [x^2, x, 1], padded to K=16
-__host__ __device__ inline int nchunks(int C) { return (C + NC - 1) / NC; }
+__host__ __device__ inline int nchunks(int C) { return (C + 2 * NC - 1) / (2 * NC) * 2; }  // even: pass 0 runs pairs
 
 // Layout of the tensor-core part of the diagonal table (after the (2F+1) x C FP64 table).
 struct Layout {
@@ -172,11 +172,11 @@ __device__ __forceinline__ void insert_top(float (&top)[NK], float t) {
     top[i] = hi;
   }
 }
-// Accumulator buffer b = n % 2 hosts chunk n of either pass: the number of earlier uses of b (its
-// mbarrier phase) at (tile li, pass, chunk n), for both sides.
+// Accumulator buffers b = 0, 1 (columns [128b, 128b + 128)).  Pass 0 computes chunk PAIRS with N = 256
+// MMAs into both buffers at once; pass 1 computes chunk n into buffer n % 2.  Number of earlier uses
+// of buffer b (its mbarrier phase) at (tile li, pass, index n = pair or chunk), for both sides.
 __device__ __forceinline__ uint32_t buf_uses(int b, uint32_t li, int pass, int n, int NCH) {
-  const uint32_t per_pass = (NCH - b + 1) / 2;
-  return (2 * li + pass) * per_pass + n / 2;
+  return li * NCH + (pass == 0 ? n : NCH / 2 + n / 2);
 }
 __device__ __forceinline__ uint32_t acc_col(int b) { return (uint32_t)(b * NC); }
 __device__ __forceinline__ uint32_t a_col(uint32_t li) { return 256u + 128u * (li & 1u); }
@@ -270,24 +270,31 @@ __global__ void __launch_bounds__(NT, 1)
       uint32_t q = 0;
       for (int64_t it = 0; it < iters; it++)
         for (int pass = 0; pass < 2; pass++) {
-          const int SP = pass == 0 ? pipe.sp0 : pipe.sp1;  // k-steps per stage
-          for (int n = 0; n < NCH; n++)
-            for (int s0 = 0; s0 < KS; s0 += SP, q++) {
-              const int slot = q % NST, ns = min(SP, KS - s0);
-              tc::mbar_wait_backoff(&empty[slot], ((q / NST) & 1) ^ 1, pipe.sleep_prod);
-              const uint32_t piece = ns * 4096, share = piece / CL;  // hi (and lo) words of ns k-steps
-              tc::mbar_arrive_expect_tx(&full[slot], pass == 0 ? piece : 2 * piece);
-              const size_t src = ((size_t)n * KS + s0) * 2048 + crank * (share / 2);
-              uint8_t* dst = ring + slot * STAGE + crank * share;
-              tc::bulk_g2s_mc(dst, blob + src, share, &full[slot], mask);
-              if (pass == 1) tc::bulk_g2s_mc(dst + piece, blob_lo + src, share, &full[slot], mask);
+          const int nst = pass == 0 ? NCH / 2 : NCH;  // stages: chunk pairs (pass 0), chunks (pass 1)
+          for (int n = 0; n < nst; n++, q++) {
+            const int slot = q % NST;
+            tc::mbar_wait_backoff(&empty[slot], ((q / NST) & 1) ^ 1, pipe.sleep_prod);
+            tc::mbar_arrive_expect_tx(&full[slot], KS * 8192);
+            uint8_t* st = ring + slot * STAGE;
+            if (pass == 0) {
+              // hi tiles of chunk 2n + crank, interleaved by k-step: (chunk 2n + r, s) at s * 8 KB + r * 4 KB,
+              // so each k-step's 256 components form one K-major N = 256 operand
+              const size_t ch = 2 * (size_t)n + crank;
+              for (int s2 = 0; s2 < KS; s2++)
+                tc::bulk_g2s_mc(st + s2 * 8192 + crank * 4096, blob + (ch * KS + s2) * 2048, 4096, &full[slot], mask);
+            } else {
+              const uint32_t piece = KS * 4096, share = piece / CL;  // hi then lo words of the chunk
+              const size_t src = (size_t)n * KS * 2048 + crank * (share / 2);
+              tc::bulk_g2s_mc(st + crank * share, blob + src, share, &full[slot], mask);
+              tc::bulk_g2s_mc(st + piece + crank * share, blob_lo + src, share, &full[slot], mask);
             }
+          }
         }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM)
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_f16(TM, NC);
+      const uint32_t idesc = tc::idesc_f16(TM, NC), idesc2 = tc::idesc_f16(TM, 2 * NC);
       const uint32_t rb = tc::smem_u32(ring);
       uint32_t q = 0, li = 0;
       const uint16_t mask = (uint16_t)((1u << CL) - 1u);
@@ -295,33 +302,43 @@ __global__ void __launch_bounds__(NT, 1)
         tc::mbar_wait_backoff(&afull[li & 1], (li >> 1) & 1, 64);
         const uint32_t tA_hi = tmem + a_col(li), tA_lo = tA_hi + 64;
         tc::fence_after_sync();
-        for (int pass = 0; pass < 2; pass++) {
-          const int SP = pass == 0 ? pipe.sp0 : pipe.sp1;
-          for (int n = 0; n < NCH; n++) {
-            const int b = n % 2;
-            tc::mbar_wait_backoff(&tempty[b], (buf_uses(b, li, pass, n, NCH) & 1) ^ 1, pipe.sleep_mma);
-            tc::fence_after_sync();
-            const uint32_t d = tmem + acc_col(b);
-            for (int s0 = 0; s0 < KS; s0 += SP, q++) {
-              const int slot = q % NST, ns = min(SP, KS - s0);
-              tc::mbar_wait_backoff(&full[slot], (q / NST) & 1, pipe.sleep_mma);
-              tc::fence_after_sync();
-              if (debug != 3) {  // debug 3: copies only
-                for (int i = 0; i < ns; i++) {
-                  const int s = s0 + i;
-                  const uint64_t bh = tc::smem_desc(rb + slot * STAGE + i * 4096, 128, 256);
-                  tc::mma_f16_ts(d, tA_hi + 8 * s, bh, idesc, s > 0);
-                  if (pass == 1) {  // 3xFP16: a_hi b_hi + a_hi b_lo + a_lo b_hi
-                    const uint64_t bl = tc::smem_desc(rb + slot * STAGE + (ns + i) * 4096, 128, 256);
-                    tc::mma_f16_ts(d, tA_hi + 8 * s, bl, idesc, 1);
-                    tc::mma_f16_ts(d, tA_lo + 8 * s, bh, idesc, 1);
-                  }
-                }
-              }
-              tc::mma_commit_mc(&empty[slot], mask);  // releases the slot in every CTA of the cluster
+        // pass 0: chunk pairs, one N = 256 MMA per k16-step into both accumulator buffers
+        for (int p = 0; p < NCH / 2; p++, q++) {
+          const uint32_t ph = (buf_uses(0, li, 0, p, NCH) & 1) ^ 1;
+          tc::mbar_wait_backoff(&tempty[0], ph, pipe.sleep_mma);
+          tc::mbar_wait_backoff(&tempty[1], ph, pipe.sleep_mma);
+          const int slot = q % NST;
+          tc::mbar_wait_backoff(&full[slot], (q / NST) & 1, pipe.sleep_mma);
+          tc::fence_after_sync();
+          if (debug != 3) {  // debug 3: copies only
+            for (int s2 = 0; s2 < KS; s2++) {
+              const uint64_t bh = tc::smem_desc(rb + slot * STAGE + s2 * 8192, 128, 256);
+              tc::mma_f16_ts(tmem, tA_hi + 8 * s2, bh, idesc2, s2 > 0);
             }
-            tc::mma_commit(&tfull[b]);
           }
+          tc::mma_commit_mc(&empty[slot], mask);  // releases the slot in every CTA of the cluster
+          tc::mma_commit(&tfull[0]);
+          tc::mma_commit(&tfull[1]);
+        }
+        // pass 1: chunks, 3xFP16 (a_hi b_hi + a_hi b_lo + a_lo b_hi), double-buffered accumulators
+        for (int n = 0; n < NCH; n++, q++) {
+          const int b = n % 2;
+          tc::mbar_wait_backoff(&tempty[b], (buf_uses(b, li, 1, n, NCH) & 1) ^ 1, pipe.sleep_mma);
+          const int slot = q % NST;
+          tc::mbar_wait_backoff(&full[slot], (q / NST) & 1, pipe.sleep_mma);
+          tc::fence_after_sync();
+          const uint32_t d = tmem + acc_col(b);
+          if (debug != 3) {
+            for (int s2 = 0; s2 < KS; s2++) {
+              const uint64_t bh = tc::smem_desc(rb + slot * STAGE + s2 * 4096, 128, 256);
+              const uint64_t bl = tc::smem_desc(rb + slot * STAGE + (KS + s2) * 4096, 128, 256);
+              tc::mma_f16_ts(d, tA_hi + 8 * s2, bh, idesc, s2 > 0);
+              tc::mma_f16_ts(d, tA_hi + 8 * s2, bl, idesc, 1);
+              tc::mma_f16_ts(d, tA_lo + 8 * s2, bh, idesc, 1);
+            }
+          }
+          tc::mma_commit_mc(&empty[slot], mask);
+          tc::mma_commit(&tfull[b]);
         }
         tc::mma_commit(&aempty[li & 1]);
       }
@@ -435,29 +452,38 @@ __global__ void __launch_bounds__(NT, 1)
       float top[NK];
 #pragma unroll
       for (int i = 0; i < NK; i++) top[i] = i < NK - K ? INFINITY : -INFINITY;
-      for (int n = 0; n < NCH; n++) {
-        const int b = n % 2;
-        tc::mbar_wait(&tfull[b], buf_uses(b, li, 0, n, NCH) & 1);
+      for (int p = 0; p < NCH / 2; p++) {
+        const uint32_t ph = buf_uses(0, li, 0, p, NCH) & 1;
+        tc::mbar_wait(&tfull[0], ph);
+        tc::mbar_wait(&tfull[1], ph);
         tc::fence_after_sync();
-        const uint32_t col = acc_col(b) + h * (NC / H);
-        float v[2][32];
-        tc::tmem_ld32(lane_addr + col, v[0]);
-        tc::tmem_ld32(lane_addr + col + 32, v[1]);
-        tc::tmem_ld_wait();
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[b]);
+#pragma unroll 1
+        for (int piece = 0; piece < 2; piece++) {  // this half's 128 of the pair's 256 columns, 64 at a time
+          const uint32_t col = h * (2 * NC / H) + piece * 64;
+          float v[2][32];
+          tc::tmem_ld32(lane_addr + col, v[0]);
+          tc::tmem_ld32(lane_addr + col + 32, v[1]);
+          tc::tmem_ld_wait();
+          if (piece == 1) {
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) {
+              tc::mbar_arrive(&tempty[0]);
+              tc::mbar_arrive(&tempty[1]);
+            }
+          }
 #pragma unroll
-        for (int j = 0; j < 2; j++) {
-          if ((debug >= 2 && debug <= 7 && debug != 6) || debug == 14) continue;  // diagnostics (2, 3, 7, 14)
-          if (group == 32) {
-            insert_top<NK>(top, group_max<32>(v[j], 0));
-          } else if (group == 8) {
+          for (int j = 0; j < 2; j++) {
+            if ((debug >= 2 && debug <= 7 && debug != 6) || debug == 14) continue;  // diagnostics (2, 3, 7, 14)
+            if (group == 32) {
+              insert_top<NK>(top, group_max<32>(v[j], 0));
+            } else if (group == 8) {
 #pragma unroll
-            for (int q = 0; q < 4; q++) insert_top<NK>(top, group_max<8>(v[j], 8 * q));
-          } else {
+              for (int q = 0; q < 4; q++) insert_top<NK>(top, group_max<8>(v[j], 8 * q));
+            } else {
 #pragma unroll
-            for (int q = 0; q < 32; q++) insert_top<NK>(top, v[j][q]);
+              for (int q = 0; q < 32; q++) insert_top<NK>(top, v[j][q]);
+            }
           }
         }
       }
@@ -860,12 +886,12 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   const float kappa1 = ek1 ? (float)atof(ek1) : stc::KAPPA1;
   // group maxima of 32 (or 8, or single scores) while at least 2K groups exist
   const int group = C >= 64 * K ? 32 : (C >= 16 * K ? 8 : 1);
-  stc::Pipe pipe{65536, 8, 8, 64, 0};  // 2 stages of 64 KB: pass 0 8 k16-steps (hi), pass 1 8 (hi + lo)
-  if (const char* ep = getenv("TVK_SEL_PIPE"))  // stage_bytes,sp0,sp1,sleep_prod,sleep_mma
-    sscanf(ep, "%d,%d,%d,%d,%d", &pipe.stage_bytes, &pipe.sp0, &pipe.sp1, &pipe.sleep_prod, &pipe.sleep_mma);
-  TVK_REQUIRE(pipe.stage_bytes >= 8192 && stc::RING % pipe.stage_bytes == 0 && stc::RING / pipe.stage_bytes <= stc::MAXST &&
-                  pipe.sp0 * 4096 <= pipe.stage_bytes && pipe.sp1 * 8192 <= pipe.stage_bytes && pipe.sp0 > 0 && pipe.sp1 > 0,
-              "select_tc: bad TVK_SEL_PIPE");
+  // one B stage = the hi words of a chunk pair (pass 0) or hi + lo of one chunk (pass 1): KS * 8 KB
+  const int KS = stc::kp(F) / 16;
+  stc::Pipe pipe{KS * 8192, KS, KS, 64, 0};
+  if (const char* ep = getenv("TVK_SEL_PIPE"))  // sleep_prod,sleep_mma (ns back-off of the single-thread roles)
+    sscanf(ep, "%d,%d", &pipe.sleep_prod, &pipe.sleep_mma);
+  TVK_REQUIRE(stc::RING / pipe.stage_bytes >= 2 && stc::RING / pipe.stage_bytes <= stc::MAXST, "select_tc: bad ring");
   // stream-ordered scratch: [flagged count | frame indices], candidate runs, counts, frame params
   const size_t b_flag = stc::al(sizeof(int) * (T + 1), 256);
   const size_t b_cand = stc::al(sizeof(float2) * 2 * stc::CAP * (size_t)T, 256);
