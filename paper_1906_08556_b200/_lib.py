@@ -132,15 +132,49 @@ def ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+_STAGE_MIN = 8 << 20          # host arrays at least this large go through the pinned staging buffer
+_stage = {"buf": None, "ev": None}
+_stage_pool = None
+
+
+def _stage_copy(dst, src):
+    """dst[:] = src for equal-shape CPU tensors, row blocks copied by a small thread pool (numpy copies
+    release the GIL), so a large host array reaches pinned memory at memory bandwidth."""
+    global _stage_pool
+    import concurrent.futures as cf
+    if _stage_pool is None:
+        _stage_pool = cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1), thread_name_prefix="tvk-stage")
+    d, s_ = dst.numpy().reshape(-1), src.numpy().reshape(-1)
+    n = d.shape[0]
+    step = -(-n // _stage_pool._max_workers)
+    list(_stage_pool.map(lambda lo: np.copyto(d[lo:lo + step], s_[lo:lo + step]), range(0, n, step)))
+
+
 def to_dev(a, dtype=torch.float64):
-    """Host array -> contiguous device tensor (pinned staging for large copies)."""
+    """Host array -> contiguous device tensor.  Large arrays (>= 8 MiB, e.g. a 2048 x 60 x 60 covariance
+    stack) are staged through one reused pinned buffer and copied asynchronously."""
     if isinstance(a, torch.Tensor):
         return a.to(device=device(), dtype=dtype).contiguous()
     arr = np.ascontiguousarray(a)
     t = torch.from_numpy(arr)
     if t.dtype != dtype:
         t = t.to(dtype)
-    return t.to(device(), non_blocking=False).contiguous()
+    if t.numel() * t.element_size() < _STAGE_MIN:
+        return t.to(device(), non_blocking=False).contiguous()
+    nbytes = t.numel() * t.element_size()
+    if _stage["ev"] is not None:
+        _stage["ev"].synchronize()  # the previous staged copy has left the buffer
+    buf = _stage["buf"]
+    if buf is None or buf.numel() < nbytes:
+        buf = _stage["buf"] = torch.empty(max(nbytes, 64 << 20), dtype=torch.uint8, pin_memory=True)
+    view = buf[:nbytes].view(t.dtype).view(t.shape)
+    _stage_copy(view, t)
+    out = torch.empty(t.shape, dtype=t.dtype, device=device())
+    out.copy_(view, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    _stage["ev"] = ev
+    return out
 
 
 def empty(shape, dtype=torch.float64):
