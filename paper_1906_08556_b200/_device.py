@@ -142,6 +142,7 @@ def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True, den
 
 
 STREAM_CHUNK = 1 << 19  # frames per chunk of the host-input alignment pipeline
+N_SLOTS = 4             # pinned result staging slots = pieces whose host unstaging may run concurrently
 _staging = {}             # (chunk, k) -> pinned host staging slots, reused across calls
 _copier = None
 
@@ -152,7 +153,7 @@ def _pinned_slots(chunk, k):
         _staging.clear()
         _staging[key] = [(torch.empty(chunk + 1, dtype=torch.int64, pin_memory=True),
                           torch.empty(chunk * k, dtype=torch.int32, pin_memory=True),
-                          torch.empty(chunk * k, dtype=torch.float32, pin_memory=True)) for _ in range(2)]
+                          torch.empty(chunk * k, dtype=torch.float32, pin_memory=True)) for _ in range(N_SLOTS)]
     return _staging[key]
 
 
@@ -182,9 +183,10 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
     wts = np.empty(T * k, np.float32)
     offsets[0] = 0
     if _copier is None:
-        _copier = cf.ThreadPoolExecutor(max_workers=1, thread_name_prefix="tvk-copy")
+        # first-touch page faults of the returned arrays dominate the unstaging: run pieces in parallel
+        _copier = cf.ThreadPoolExecutor(max_workers=N_SLOTS, thread_name_prefix="tvk-copy")
     slots = _pinned_slots(chunk, k)
-    slot_busy = [None, None]
+    slot_busy = [None] * N_SLOTS
     comp_stream = torch.cuda.current_stream()
     copy_stream, drain_stream = torch.cuda.Stream(), torch.cuda.Stream()
     bufs = [_lib.empty((chunk, F), host.dtype) for _ in range(2)]
@@ -250,12 +252,12 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
         done.record(comp_stream)
         free[i % 2] = done
         if pending is not None:
-            base = drain(pending, base, nd % 2)
+            base = drain(pending, base, nd % N_SLOTS)
             nd += 1
         pending = (lo, n, res, done)
         lo += n
     if pending is not None:
-        base = drain(pending, base, nd % 2)
+        base = drain(pending, base, nd % N_SLOTS)
     for f in slot_busy:
         if f is not None:
             f.result()
