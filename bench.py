@@ -107,37 +107,49 @@ def sample_frames(w, mu, cov, n, seed, device):
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (the recipe's clocks line)."""
+    """nvidia-smi sampler (the recipe's clocks line).  Started before the warm-up so it is already
+    sampling when the timed region begins; only samples stamped inside [mark(), stop()] are kept."""
 
     def __init__(self, index):
         self.proc = None
+        self.t0 = None
         self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                ["nvidia-smi", "-i", str(index), "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
+    def mark(self):
+        self.t0 = time.time()
+
     def stop(self):
         if self.proc is None:
             return None
+        t1 = time.time()
+        time.sleep(0.15)  # let the sample covering the end of the region land
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        import datetime
         rows = []
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                try:
-                    rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
-                except ValueError:
-                    pass
+            if len(parts) < 8:
+                continue
+            try:
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if self.t0 is not None and not (self.t0 <= ts <= t1 + 0.1):
+                    continue
+                rows.append((float(parts[1]), float(parts[2]), parts[4:8]))
+            except ValueError:
+                pass
         if not rows:
             return None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -257,16 +269,19 @@ def bench_ours(args):
         torch.cuda.synchronize()
         return ev0.elapsed_time(ev1) / reps
 
+    clocks = Clocks(local)
     for _ in range(args.warmup):
         step()
+    torch.cuda.synchronize()
     barrier()
     log("[bench] warm-up done")
-    clocks = Clocks(local)
+    clocks.mark()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
+    torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
