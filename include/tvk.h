@@ -53,6 +53,12 @@ int tvk_version(void);
 /* Copies the calling thread's last error message into buf (NUL-terminated); returns its length. */
 int tvk_last_error(char* buf, int64_t n);
 
+/* Host-side ALN1 alignment-cache decoder walk (io_formats.py:154-227, read_alignment): for one
+ * utterance's u32 frame stream, starts[t] / counts[t] = word offset and entry count of frame t, *end =
+ * words consumed.  TVK_ERR_INVALID with the reference's message when the stream is short.  No device. */
+int tvk_aln1_scan(const uint32_t* words, int64_t n_words, int64_t n_frames, int64_t* starts, int64_t* counts,
+                  int64_t* end);
+
 /* ---------------------------------------------------------------- dense algebra */
 
 /* Batched FP64 GEMM on the DMMA tensor pipe, row-major:

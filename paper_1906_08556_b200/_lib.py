@@ -34,6 +34,7 @@ _d = ctypes.c_double
 # name -> (restype, argtypes); mirrors include/tvk.h
 SIGNATURES = {
     "tvk_version": (_i, []),
+    "tvk_aln1_scan": (_i, [_p, _i64, _i64, _p, _p, _p]),
     "tvk_last_error": (_i, [ctypes.c_char_p, _i64]),
     "tvk_dgemm": (_i, [_i, _i, _i, _i, _i, _d, _p, _i64, _i64, _p, _i64, _i64, _d, _p, _i64, _i64, _i, _i, _i,
                        _p, _p]),

@@ -26,3 +26,26 @@ extern "C" int tvk_last_error(char* buf, int64_t n) {
   }
   return len;
 }
+
+// ALN1 frame-record walk (read_alignment's decoder, io_formats.py:154-227): host code, no device.
+// words = one utterance's u32 stream [count_t, (component, weight bits) * count_t] for t < n_frames.
+extern "C" int tvk_aln1_scan(const uint32_t* words, int64_t n_words, int64_t n_frames, int64_t* starts,
+                             int64_t* counts, int64_t* end) {
+  int64_t pos = 0;
+  for (int64_t t = 0; t < n_frames; t++) {
+    if (pos >= n_words) {
+      tvk::set_error("aln1: frame record shorter than declared (entry count)");
+      return TVK_ERR_INVALID;
+    }
+    const int64_t k = words[pos];
+    starts[t] = pos;
+    counts[t] = k;
+    pos += 1 + 2 * k;
+  }
+  if (pos > n_words) {
+    tvk::set_error("aln1: frame record shorter than declared (frame entries)");
+    return TVK_ERR_INVALID;
+  }
+  *end = pos;
+  return TVK_OK;
+}

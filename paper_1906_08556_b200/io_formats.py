@@ -155,18 +155,21 @@ def _decode_frames(words, n_frames):
     """Inverse of _encode_frames; frame starts found by walking the count words."""
     from .gmm import SparseAlignment
 
+    import ctypes
+
+    from . import _lib
+
+    words = np.ascontiguousarray(words, dtype="<u4")
     starts = np.empty(n_frames, dtype=np.int64)
     counts = np.empty(n_frames, dtype=np.int64)
-    pos = 0
-    # chunked walk: each step advances by 1 + 2*count; vectorize over the known prefix
-    for t in range(n_frames):
-        if pos >= words.shape[0]:
-            raise FormatError("frame record shorter than declared (entry count)")
-        k = int(words[pos])
-        starts[t], counts[t] = pos, k
-        pos += 1 + 2 * k
-    if pos > words.shape[0]:
-        raise FormatError("frame record shorter than declared (frame entries)")
+    end = ctypes.c_int64(0)
+    # the sequential count-word walk runs in libtvk's host code (tvk_aln1_scan)
+    st = _lib.load().tvk_aln1_scan(words.ctypes.data_as(ctypes.c_void_p), words.shape[0], n_frames,
+                                   starts.ctypes.data_as(ctypes.c_void_p), counts.ctypes.data_as(ctypes.c_void_p),
+                                   ctypes.byref(end))
+    if st != _lib.TVK_OK:
+        raise FormatError(_lib.last_error().replace("aln1: ", ""))
+    pos = int(end.value)
     E = int(counts.sum())
     offsets = np.zeros(n_frames + 1, dtype=np.int64)
     np.cumsum(counts, out=offsets[1:])
