@@ -147,3 +147,19 @@ def test_fmx1_round_trip(tmp_path):
     open(p, "ab").write(b"x")
     with pytest.raises(FormatError):
         read_matrix(p)
+
+
+def test_aln1_corrupt_counts_raise(tmp_path):
+    """A count word that runs past the record raises FormatError (io_formats.py:200-227 semantics)."""
+    from paper_1906_08556_b200.gmm import SparseAlignment
+    from paper_1906_08556_b200.io_formats import FormatError, read_alignment, write_alignment
+    ali = SparseAlignment.from_frames([(np.array([1, 3]), np.array([0.25, 0.75], np.float32)),
+                                       (np.array([2]), np.array([1.0], np.float32))])
+    path = str(tmp_path / "y.aln")
+    write_alignment(path, {"u": ali}, top_k=2)
+    raw = bytearray(open(path, "rb").read())
+    first = 24 + 4 + 1 + 8  # header, id length, id, frame count
+    raw[first:first + 4] = struct.pack("<I", 1000)
+    open(path, "wb").write(bytes(raw))
+    with pytest.raises(FormatError, match="shorter than declared"):
+        read_alignment(path)
