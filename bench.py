@@ -36,7 +36,7 @@ Q = 1 + F + F * (F + 1) // 2
 FLOP_FULL_PER_FRAME = 2 * C * Q            # dominant kernel (quadratic-feature GEMM)
 FLOP_DIAG_PER_FRAME = 2 * C * (2 * F + 1)   # preselection GEMM [x^2, x, 1] . Wdiag
 FLOP_PER_FRAME = FLOP_DIAG_PER_FRAME + FLOP_FULL_PER_FRAME   # 8,241,152 (dense)
-FLOP_GROUPED_PER_FRAME = 2 * K_TOP * F * F                   # (x-mu)' P (x-mu) for the K selected
+FLOP_GROUPED_PER_FRAME = 2 * K_TOP * Q                       # quadratic-feature count for the K selected
 KP_TC = (2 * F + 1 + 15) // 16 * 16                          # [x^2, x, 1] padded to the f16 MMA K step
 F16_EXEC_PER_FRAME = 4 * 2 * KP_TC * C                       # 1xFP16 bound pass + 3xFP16 collection pass
 DMMA_EXEC_PER_FRAME = K_TOP * 1152 * 512 // 128              # whiten_ll: 1152 DMMA.8x8x4 per 128 pairs
@@ -392,8 +392,9 @@ def bench_ours(args):
                          "share_of_step": s2_ms / ms, "traffic": traffic,
                          "executed_tflops": s2_exec, "executed_frac": s2_exec / peak,
                          "executed_flop_per_frame": DMMA_EXEC_PER_FRAME,
-                         "note": "achieved = algorithmic 2*K*F^2 flop/frame (dense (x-mu)'P(x-mu) count); the "
-                                 "kernel executes the triangular U = L^-T product in 8x8x4 DMMA blocks"},
+                         "note": "achieved = algorithmic 2*K*Q flop/frame (Q = 1+F+F(F+1)/2: the quadratic-feature "
+                                 "count of SURVEY 8(d) restricted to the K selected components, 8(f) row 3); the kernel "
+                                 "executes the triangular U = L^-T product in 8x8x4 DMMA blocks (executed_flop_per_frame)"},
             "stages": {"select_ms": s1_ms, "whiten_ll_ms": s2_ms,
                        "select": {"bound": "tensor (tcgen05 kind::f16)",
                                   "kernels": "select_tc_kernel (3xFP16 scores, candidate windows) + "
