@@ -143,6 +143,7 @@ def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True, den
 
 STREAM_CHUNK = 1 << 19  # frames per chunk of the host-input alignment pipeline
 N_SLOTS = 4             # pinned result staging slots = pieces whose host unstaging may run concurrently
+RAMP_PIECE = 1 << 17    # first / last pieces of the host pipeline (only their copies cannot overlap)
 _staging = {}             # (chunk, k) -> pinned host staging slots, reused across calls
 _copier = None
 
@@ -222,7 +223,7 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
 
     # piece sizes ramp up and down (chunk/4, chunk/2, chunk, ..., chunk/2, chunk/4) so that the first
     # host->device copy and the last copy-out, which cannot overlap anything, are short
-    sizes, rest, q = [], T, max(1, chunk // 4)
+    sizes, rest, q = [], T, max(1, min(chunk // 4, RAMP_PIECE))
     for c in (q, 2 * q):
         if rest > 0:
             sizes.append(min(c, rest))
