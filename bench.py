@@ -39,7 +39,8 @@ FLOP_PER_FRAME = FLOP_DIAG_PER_FRAME + FLOP_FULL_PER_FRAME   # 8,241,152 (SURVEY
 FLOP_GROUPED_PER_FRAME = 2 * K_TOP * Q                       # quadratic-feature count for the K selected
 KP_TC = (2 * F + 1 + 15) // 16 * 16                          # [x^2, x, 1] padded to the f16 MMA K step
 F16_EXEC_PER_FRAME = 4 * 2 * KP_TC * C                       # 1xFP16 bound pass + 3xFP16 collection pass
-DMMA_EXEC_PER_FRAME = K_TOP * 1152 * 512 // 128              # whiten_ll: 1152 DMMA.8x8x4 per 128 pairs
+# whiten_ll: per 128-pair tile, 8 warps x sum over k4-steps kk < ceil(F/4) of 2 * (8 - kk // 2) DMMA.8x8x4
+DMMA_EXEC_PER_FRAME = K_TOP * 8 * sum(2 * (8 - kk // 2) for kk in range((F + 3) // 4)) * 512 // 128
 WINDOW_FRAMES = 131072                                       # grouped full-LL frame window (align_grouped.cu)
 
 

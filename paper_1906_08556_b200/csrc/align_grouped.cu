@@ -178,9 +178,10 @@ __device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem) {
 // (4 wide) only when 4 kk <= 8 n + 7 (U upper triangular).
 template <typename XT>
 __device__ __forceinline__ void whiten_mma(const XT* X, const double* U, const double* mu, int w, int g, int t4,
-                                           double (&acc)[2][8][2]) {
+                                           int kkmax, double (&acc)[2][8][2]) {
 #pragma unroll
   for (int kk = 0; kk < GP / 4; kk++) {
+    if (kk >= kkmax) break;  // k-steps past F: zero rows of U
     const int k = kk * 4 + t4;
     const double m = mu[k];
     double a[2];
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(GT, 2)
       for (int i = 0; i < 2; i++)
 #pragma unroll
         for (int n = 0; n < 8; n++) acc[i][n][0] = acc[i][n][1] = 0.0;
-      whiten_mma(S.X[xb], S.U, S.mu, warp, g, t4, acc);
+      whiten_mma(S.X[xb], S.U, S.mu, warp, g, t4, (F + 3) / 4, acc);
 #pragma unroll
       for (int i = 0; i < 2; i++) {
         double s = 0.0;
