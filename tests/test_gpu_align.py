@@ -328,8 +328,9 @@ def _select(gpu, x, dm, k, mode, monkeypatch, values=True):
 
 
 @pytest.mark.parametrize("C,F,k,sd", [(2048, 60, 20, 0.3), (100, 13, 7, 0.5), (300, 63, 32, 0.5), (20, 5, 20, 0.5),
-                                      (129, 8, 1, 0.5), (700, 24, 20, 3.0)],
-                         ids=["config2", "C100", "F63K32", "C=K", "K1", "spread"])
+                                      (129, 8, 1, 0.5), (700, 24, 20, 3.0), (2100, 40, 20, 0.3),
+                                      (16384, 20, 20, 0.3)],
+                         ids=["config2", "C100", "F63K32", "C=K", "K1", "spread", "odd_pair", "C16384"])
 def test_tensor_core_preselection_is_exact(gpu, monkeypatch, C, F, k, sd):
     """The 3xTF32 tcgen05 preselection (select_tc.cu) returns exactly the stable top-K of the FP64
     scores: same indices and order as the FP64 DMMA kernel and the oracle's stable argsort."""
