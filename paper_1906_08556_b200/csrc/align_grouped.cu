@@ -28,7 +28,7 @@ constexpr int GROWS = 128;      // pairs per tile
 constexpr int GT = 256;         // threads (8 warps of 32 rows x 4 column blocks)
 constexpr int GS = GP + 4;      // smem row stride of U (doubles) and of the frame rows (elements)
 constexpr int kSortChunk = 4096;
-constexpr int64_t kGroupWindowFrames = 131072;  // 31 MB of f32 frames per window
+constexpr int64_t kGroupWindowFrames = 131072;  // 31 MB of f32 frames: the 20 gathers of a frame hit L2
 
 // Whitening table row: [U = L^-T (64 x 64, zero padded) | mu (64) | const | pad],
 // const = log w_c - (F log 2pi + log|Sigma_c|)/2.
@@ -339,7 +339,26 @@ static GroupWs group_carve(void* base, int64_t n_pairs, int C) {
 }
 
 int64_t grouped_workspace_bytes(int64_t n_pairs, int C) {
-  return (int64_t)group_carve(nullptr, std::min<int64_t>(n_pairs, kGroupWindowFrames * 32), C).bytes;
+  const int64_t one = (int64_t)group_carve(nullptr, std::min<int64_t>(n_pairs, kGroupWindowFrames * 32), C).bytes;
+  return n_pairs > kGroupWindowFrames ? 2 * one : one;  // two windows in flight (see grouped_full_ll)
+}
+
+// Second stream + fork/join events of the window pipeline, one set per device.
+struct WindowStreams {
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static WindowStreams& window_streams() {
+  static WindowStreams ws[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  WindowStreams& w = ws[dev & 63];
+  if (!w.s2) {
+    cudaStreamCreateWithFlags(&w.s2, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&w.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&w.join, cudaEventDisableTiming);
+  }
+  return w;
 }
 
 template <typename XT, bool VEC>
@@ -380,27 +399,47 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
   // frame windows sized so the window's frames and the whitening table stay L2-resident while the
   // window's pairs (sorted by component, i.e. random in frame order) gather their frame rows
   const int64_t win = std::min<int64_t>(T, kGroupWindowFrames);
-  GroupWs w = group_carve(ws_base, win * K, C);
-  TVK_REQUIRE(ws_base != nullptr && (int64_t)w.bytes <= ws_bytes, "grouped full log-likelihood: workspace too small");
+  const int nwin = (int)((T + win - 1) / win);
+  // windows alternate between the caller's stream and a second one, each with its own workspace set,
+  // so one window's pair sort and kernel ramp overlap the previous window's whitening tail
+  GroupWs w[2];
+  w[0] = group_carve(ws_base, win * K, C);
+  TVK_REQUIRE(ws_base != nullptr && (int64_t)w[0].bytes * (nwin > 1 ? 2 : 1) <= ws_bytes,
+              "grouped full log-likelihood: workspace too small");
+  if (nwin > 1) w[1] = group_carve((char*)ws_base + w[0].bytes, win * K, C);
   size_t sc_smem = sizeof(int) * 2 * C;
   cudaFuncSetAttribute(pair_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool vec = ((F * sizeof(XT)) % 16 == 0) && ((uintptr_t)x % 16 == 0);
-  for (int64_t f0 = 0; f0 < T; f0 += win) {
+  WindowStreams* ws2 = nullptr;
+  if (nwin > 1) {
+    ws2 = &window_streams();
+    cudaEventRecord(ws2->fork, st);
+    cudaStreamWaitEvent(ws2->s2, ws2->fork, 0);
+  }
+  for (int i = 0; i < nwin; i++) {
+    const int64_t f0 = (int64_t)i * win;
     const int64_t nf = std::min<int64_t>(win, T - f0);
     const int64_t np = nf * K;
     const int32_t* wsel = sel + f0 * K;
-    TVK_TRY(sort_tiles(wsel, nullptr, np, C, w, st));
+    cudaStream_t s = (i & 1) ? ws2->s2 : st;
+    const GroupWs& wi = w[i & 1];
+    TVK_TRY(sort_tiles(wsel, nullptr, np, C, wi, s));
     // the kernel reads the tile count from tile_start[C]
-    GroupWs wc = w;
-    wc.tile_start = w.tile_start + C;
+    GroupWs wc = wi;
+    wc.tile_start = wi.tile_start + C;
     if (vec)
-      TVK_TRY((launch_whiten<XT, true>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, st)));
+      TVK_TRY((launch_whiten<XT, true>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s)));
     else
-      TVK_TRY((launch_whiten<XT, false>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, st)));
+      TVK_TRY((launch_whiten<XT, false>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s)));
   }
+  if (ws2) {
+    cudaEventRecord(ws2->join, ws2->s2);
+    cudaStreamWaitEvent(st, ws2->join, 0);
+  }
+  TVK_CHECK_LAUNCH("grouped windows");
   return TVK_OK;
 }
 
