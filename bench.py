@@ -41,7 +41,7 @@ KP_TC = (2 * F + 1 + 15) // 16 * 16                          # [x^2, x, 1] padde
 F16_EXEC_PER_FRAME = 4 * 2 * KP_TC * C                       # 1xFP16 bound pass + 3xFP16 collection pass
 # whiten_ll: per 128-pair tile, 8 warps x sum over k4-steps kk < ceil(F/4) of 2 * (8 - kk // 2) DMMA.8x8x4
 DMMA_EXEC_PER_FRAME = K_TOP * 8 * sum(2 * (8 - kk // 2) for kk in range((F + 3) // 4)) * 512 // 128
-WINDOW_FRAMES = 1048576                                      # grouped full-LL frame window (align_grouped.cu)
+WINDOW_FRAMES = 131072                                       # grouped full-LL frame window (align_grouped.cu)
 
 
 def f16_peak():
