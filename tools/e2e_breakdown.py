@@ -25,7 +25,7 @@ tm("diag device_table", lambda: dm.device_table())
 tm("full device_table", lambda: fm.device_table())
 dt, ft = dm.device_table(), fm.device_table()
 tm("H2D 2.4 GB pinned", lambda: host.to("cuda", non_blocking=True))
-for ch in (1 << 18, 3 << 17, 1 << 19):
+for ch in (1 << 19, 3 << 18, 1 << 20):
     tm(f"align_host chunk {ch}", lambda: _device.align_host(host, dt, ft, 20, 0.025, chunk=ch))
 tm("align_frames (public)", lambda: pkg.align_frames(dm, fm, host, top_k=20, prune=0.025))
 import cProfile, pstats
