@@ -821,8 +821,8 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
     const unsigned cl_mask = __ballot_sync(0xffffffffu, clustered);
     if (cl_mask) {
       int cntb = 0;
-      const int hi = 32 - __clz(cl_mask);
-      for (int j = __ffs(cl_mask) - 1; j < hi; j++) {
+      for (unsigned m = cl_mask; m; m &= m - 1u) {  // clustered lanes only (warp-uniform mask)
+        const int j = __ffs(m) - 1;
         const double ov = __shfl_sync(0xffffffffu, ev, j);
         const int oc = __shfl_sync(0xffffffffu, c, j);
         if (clustered && j >= st && j < en && j != lane && better(ov, oc, ev, c)) cntb++;
