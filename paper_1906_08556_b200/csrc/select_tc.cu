@@ -587,60 +587,170 @@ __global__ void __launch_bounds__(NT, 1)
 // One CTA per flagged frame (list written by select_tc_kernel): every thread scores C/256
 // components in FP64, the CTA keeps the scores in shared memory and extracts the stable top-K by K
 // rounds of a block arg-best.
+__device__ __forceinline__ void warp_exact_score2(double x0, double x1, const double* __restrict__ r0,
+                                                  const double* __restrict__ r1, int F, int lane, double& s0,
+                                                  double& s1) {
+  double p = 0.0, q = 0.0;
+  if (lane < F) {
+    p = x0 * fma(__ldg(r0 + lane), x0, __ldg(r0 + F + lane));
+    q = x0 * fma(__ldg(r1 + lane), x0, __ldg(r1 + F + lane));
+  }
+  if (lane + 32 < F) {
+    p = fma(x1, fma(__ldg(r0 + lane + 32), x1, __ldg(r0 + F + lane + 32)), p);
+    q = fma(x1, fma(__ldg(r1 + lane + 32), x1, __ldg(r1 + F + lane + 32)), q);
+  }
+  if (lane == 0) {
+    p += __ldg(r0 + 2 * F);
+    q += __ldg(r1 + 2 * F);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    p += __shfl_xor_sync(0xffffffffu, p, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+  s0 = p;
+  s1 = q;
+}
+
 constexpr int XT_THREADS = 256;
+constexpr int XT_WARPS = XT_THREADS / 32;
+
+// Warp arg-best over the values owned by the lanes (lane l owns entries l, l + 32, ... of `vals` /
+// `idx`, `cnt` entries in all); K rounds, the winner lane clears its entry (stable rule: larger value
+// first, NaN last, lower index on ties).  Writes the K winners to (ov, oi).  cnt <= 32 * 64.
+__device__ __forceinline__ void warp_topk(const double* vals, const int* idx, int cnt, int K, int lane, double* ov,
+                                          int* oi) {
+  uint64_t taken = 0;
+  auto lane_best = [&](double& bv, int& bi, int& bj) {
+    bv = NAN;
+    bi = 0x7fffffff;
+    bj = -1;
+    for (int j = 0; lane + 32 * j < cnt; j++) {
+      const int e = lane + 32 * j;
+      if (!((taken >> j) & 1ull) && better(vals[e], idx[e], bv, bi)) {
+        bv = vals[e];
+        bi = idx[e];
+        bj = j;
+      }
+    }
+  };
+  double mv;
+  int mi, mj;
+  lane_best(mv, mi, mj);
+  for (int k = 0; k < K; k++) {
+    double bv = mv;
+    int bi = mi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(v2, i2, bv, bi)) {
+        bv = v2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      ov[k] = bv;
+      oi[k] = bi;
+    }
+    if (mj >= 0 && mi == bi) {  // this lane held the winner: drop it, rescan
+      taken |= 1ull << mj;
+      lane_best(mv, mi, mj);
+    }
+  }
+}
+
+// One CTA per flagged frame (list written by select_post_kernel): every thread scores C/256 components
+// in FP64 into shared memory; each warp takes the stable top-K of its 1/8 of the components (warp
+// arg-best rounds, no block barriers), then warp 0 merges the 8 lists.
 template <typename XT>
 __global__ void __launch_bounds__(XT_THREADS) select_exact_kernel(const XT* __restrict__ x, int F, int C, int K,
                                                                   const double* __restrict__ exact,
                                                                   const int* __restrict__ flagged,
                                                                   int32_t* __restrict__ sel_out,
                                                                   double* __restrict__ val_out) {
-  extern __shared__ double sc[];  // [C] scores, then [ceil(C/32)] taken bits
-  unsigned* taken = reinterpret_cast<unsigned*>(sc + C);
-  __shared__ double rv[XT_THREADS / 32];
-  __shared__ int ri[XT_THREADS / 32];
+  extern __shared__ double sc[];  // [C] scores
+  __shared__ double lv[XT_WARPS * 32];
+  __shared__ int li[XT_WARPS * 32];
+  __shared__ double fv[32];
+  __shared__ int fi[32];
   const int n = flagged[0];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per_w = (C + XT_WARPS - 1) / XT_WARPS;  // components of each warp: [warp*per_w, +per_w)
   for (int f = blockIdx.x; f < n; f += gridDim.x) {
     const int64_t t = flagged[1 + f];
     const XT* xr = x + t * F;
-    for (int c = tid; c < C; c += XT_THREADS) sc[c] = exact_score(xr, exact + (int64_t)c * (2 * F + 2), F);
-    for (int i = tid; i < (C + 31) / 32; i += XT_THREADS) taken[i] = 0u;
-    __syncthreads();
-    for (int k = 0; k < K; k++) {
-      double bv = NAN;
-      int bi = 0x7fffffff;
-      for (int c = tid; c < C; c += XT_THREADS) {
-        const double v = sc[c];
-        if (!((taken[c >> 5] >> (c & 31)) & 1u) && better(v, c, bv, bi)) {
-          bv = v;
-          bi = c;
+    const int c0 = warp * per_w, cnt = max(0, min(per_w, C - c0));
+    {  // scores of this warp's slice: two components per step, lanes over the F terms (coalesced rows)
+      const double x0 = lane < F ? (double)xr[lane] : 0.0, x1 = lane + 32 < F ? (double)xr[lane + 32] : 0.0;
+      for (int e = 0; e < cnt; e += 2) {
+        const int ca = c0 + e, cb = c0 + min(e + 1, cnt - 1);
+        double sa, sb;
+        warp_exact_score2(x0, x1, exact + (int64_t)ca * (2 * F + 2), exact + (int64_t)cb * (2 * F + 2), F, lane, sa,
+                          sb);
+        if (lane == 0) {
+          sc[ca] = sa;
+          sc[cb] = sb;
         }
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (better(ov, oi, bv, bi)) {
-          bv = ov;
-          bi = oi;
-        }
-      }
-      if (lane == 0) {
-        rv[warp] = bv;
-        ri[warp] = bi;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        for (int w = 1; w < XT_THREADS / 32; w++)
-          if (better(rv[w], ri[w], bv, bi)) {
-            bv = rv[w];
-            bi = ri[w];
-          }
-        sel_out[t * K + k] = bi;
-        if (val_out) val_out[t * K + k] = bv;
-        taken[bi >> 5] |= 1u << (bi & 31);
-      }
-      __syncthreads();
+      __syncwarp();
     }
+    {  // per-warp stable top-K over its contiguous slice (indices = component ids)
+      // entries are (sc[c0 + e], c0 + e); lane l owns e = l, l + 32, ...
+      uint64_t taken = 0;
+      auto lane_best = [&](double& bv, int& bi, int& bj) {
+        bv = NAN;
+        bi = 0x7fffffff;
+        bj = -1;
+        for (int j = 0; lane + 32 * j < cnt; j++) {
+          const int c = c0 + lane + 32 * j;
+          if (!((taken >> j) & 1ull) && better(sc[c], c, bv, bi)) {
+            bv = sc[c];
+            bi = c;
+            bj = j;
+          }
+        }
+      };
+      double mv;
+      int mi, mj;
+      lane_best(mv, mi, mj);
+      const int kk = min(K, cnt);
+      for (int k = 0; k < kk; k++) {
+        double bv = mv;
+        int bi = mi;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (better(v2, i2, bv, bi)) {
+            bv = v2;
+            bi = i2;
+          }
+        }
+        if (lane == 0) {
+          lv[warp * 32 + k] = bv;
+          li[warp * 32 + k] = bi;
+        }
+        if (mj >= 0 && mi == bi) {
+          taken |= 1ull << mj;
+          lane_best(mv, mi, mj);
+        }
+      }
+      for (int k = kk + lane; k < 32; k += 32) {  // unused slots never win
+        lv[warp * 32 + k] = NAN;
+        li[warp * 32 + k] = 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      warp_topk(lv, li, XT_WARPS * 32, K, lane, fv, fi);
+      __syncwarp();
+      for (int k = lane; k < K; k += 32) {
+        sel_out[t * K + k] = fi[k];
+        if (val_out) val_out[t * K + k] = fv[k];
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -688,31 +798,6 @@ __device__ __forceinline__ void warp_sort_desc(uint64_t (&k)[2], int lane) {
       }
     }
   }
-}
-
-__device__ __forceinline__ void warp_exact_score2(double x0, double x1, const double* __restrict__ r0,
-                                                  const double* __restrict__ r1, int F, int lane, double& s0,
-                                                  double& s1) {
-  double p = 0.0, q = 0.0;
-  if (lane < F) {
-    p = x0 * fma(__ldg(r0 + lane), x0, __ldg(r0 + F + lane));
-    q = x0 * fma(__ldg(r1 + lane), x0, __ldg(r1 + F + lane));
-  }
-  if (lane + 32 < F) {
-    p = fma(x1, fma(__ldg(r0 + lane + 32), x1, __ldg(r0 + F + lane + 32)), p);
-    q = fma(x1, fma(__ldg(r1 + lane + 32), x1, __ldg(r1 + F + lane + 32)), q);
-  }
-  if (lane == 0) {
-    p += __ldg(r0 + 2 * F);
-    q += __ldg(r1 + 2 * F);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    p += __shfl_xor_sync(0xffffffffu, p, o);
-    q += __shfl_xor_sync(0xffffffffu, q, o);
-  }
-  s0 = p;
-  s1 = q;
 }
 
 template <typename XT>
@@ -950,9 +1035,9 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
     cudaFreeAsync(scratch, st);
     return TVK_OK;
   }
-  const size_t xsm = sizeof(double) * C + sizeof(unsigned) * ((C + 31) / 32);
+  const size_t xsm = sizeof(double) * C;
   cudaFuncSetAttribute(stc::select_exact_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
-  stc::select_exact_kernel<XT><<<num_sms() * 2, stc::XT_THREADS, xsm, st>>>(x, F, C, K, (const double*)(base + L.exact),
+  stc::select_exact_kernel<XT><<<num_sms() * 8, stc::XT_THREADS, xsm, st>>>(x, F, C, K, (const double*)(base + L.exact),
                                                                              flagged, sel, val);
   TVK_CHECK_LAUNCH("select_exact");
   cudaFreeAsync(scratch, st);
