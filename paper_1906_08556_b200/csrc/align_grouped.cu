@@ -15,6 +15,8 @@
 // bit-reproducible although the bucket order is not.
 #include <math.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "internal.h"
 #include "spd_small.cuh"
@@ -343,22 +345,16 @@ int64_t grouped_workspace_bytes(int64_t n_pairs, int C) {
   return n_pairs > kGroupWindowFrames ? 2 * one : one;  // two windows in flight (see grouped_full_ll)
 }
 
-// Second stream + fork/join events of the window pipeline, one set per device.
-struct WindowStreams {
-  cudaStream_t s2 = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-static WindowStreams& window_streams() {
-  static WindowStreams ws[64];
+// Second stream of the window pipeline, one per device (fork/join events are per call, so concurrent
+// host threads cannot cross their dependencies).
+static cudaStream_t window_stream() {
+  static cudaStream_t s2[64] = {};
+  static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
-  WindowStreams& w = ws[dev & 63];
-  if (!w.s2) {
-    cudaStreamCreateWithFlags(&w.s2, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&w.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&w.join, cudaEventDisableTiming);
-  }
-  return w;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!s2[dev & 63]) cudaStreamCreateWithFlags(&s2[dev & 63], cudaStreamNonBlocking);
+  return s2[dev & 63];
 }
 
 template <typename XT, bool VEC>
@@ -413,32 +409,39 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool vec = ((F * sizeof(XT)) % 16 == 0) && ((uintptr_t)x % 16 == 0);
-  WindowStreams* ws2 = nullptr;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   if (nwin > 1) {
-    ws2 = &window_streams();
-    cudaEventRecord(ws2->fork, st);
-    cudaStreamWaitEvent(ws2->s2, ws2->fork, 0);
+    s2 = window_stream();
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    cudaEventRecord(fork, st);
+    cudaStreamWaitEvent(s2, fork, 0);
   }
+  int rc = TVK_OK;
   for (int i = 0; i < nwin; i++) {
     const int64_t f0 = (int64_t)i * win;
     const int64_t nf = std::min<int64_t>(win, T - f0);
     const int64_t np = nf * K;
     const int32_t* wsel = sel + f0 * K;
-    cudaStream_t s = (i & 1) ? ws2->s2 : st;
+    cudaStream_t s = (i & 1) ? s2 : st;
     const GroupWs& wi = w[i & 1];
-    TVK_TRY(sort_tiles(wsel, nullptr, np, C, wi, s));
+    rc = sort_tiles(wsel, nullptr, np, C, wi, s);
+    if (rc != TVK_OK) break;
     // the kernel reads the tile count from tile_start[C]
     GroupWs wc = wi;
     wc.tile_start = wi.tile_start + C;
-    if (vec)
-      TVK_TRY((launch_whiten<XT, true>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s)));
-    else
-      TVK_TRY((launch_whiten<XT, false>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s)));
+    rc = vec ? launch_whiten<XT, true>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s)
+             : launch_whiten<XT, false>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s);
+    if (rc != TVK_OK) break;
   }
-  if (ws2) {
-    cudaEventRecord(ws2->join, ws2->s2);
-    cudaStreamWaitEvent(st, ws2->join, 0);
+  if (s2) {  // always join, also after an error
+    cudaEventRecord(join, s2);
+    cudaStreamWaitEvent(st, join, 0);
+    cudaEventDestroy(fork);  // released once the recorded work completes
+    cudaEventDestroy(join);
   }
+  if (rc != TVK_OK) return rc;
   TVK_CHECK_LAUNCH("grouped windows");
   return TVK_OK;
 }
