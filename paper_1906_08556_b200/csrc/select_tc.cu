@@ -53,6 +53,7 @@ constexpr int NT = 128 + NEPI;
 constexpr int CAP = 24;        // candidate buffer entries per (frame, half)
 constexpr float KAPPA = 1.0f / 65536.0f;  // 3xTF32 bound: 28x the max observed error
 constexpr float KAPPA1 = 1.0f / 4096.0f;   // pass-0 slack (heuristic: the window check below is exact)
+constexpr int kPass0Pieces = 4;  // A feature pieces of the next tile built between pass-0 pairs (rest: pass 1)
 constexpr int MAX_F = 63;      // A hi/lo (2F+1 f16, padded to 16, two per column) in TMEM columns 256-383
 
 __host__ __device__ inline int kp(int F) { return (2 * F + 1 + 15) / 16 * 16; }  // [x^2, x, 1], padded to K=16
@@ -448,6 +449,19 @@ __global__ void __launch_bounds__(NT, 1)
       const float m = kappa * S * inv, m2 = 2.0f * m;  // in score units of the tile (2^E)
       const bool live = t < T && isfinite(S);  // rows past T (and non-finite frames) take nothing
 
+      // A operand of the next tile into the other TMEM A buffer (its last reader, tile li-1, is
+      // done), built between the pass-0 chunk pairs, where the epilogue mostly waits for the MMAs:
+      // scales after pair 1 (the frames copied at the tile start have landed by then), one feature
+      // piece after each later pair
+      float S_next = 0.0f, inv_next = 1.0f;
+      const bool has_next = it + 1 < iters;
+      auto prep_next = [&]() {
+        if (li >= 1) tc::mbar_wait(&aempty[(li + 1) & 1], ((li - 1) >> 1) & 1);
+        const Prep pn = prep_A(tile + gridDim.x);
+        inv_next = pn.inv;
+        S_next = pn.S;
+      };
+      const int npair = NCH / 2;
       // ---- pass 0 (1xTF32): K-th largest of the group maxima, a lower bound of the K-th exact score
       float top[NK];
 #pragma unroll
@@ -486,7 +500,12 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
         }
+        if (has_next && p == 1) prep_next();
+        if (has_next && p >= 2 && p - 2 < kPass0Pieces && debug != 13) piece_A(tile + gridDim.x, li + 1, inv_next, p - 2);
       }
+      // feature pieces not built in pass 0 (few pairs) are built in pass 1 together with the rest
+      const int pc0 = has_next ? (npair <= 1 ? 0 : min(kPass0Pieces, npair - 2)) : 8;
+      if (has_next && npair <= 1) prep_next();
       mark(it, 1);
 
       // union of both halves' lists: half 1 publishes, half 0 merges and publishes the threshold
@@ -508,16 +527,6 @@ __global__ void __launch_bounds__(NT, 1)
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
       const float thr = live ? kth1[r] : INFINITY;
       mark(it, 2);
-      // A operand of the next tile into the other TMEM A buffer (its last reader, tile li-1, is
-      // done): scales now, the feature pieces between the pass-1 chunks below
-      float S_next = 0.0f, inv_next = 1.0f;
-      const bool has_next = it + 1 < iters;
-      auto prep_next = [&]() {
-        if (li >= 1) tc::mbar_wait(&aempty[(li + 1) & 1], ((li - 1) >> 1) & 1);
-        const Prep pn = prep_A(tile + gridDim.x);
-        inv_next = pn.inv;
-        S_next = pn.S;
-      };
       mark(it, 3);
 
       // ---- pass 1 (3xTF32): collect every score >= thr
@@ -551,11 +560,10 @@ __global__ void __launch_bounds__(NT, 1)
             cnt += v[u] >= thr ? 1 : 0;
           }
         }
-        if (has_next && n == 0) prep_next();
-        if (has_next && n >= 1 && n <= 8 && debug != 13) piece_A(tile + gridDim.x, li + 1, inv_next, n - 1);
+        if (n >= 1 && pc0 + (n - 1) < 8) piece_A(tile + gridDim.x, li + 1, inv_next, pc0 + n - 1);
       }
       if (has_next) {
-        for (int pc = NCH > 1 ? NCH - 1 : 0; pc < 8; pc++) piece_A(tile + gridDim.x, li + 1, inv_next, pc);
+        for (int pc = pc0 + (NCH > 1 ? NCH - 1 : 0); pc < 8; pc++) piece_A(tile + gridDim.x, li + 1, inv_next, pc);
         finish_A(li + 1);
       }
 
