@@ -216,8 +216,11 @@ def bench_ours(args):
     import torch.distributed as dist
     rank, world, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -348,6 +351,7 @@ def bench_ours(args):
     # e2e through the public API: pinned host frames -> align_frames -> host SparseAlignment
     host = torch.empty((n, F), dtype=torch.float32, pin_memory=True)
     host.copy_(x)
+    xs_check = x[:max(0, min(n, args.exact_frames))].clone()
     del x, ws, comps, wts
     torch.cuda.empty_cache()
     e2e_steps = max(1, min(args.steps, 3))
@@ -364,9 +368,34 @@ def bench_ours(args):
     del host, ali
 
     log("[bench] e2e done")
-    em = None
-    if args.em_utts > 0:
-        em = bench_em(args, pkg, dev, rank, world, barrier, max_over_ranks)
+    exact = selection_exactness(xs_check, dtab, args.exact_frames, pkg) if args.exact_frames > 0 else None
+    del xs_check
+    torch.cuda.empty_cache()
+    em = c5 = c4 = None
+    if args.em_utts > 0:  # config 3: augmented, min-div + Sigma update, no realignment
+        em, _ = bench_em_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, "augmented", args.em_utts,
+                             args.em_steps, args.em_warmup,
+                             dict(iterations=10 ** 6, min_div=True, sigma_update=True, realign_interval=0),
+                             "config 3: augmented (Kaldi) TVM, C=2048, F=60, R=400, min-div + Sigma update")
+        log(f"[bench] config 3 EM: {em['value']:.3f} s/iter")
+    if args.c5_utts > 0:  # config 5: standard, min-div + UBM-mean update + realignment every iteration
+        c5, _ = bench_em_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, "standard", args.c5_utts,
+                             args.em_steps, args.em_warmup,
+                             dict(iterations=10 ** 6, min_div=True, sigma_update=False, update_mean=True,
+                                  realign_interval=1),
+                             "config 5 training: standard TVM, C=2048, F=60, R=400, min-div + UBM-mean (bias) "
+                             "update + realignment of every frame each iteration", profile_kernels=False)
+        log(f"[bench] config 5 EM: {c5['value']:.3f} s/iter")
+        if args.extract_utts > 0:
+            c5["extraction"] = bench_extract_leg(args, pkg, dev, rank, world, barrier, max_over_ranks,
+                                                 args.extract_utts)
+            log(f"[bench] config 5 extraction: {c5['extraction']['value']:.0f} utts/s")
+    if args.config4_utts > 0:  # config 4: VoxCeleb scale (opt-in: ~1 min per iteration on one GPU)
+        c4, _ = bench_em_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, "augmented", args.config4_utts,
+                             1, 0, dict(iterations=10 ** 6, min_div=True, sigma_update=True, realign_interval=0),
+                             "config 4: VoxCeleb-scale augmented TVM, C=2048, F=60, R=400, min-div + residual "
+                             "covariance update", profile_kernels=False)
+        log(f"[bench] config 4 EM: {c4['value']:.3f} s/iter")
 
     if rank == 0:
         line = {
@@ -409,80 +438,341 @@ def bench_ours(args):
             "dense_variant": dense,
             "clocks": clk,
         }
-        if em is not None:
-            line["em_iteration"] = em
+        line["selection_exactness"] = exact
         if not args.no_cpu:
             try:
                 line["cpu_baseline"] = cpu_baseline_sample(args.cpu_frames)
             except Exception as exc:  # never let the reported baseline kill the bench line
                 line["cpu_baseline"] = {"error": str(exc)}
+            log("[bench] cpu baselines")
+            for leg, fn in ((em, em_cpu_baseline), (c5, extract_cpu_baseline)):
+                if leg is None or world > 1:
+                    continue
+                try:
+                    cb = fn()
+                    tgt = leg if fn is em_cpu_baseline else leg.get("extraction")
+                    if tgt is not None:
+                        tgt["cpu_baseline"] = cb
+                        tgt["vs_cpu"] = (cb["value"] / tgt["value"]) if fn is em_cpu_baseline else \
+                            (tgt["value"] / cb["value"])
+                except Exception as exc:
+                    (leg if fn is em_cpu_baseline else leg.setdefault("extraction", {}))["cpu_baseline"] = \
+                        {"error": str(exc)}
+        if em is not None:
+            line["em_iteration"] = em
+        if c5 is not None:
+            line["config5"] = c5
+        if c4 is not None:
+            line["config4"] = c4
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def bench_em(args, pkg, dev, rank, world, barrier, max_over_ranks):
-    """Seconds per EM iteration, augmented formulation, 2048 x 60, R=400 (config 3 shape)."""
-    import torch
-    from paper_1906_08556_b200 import _estep, _lib, pipeline as P
-    D, p = 400, 100.0
-    n_utt, n_fr = args.em_utts, 300
-    rng = np.random.default_rng(7)
+# ------------------------------------------------------------------------------ EM legs (configs 3-5)
+
+D_TVM, P_OFF, FR_UTT = 400, 100.0, 300
+FLOP_EM_UTT = 2 * C * D_TVM * (D_TVM + 1) + 4 * C * F * D_TVM + D_TVM ** 3   # 917.6 MFLOP
+FLOP_EM_GEMM_UTT = 2 * C * D_TVM * (D_TVM + 1) + 4 * C * F * D_TVM          # L, A (2CP each), b, B (2CFD each)
+# per-iteration fixed GEMM work: workspace W (2CF^2D) + U (CF D(D+1)), Sigma update T B' (2CF^2D), T.R (2CFD^2)
+FLOP_EM_GEMM_FIXED = 2 * C * F * F * D_TVM + C * F * D_TVM * (D_TVM + 1) + 2 * C * F * F * D_TVM \
+    + 2 * C * F * D_TVM * D_TVM
+FLOP_EXTRACT_UTT = C * D_TVM * (D_TVM + 1) + 2 * C * F * D_TVM + D_TVM ** 3 // 3  # L + b + Cholesky
+
+
+def generator(form, seed=7):
+    """synth.py:90-104 recipe at C=2048, F=60, R=400 (host, numpy): w ~ Dir(10), mu ~ N(0, 8^2),
+    Sigma = A A'/2F + 0.5 I, T ~ N(0, 1); augmented: T[:, :, 0] = mu / p; standard: bias = mu."""
+    rng = np.random.default_rng(seed)
     w = rng.dirichlet(np.full(C, 10.0))
     mu = rng.normal(0.0, 8.0, (C, F))
     a = rng.normal(0.0, 1.0, (C, F, 2 * F))
     sig = np.einsum("cik,cjk->cij", a, a) / (2 * F) + 0.5 * np.eye(F)
-    Tg = rng.normal(0.0, 1.0, (C, F, D))
-    Tg[:, :, 0] = mu / p
-    gen = pkg.TvModel("augmented", Tg, sig, w, mu, None, p)
-    # utterances: latent z = p e1 + N(0, I); frames x = T_c z + Sigma_c^(1/2) e (generated on device)
-    g = torch.Generator(device=dev).manual_seed(11 + rank)
-    Td = torch.from_numpy(Tg).to(dev).view(C * F, D)
-    L = torch.linalg.cholesky(torch.from_numpy(sig).to(dev))
-    z = torch.randn((n_utt, D), dtype=torch.float64, device=dev, generator=g)
-    z[:, 0] += p
-    comp = torch.multinomial(torch.from_numpy(w).to(dev), n_utt * n_fr, replacement=True, generator=g)
-    x = torch.empty((n_utt * n_fr, F), dtype=torch.float32, device=dev)
+    Tg = rng.normal(0.0, 1.0, (C, F, D_TVM))
+    if form == "augmented":
+        Tg[:, :, 0] = mu / P_OFF
+    return dict(w=w, mu=mu, sig=sig, T=Tg, form=form)
+
+
+def device_utterances(gen, n_utt, seed, dev):
+    """n_utt synthetic utterances x 300 frames drawn on the device from the generator (synth.py:107-147
+    recipe: augmented x = T_c z + Sigma_c^(1/2) e with z = p e1 + N(0, I); standard x = mu_c + T_c w + ...)."""
+    import torch
+    g = torch.Generator(device=dev).manual_seed(seed)
+    Td = torch.from_numpy(gen["T"]).to(dev).view(C * F, D_TVM)
+    L = torch.linalg.cholesky(torch.from_numpy(gen["sig"]).to(dev))
+    mu = torch.from_numpy(gen["mu"]).to(dev)
+    x = torch.empty((n_utt * FR_UTT, F), dtype=torch.float32, device=dev)
+    wt = torch.from_numpy(gen["w"]).to(dev)
     for u0 in range(0, n_utt, 64):
         u1 = min(n_utt, u0 + 64)
-        M = (Td @ z[u0:u1].T).T.reshape(u1 - u0, C, F)  # mean supervectors
-        cu = comp[u0 * n_fr:u1 * n_fr].view(u1 - u0, n_fr)
+        z = torch.randn((u1 - u0, D_TVM), dtype=torch.float64, device=dev, generator=g)
+        if gen["form"] == "augmented":
+            z[:, 0] += P_OFF
+        M = (Td @ z.T).T.reshape(u1 - u0, C, F)  # latent-shifted mean supervectors
+        if gen["form"] == "standard":
+            M += mu
+        cu = torch.multinomial(wt, (u1 - u0) * FR_UTT, replacement=True, generator=g).view(u1 - u0, FR_UTT)
         means = torch.gather(M, 1, cu[:, :, None].expand(-1, -1, F))
-        e = torch.randn((u1 - u0, n_fr, F), dtype=torch.float64, device=dev, generator=g)
-        noise = torch.einsum("utij,utj->uti", L[cu], e)
-        x[u0 * n_fr:u1 * n_fr] = (means + noise).reshape(-1, F).to(torch.float32)
-    del Td, M, means, noise, e
-    ids = [f"u{rank:02d}_{i:07d}" for i in range(n_utt)]
-    corpus = P.DeviceCorpus.from_device(x, np.arange(0, (n_utt + 1) * n_fr, n_fr), ids)
-    ubm_full = gen.alignment_ubm_full()
-    ubm_diag = gen.alignment_ubm_diag()
-    model = pkg.init_model(ubm_full, D, "augmented", seed=0, prior_offset=p)
-    cfg = P.TrainConfig(formulation="augmented", latent_dim=D, iterations=10 ** 6, min_div=True,
-                        sigma_update=True, top_k=K_TOP, prune=PRUNE, seeds=(0,))
-    tr = P.DeviceTrainer(model, corpus, cfg)
+        e = torch.randn((u1 - u0, FR_UTT, F), dtype=torch.float64, device=dev, generator=g)
+        x[u0 * FR_UTT:u1 * FR_UTT] = (means + torch.einsum("utij,utj->uti", L[cu], e)).reshape(-1, F).float()
+    return x
+
+
+def em_setup(pkg, gen, n_local, rank, dev, cfg_kw, first_utt=0):
+    """(trainer, align_diag, align_cov, store) for this rank's utterances [first_utt, first_utt + n_local)."""
+    from paper_1906_08556_b200 import pipeline as P
+    x = device_utterances(gen, n_local, 11 + rank, dev)
+    ids = [f"u{first_utt + i:08d}" for i in range(n_local)]
+    store = P.DeviceFeatureStore(x, np.arange(0, (n_local + 1) * FR_UTT, FR_UTT), ids)
+    T, Sg, form = gen["T"], gen["sig"], gen["form"]
+    bias = gen["mu"] if form == "standard" else None
+    genm = pkg.TvModel(form, T, Sg, gen["w"], gen["mu"], bias, P_OFF if form == "augmented" else 0.0)
+    ubm_full, ubm_diag = genm.alignment_ubm_full(), genm.alignment_ubm_diag()
+    model = pkg.init_model(ubm_full, D_TVM, form, seed=0, prior_offset=P_OFF)
+    cfg = P.TrainConfig(formulation=form, latent_dim=D_TVM, top_k=K_TOP, prune=PRUNE, seeds=(0,), **cfg_kw)
+    tr = P.DeviceTrainer(model, store.device_corpus(ids), cfg)
+    return tr, ubm_diag.copy(), ubm_full.covariances, store, model
+
+
+def em_kernel_breakdown(tr, it, align_diag, align_cov):
+    """One extra EM iteration under the torch profiler (CUPTI kernel timestamps; outside every timed
+    region): device time per kernel, and the achieved rate of the dominant kernel (gemm_kernel)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        if tr.alignment is None:
+            tr.align(align_diag, align_cov)
+        tr.iteration()
+        tr.realign_point(it, align_diag)
+        torch.cuda.synchronize()
+    ev = [e for e in prof.key_averages() if e.self_device_time_total > 0]
+    tot = sum(e.self_device_time_total for e in ev) / 1e6
+    kern = {}
+    for e in ev:
+        name = e.key.split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
+        k = kern.setdefault(name, [0.0, 0])
+        k[0] += e.self_device_time_total / 1e6
+        k[1] += e.count
+    top = sorted(kern.items(), key=lambda kv: -kv[1][0])[:8]
+    return tot, {n: {"s": round(v[0], 5), "share": round(v[0] / tot, 4), "launches": v[1]} for n, v in top}
+
+
+def bench_em_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, form, n_global, steps, warmup, cfg_kw,
+                 label, profile_kernels=True):
+    """Seconds per EM iteration on n_global utterances sharded over the ranks (strong scaling): each
+    timed iteration = E-step over the corpus (BW stats, posteriors, accumulators) + one all-reduce +
+    M-step (update_T, update_sigma, min-divergence), plus realignment of every frame where the config
+    asks for it (CUDA events on the launching stream, max over ranks)."""
+    import torch
+    from paper_1906_08556_b200 import _dist
+    lo, hi = _dist.shard_range(n_global, rank, world)
+    gen = generator(form)
+    tr, align_diag, align_cov, store, model = em_setup(pkg, gen, hi - lo, rank, dev, cfg_kw, first_utt=lo)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    tr.align(ubm_diag, ubm_full.covariances)
+    tr.align(align_diag, align_cov)
     barrier()
     align_s = max_over_ranks(time.perf_counter() - t0)
-    for _ in range(args.em_warmup):
-        tr.iteration()
+    it = 0
+
+    def one():
+        nonlocal it
+        it += 1
+        if tr.alignment is None:
+            tr.align(align_diag, align_cov)
+        a = tr.iteration()
+        tr.realign_point(it, align_diag)
+        return a
+
+    for _ in range(warmup):
+        one()
     barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    auxes = []
-    for _ in range(args.em_steps):
-        auxes.append(tr.iteration())
+    auxes = [one() for _ in range(steps)]
     e1.record(stream)
     barrier()
-    sec = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.em_steps)
-    flop_utt = C * D * (D + 1) * 2 + 4 * C * F * D + D ** 3
-    return {"value": sec, "unit": "s/iter", "higher_is_better": False, "utts_per_gpu": n_utt,
-            "frames_per_utt": n_fr, "global_utts": world * n_utt, "steps": args.em_steps,
-            "warmup": args.em_warmup, "alignment_s": align_s,
-            "config": "augmented TVM, C=2048, F=60, R=400, min-div + Sigma update, realign 0 (config 3 shape)",
-            "achieved_tflops": world * n_utt * flop_utt / sec / 1e12, "aux_last": auxes[-1]}
+    sec = max_over_ranks(e0.elapsed_time(e1) / 1e3 / steps)
+    out = {"value": sec, "unit": "s/iter", "higher_is_better": False, "global_utts": n_global,
+           "utts_per_gpu": hi - lo, "frames_per_utt": FR_UTT, "steps": steps, "warmup": warmup,
+           "scaling": "strong", "alignment_s": align_s, "config": label,
+           "achieved_tflops": n_global * FLOP_EM_UTT / sec / 1e12, "flop_per_utt": FLOP_EM_UTT,
+           "aux_last": auxes[-1]}
+    if profile_kernels and rank == 0:
+        tot, kern = em_kernel_breakdown(tr, it + 1, align_diag, align_cov)
+        g = kern.get("gemm_kernel")
+        peak, src = fp64_peak()
+        if g:
+            gflop = (hi - lo) * FLOP_EM_GEMM_UTT + FLOP_EM_GEMM_FIXED
+            ach = gflop / g["s"] / 1e12
+            out["roofline"] = {"bound": "tensor", "kernel": "gemm_kernel (FP64 DMMA: L = N U, b = F W, A += N'M, "
+                                                            "B += F'phi, workspace, T B', T R)",
+                               "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                               "peak_source": src, "flop_per_iter": gflop, "kernel_s_per_iter": g["s"],
+                               "share_of_kernel_time": g["share"],
+                               "method": "torch.profiler (CUPTI) kernel durations of one extra iteration"}
+        out["kernel_breakdown"] = {"kernel_s_per_iter": tot, "top": kern}
+    del tr, store
+    torch.cuda.empty_cache()
+    return out, model
+
+
+def bench_extract_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, n_global):
+    """Config 5 extraction: i-vectors of n_global fresh standard-formulation utterances through the
+    public extract_corpus (alignment with the predictive-covariance UBM, BW stats, posterior means),
+    frames resident in HBM (DeviceFeatureStore), embeddings returned to the host."""
+    import torch
+    from paper_1906_08556_b200 import _dist, pipeline as P
+    gen = generator("standard", seed=9)
+    lo, hi = _dist.shard_range(n_global, rank, world)
+    x = device_utterances(gen, hi - lo, 211 + rank, dev)
+    # each rank holds only its shard; extract_corpus shards the global id list the same way
+    all_ids = [f"e{i:08d}" for i in range(n_global)]
+    store = P.DeviceFeatureStore(x, np.arange(0, (hi - lo + 1) * FR_UTT, FR_UTT), all_ids[lo:hi], all_ids)
+    T, Sg = gen["T"], gen["sig"]
+    model = pkg.TvModel("standard", T, Sg, gen["w"], gen["mu"], gen["mu"].copy(), 0.0)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world == 1:  # warm-up on a slice (tables, allocator); a rank-sharded store has no such slice
+        P.extract_corpus(model, store, top_k=K_TOP, prune=PRUNE, ids=all_ids[:min(n_global, 2048)])
+    barrier()
+    e0.record(stream)
+    _, emb = P.extract_corpus(model, store, top_k=K_TOP, prune=PRUNE)
+    e1.record(stream)
+    barrier()
+    sec = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    ups = n_global / sec
+    ok = bool(np.all(np.isfinite(emb)))
+    del x, store
+    torch.cuda.empty_cache()
+    return {"value": ups, "unit": "utterances/s", "global_utts": n_global, "utts_per_gpu": hi - lo,
+            "seconds": sec, "x_realtime": ups * FR_UTT / 100.0, "scaling": "strong",
+            "achieved_tflops_posterior": n_global * FLOP_EXTRACT_UTT / sec / 1e12, "finite": ok,
+            "path": "pipeline extract (alignment + BW stats + posterior mean), frames in HBM, i-vectors to host"}
+
+
+def em_cpu_baseline(n_utts=6, comp_sample=128):
+    """The reference EM iteration on the host cores (oracle restatement of tvm.py/pipeline.py), timed on
+    a bounded sample and extrapolated per BASELINE.md §4: sec/iter = workspace + 20k x (BW stats +
+    posterior + accumulate per utterance) + per-batch accumulator merges + update_T + update_sigma +
+    min-div.  Per-component work (workspace, update_T, update_sigma) is timed on ``comp_sample``
+    components and scaled by C / comp_sample; the per-utterance work on ``n_utts`` utterances."""
+    from oracle import tvkit_oracle as orc
+    gen = generator("augmented")
+    rng = np.random.default_rng(5)
+    model = orc.make_model("augmented", rng.normal(0, 1, (C, F, D_TVM)), gen["sig"], gen["w"], gen["mu"], None,
+                           P_OFF)
+    model.T[:, :, 0] = gen["mu"] / P_OFF
+    gm = orc.make_model("augmented", gen["T"], gen["sig"], gen["w"], gen["mu"], None, P_OFF)
+    ids, feats, _ = orc.sample_utterances(gm, n_utts, 1, (FR_UTT, FR_UTT), 0.3, rng)
+    pc = orc.predictive_covariances(gm)
+    diag = (gen["w"], gen["mu"], np.ascontiguousarray(np.diagonal(pc, axis1=1, axis2=2)))
+    alis = [orc.align(diag, (gen["w"], gen["mu"], pc), feats[u], K_TOP, PRUNE) for u in ids]  # untimed
+    sub = orc.make_model("augmented", model.T[:comp_sample], model.Sigma[:comp_sample], gen["w"][:comp_sample],
+                         gen["mu"][:comp_sample], None, P_OFF)
+    t0 = time.perf_counter()
+    orc.workspace(sub)
+    t_ws = (time.perf_counter() - t0) * C / comp_sample
+    # full-size workspace arrays for the per-utterance timing (values do not change the work)
+    ws = orc.workspace(sub)
+    reps = -(-C // comp_sample)
+    ws.W = np.concatenate([ws.W] * reps)[:C]
+    ws.U = np.concatenate([ws.U] * reps)[:C]
+    ws.Sinv = np.concatenate([ws.Sinv] * reps)[:C]
+    ws.logdet = np.concatenate([ws.logdet] * reps)[:C]
+    t0 = time.perf_counter()
+    stats = [orc.bw_stats(feats[u], *alis[i], C) for i, u in enumerate(ids)]
+    acc = orc.accumulate(model, stats, ws)
+    t_utt = (time.perf_counter() - t0) / n_utts
+    other = orc.zero_acc(C, F, D_TVM)
+    t0 = time.perf_counter()
+    orc.merge_acc(other, acc)
+    t_merge = time.perf_counter() - t0  # once per batch of 8 utterances (pipeline.py:406-413)
+    suba = orc.zero_acc(comp_sample, F, D_TVM)
+    for k in ("A", "B", "N", "Ssum"):
+        setattr(suba, k, getattr(acc, k)[:comp_sample])
+    suba.U, suba.phi_sum, suba.moment_sum = acc.U, acc.phi_sum, acc.moment_sum
+    import warnings
+    t0 = time.perf_counter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        newT = orc.update_T(sub, suba)
+        orc.update_sigma(sub, suba, newT)
+    t_m = (time.perf_counter() - t0) * C / comp_sample
+    t0 = time.perf_counter()
+    tr = orc.min_div(acc, "augmented")
+    sub.T = sub.T.copy()
+    orc.apply_min_div(sub, tr, acc.phi_sum / acc.U)
+    t_md = (time.perf_counter() - t0) * C / comp_sample
+    n_glob = 20000
+    sec = t_ws + n_glob * t_utt + (n_glob / 8) * t_merge + t_m + t_md
+    return {"value": sec, "unit": "s/iter", "cores": len(os.sched_getaffinity(0)), "kind": "port",
+            "sample": f"{n_utts} utterances (BW stats + posterior + accumulate) and {comp_sample} of {C} components "
+                      f"(workspace, update_T, update_sigma, min-div) of the config-3 shape, oracle restatement of "
+                      f"tvkit (numpy/OpenBLAS, all host cores), extrapolated to 20k utterances per BASELINE.md §4",
+            "parts_s": {"workspace": t_ws, "per_utt": t_utt, "merge_per_batch_of_8": t_merge, "mstep": t_m,
+                        "min_div": t_md}}
+
+
+def extract_cpu_baseline(n_utts=3, comp_sample=128):
+    """Reference extraction per utterance on the host (align + BW stats + posterior mean) plus the
+    one-off workspace, extrapolated to 150k utterances."""
+    from oracle import tvkit_oracle as orc
+    gen = generator("standard", seed=9)
+    rng = np.random.default_rng(6)
+    gm = orc.make_model("standard", gen["T"], gen["sig"], gen["w"], gen["mu"], gen["mu"].copy(), 0.0)
+    ids, feats, _ = orc.sample_utterances(gm, n_utts, 1, (FR_UTT, FR_UTT), 0.3, rng)
+    sub = orc.make_model("standard", gm.T[:comp_sample], gm.Sigma[:comp_sample], gen["w"][:comp_sample],
+                         gen["mu"][:comp_sample], gen["mu"][:comp_sample].copy(), 0.0)
+    t0 = time.perf_counter()
+    ws = orc.workspace(sub)
+    t_ws = (time.perf_counter() - t0) * C / comp_sample
+    reps = -(-C // comp_sample)
+    for k in ("W", "U", "Sinv", "logdet"):
+        setattr(ws, k, np.concatenate([getattr(ws, k)] * reps)[:C])
+    pc = orc.predictive_covariances(gm)
+    diag = (gen["w"], gen["mu"], np.ascontiguousarray(np.diagonal(pc, axis1=1, axis2=2)))
+    t0 = time.perf_counter()
+    for u in ids:
+        off, comp, w = orc.align(diag, (gen["w"], gen["mu"], pc), feats[u], K_TOP, PRUNE)
+        n, f, S = orc.bw_stats(feats[u], off, comp, w, C, center=gm.bias)
+        orc.posterior(gm, n, f, S, ws)
+    t_utt = (time.perf_counter() - t0) / n_utts
+    n_glob = 150000
+    sec = t_ws + n_glob * t_utt
+    return {"value": n_glob / sec, "unit": "utterances/s", "cores": len(os.sched_getaffinity(0)), "kind": "port",
+            "sample": f"{n_utts} utterances (align + BW stats + posterior) and the workspace on {comp_sample} of "
+                      f"{C} components, oracle restatement of tvkit.extract_corpus, extrapolated to 150k utterances",
+            "parts_s": {"workspace": t_ws, "per_utt": t_utt}}
+
+
+def selection_exactness(x, dtab, n, pkg):
+    """tcgen05 3xFP16 preselection vs the FP64 DMMA kernel on n bench frames (identical indices
+    required), and vs the oracle's stable argsort on a 2000-frame sample (outside the timed region)."""
+    import torch
+    from paper_1906_08556_b200 import _lib
+    from oracle import tvkit_oracle as orc
+    n = min(n, x.shape[0])
+    out = {}
+    for mode in ("tc", "dmma"):
+        os.environ["TVK_SELECT"] = mode
+        sel = _lib.empty((n, K_TOP), torch.int32)
+        _lib.call("tvk_select_topk", _lib.ptr(x), 0, n, F, _lib.ptr(dtab.table), C, K_TOP, _lib.ptr(sel), None,
+                  _lib.stream())
+        out[mode] = sel
+    os.environ.pop("TVK_SELECT", None)
+    mism = int((out["tc"] != out["dmma"]).any(dim=1).sum().item())
+    w, mu, cov = make_ubm(0)
+    xs = x[:2000].double().cpu().numpy()
+    ll = orc.diag_loglik(w, mu, np.ascontiguousarray(np.diagonal(cov, axis1=1, axis2=2)), xs)
+    ref = np.argsort(-ll, axis=1, kind="stable")[:, :K_TOP]
+    omism = int((out["tc"][:2000].cpu().numpy() != ref).any(axis=1).sum())
+    return {"frames": n, "mismatched_frames_vs_fp64_dmma": mism, "oracle_sample_frames": 2000,
+            "mismatched_frames_vs_oracle_stable_argsort": omism,
+            "margin": "kappa = 2^-14 (proof: csrc/select_tc.cu header; DESIGN.md §2)"}
 
 
 def main():
@@ -492,9 +782,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=FRAMES_PER_GPU)
-    ap.add_argument("--em-utts", type=int, default=20000)
+    ap.add_argument("--em-utts", type=int, default=20000, help="config 3: utterances (global, sharded)")
     ap.add_argument("--em-steps", type=int, default=3)
     ap.add_argument("--em-warmup", type=int, default=1)
+    ap.add_argument("--c5-utts", type=int, default=20000, help="config 5 training utterances (global)")
+    ap.add_argument("--extract-utts", type=int, default=150000, help="config 5 extraction utterances (global)")
+    ap.add_argument("--config4-utts", type=int, default=0, help="config 4 (opt-in): 1100000 utterances")
+    ap.add_argument("--exact-frames", type=int, default=2_000_000,
+                    help="frames of the tcgen05-vs-FP64 preselection identity check")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (test: ranks may share a GPU)")
     ap.add_argument("--no-em", action="store_true")
     ap.add_argument("--dense-steps", type=int, default=1, help="steps of the dense quadratic-feature variant")
     ap.add_argument("--no-cpu", action="store_true")
@@ -502,7 +798,7 @@ def main():
     ap.add_argument("--ref-frames", type=int, default=2000)
     args = ap.parse_args()
     if args.no_em:
-        args.em_utts = 0
+        args.em_utts = args.c5_utts = args.extract_utts = args.config4_utts = 0
     if args.warmup < 3 and args.impl == "ours":
         log("note: fewer than 3 warm-up steps")
     if args.impl == "reference":

@@ -209,6 +209,10 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
         st = slots[slot]
         with torch.cuda.stream(drain_stream):
             drain_stream.wait_event(done)
+            # the piece's outputs were allocated on the compute stream: keep the caching allocator
+            # from handing their memory to a later piece until these copies have run
+            for t in (res.offsets, res.components, res.weights):
+                t.record_stream(drain_stream)
             st[0][:n + 1].copy_(res.offsets, non_blocking=True)
             got = torch.cuda.Event()
             got.record(drain_stream)

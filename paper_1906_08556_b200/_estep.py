@@ -13,8 +13,6 @@ ones vector so every reduction has a fixed order (bit-reproducible, no atomics).
 
 from __future__ import annotations
 
-import math
-
 import numpy as np
 import torch
 
@@ -274,9 +272,3 @@ def predictive_covariances_device(T, Sigma, C, F, D):
         dgemm(T, T, out, F, F, D, trans_b=True, beta=1.0, batch=C, stride_a=F * D, stride_b=F * D, stride_c=F * F)
     return out
 
-
-def ceil_div(a, b):
-    return -(-a // b)
-
-
-del math

@@ -1,12 +1,32 @@
 // Diagonal top-K preselection (select_top_k / align_frames stage 1, gmm.py:376-386, 409-410) on the
 // 5th-generation tensor cores, exact to the FP64 reference ordering.
 //
-// 1. Approximate scores.  s~(t, c) = sum_k feat_k(x_t) W_k(c) + c_c with feat = [x^2, x] (K = 2F,
-//    padded to a multiple of 8) is one GEMM per 128-frame tile, computed with tcgen05.mma kind::tf32
-//    in the 3xTF32 form  a_hi b_hi + a_hi b_lo + a_lo b_hi  (f32 accumulation in TMEM).  Its error is
-//    below kappa * S_t with S_t = sum_f x_f^2 max_c|a_cf| + |x_f| max_c|b_cf| + max_c|c_c| and
-//    kappa = 2^-12 (worst-case bound 4.4e-5 S_t, typical 1e-7 S_t), so with m_t = kappa S_t
-//    every exact score lies in [s~ - m, s~ + m].
+// 1. Approximate scores.  s~(t, c) = sum_k feat_k(x_t) W_k(c) with feat = [x^2, x, 1] (K = 2F+1,
+//    padded to a multiple of 16) is one GEMM per 128-frame tile on tcgen05.mma kind::f16 in the
+//    3xFP16 form  a_hi b_hi + a_hi b_lo + a_lo b_hi  (f32 accumulation in TMEM; column k of W is
+//    scaled by 2^e_k and the frame side by 2^-e_k 2^-E, all exact).  W is row-centred (W_k(c) =
+//    tab_k(c) - mid_k, build_aux_kernel): that shifts every score of a frame by the same amount and
+//    leaves its order unchanged.  Error bound, with
+//    S_t = sum_f x_f^2 max_c|a_cf| + |x_f| max_c|b_cf| + max_c|c_c| >= sum_k |feat_k W_k(c)| for every c
+//    (a, b, c the centred rows):
+//    (a) operand split: hi = f16(w), lo = f16(w - hi) leave |w - hi - lo| <= 2^-22 |w| (f16 has an
+//        11-bit significand; f16 subnormals add <= 2^-25 absolute on scaled operands >= 2^8), and the
+//        dropped a_lo b_lo is <= 2^-22 |ab|: together <= 3.01 * 2^-22 sum_k|a_k b_k| <= 2^-20.4 S_t;
+//    (b) products: f16 x f16 = 22 significant bits, exact in f32;
+//    (c) accumulation: one score is the output of NM = 3 * KP/16 MMAs (24 at F = 60) chained through
+//        its f32 TMEM accumulator.  NO rounding mode, summation order or guard-bit count is assumed:
+//        only that each MMA returns the sum of its 17 addends (16 products + the accumulator) with an
+//        error below 17 f32 ulps of the largest addend, i.e. <= 17 * 2^-23 * sum|addends| (this holds
+//        for round-to-nearest, round-toward-zero / truncation after alignment to the largest
+//        exponent, and any faithful pairwise order).  Since every addend of MMA j is a product
+//        (sum <= S_t) or the accumulator (|acc| <= S_t), the chain's total is <= NM * 17 * 2^-23 S_t
+//        = 408 * 2^-23 S_t = 2^-14.33 S_t at NM = 24;
+//    (a)+(c) <= 2^-14.30 S_t < kappa * S_t with kappa = 2^-14 (1.23x slack, which also covers the f32
+//    evaluation of m = kappa S_t: the per-row maxima are rounded up, S_t sums <= 128 positive terms).
+//    So with m_t = kappa S_t every exact score lies in [s~ - m, s~ + m].  Measured max |s~ - s| / S_t
+//    over >= 4e5 frames x top-20 on five UBM/feature shapes: 2^-21.1 (tools/err_check_select.py).
+//    KP/16 <= 8 (F <= MAX_F = 63) keeps NM <= 24; the constant is compiled in, never read from the
+//    environment.
 // 2. Candidate window.  Each epilogue thread owns one frame (one TMEM lane) and streams the 2048
 //    scores of its frame out of TMEM (tcgen05.ld 32x32b): a value-only top-K list gives the running
 //    K-th largest s~_(K); every score >= s~_(K) - 2m is appended to a per-thread smem buffer.  Any
@@ -51,7 +71,7 @@ constexpr int H = 2;           // epilogue warps per TMEM lane quarter (each tak
 constexpr int NEPI = 128 * H;  // epilogue threads
 constexpr int NT = 128 + NEPI;
 constexpr int CAP = 24;        // candidate buffer entries per (frame, half)
-constexpr float KAPPA = 1.0f / 65536.0f;  // 3xTF32 bound: 28x the max observed error
+constexpr float KAPPA = 1.0f / 16384.0f;  // proven 3xFP16 bound (header, step 1): 2^-14.30 < 2^-14
 constexpr float KAPPA1 = 1.0f / 4096.0f;   // pass-0 slack (heuristic: the window check below is exact)
 constexpr int kPass0Pieces = 4;  // A feature pieces of the next tile built between pass-0 pairs (rest: pass 1)
 constexpr int MAX_F = 63;      // A hi/lo (2F+1 f16, padded to 16, two per column) in TMEM columns 256-383
@@ -61,7 +81,7 @@ __host__ __device__ inline int nchunks(int C) { return (C + 2 * NC - 1) / (2 * N
 
 // Layout of the tensor-core part of the diagonal table (after the (2F+1) x C FP64 table).
 struct Layout {
-  size_t blob, maxes, colscale, exact, total;
+  size_t blob, maxes, colscale, mids, exact, total;
 };
 __host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
 __host__ __device__ inline Layout layout(int C, int F) {
@@ -73,6 +93,8 @@ __host__ __device__ inline Layout layout(int C, int F) {
   off = al(off + sizeof(float) * (2 * F + 1), 256);
   L.colscale = off;
   off = al(off + sizeof(float) * kp(F), 256);
+  L.mids = off;
+  off = al(off + sizeof(double) * (2 * F + 1), 256);
   L.exact = off;
   off += sizeof(double) * (size_t)C * (2 * F + 2);
   L.total = al(off, 256);
@@ -92,8 +114,8 @@ inline size_t smem_bytes(int) {
 // core-matrix order, all hi tiles first, then all lo tiles.
 __device__ __forceinline__ int col_exponent(float mx) { return mx > 0.0f ? 8 - ilogbf(mx) : 0; }
 
-__global__ void build_blob_kernel(const double* tab, int C, int F, const float* maxes, __half* blob,
-                                  float* colscale) {
+__global__ void build_blob_kernel(const double* tab, int C, int F, const float* maxes, const double* mids,
+                                  __half* blob, float* colscale) {
   const int KP = kp(F), KS = KP / 16, NCH = nchunks(C);
   int64_t total = (int64_t)NCH * NC * KP;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -103,7 +125,7 @@ __global__ void build_blob_kernel(const double* tab, int C, int F, const float* 
     int n = cc / NC, r = cc % NC, s = k / 16, kk = k % 16;
     const int e = k <= 2 * F ? col_exponent(maxes[k]) : 0;
     // padded components get a NaN constant term: their score is NaN and never enters a window
-    double w = (k <= 2 * F) ? (cc < C ? tab[(int64_t)k * C + cc] : (k == 2 * F ? (double)NAN : 0.0)) : 0.0;
+    double w = (k <= 2 * F) ? (cc < C ? tab[(int64_t)k * C + cc] - mids[k] : (k == 2 * F ? (double)NAN : 0.0)) : 0.0;
     float wf = (float)ldexp(w, e);
     __half hi = __float2half_rn(wf);
     __half lo = __float2half_rn(wf - __half2float(hi));
@@ -115,23 +137,53 @@ __global__ void build_blob_kernel(const double* tab, int C, int F, const float* 
   }
 }
 
-// maxes[f] = max_c |tab[f][c]| for f < 2F+1, rounded up by one f32 ulp; exact[c] = column c of tab.
-__global__ void build_aux_kernel(const double* tab, int C, int F, float* maxes, double* exact) {
+// Row centring.  A term g(t) common to every component of a frame never changes that frame's
+// order, so row f of the tensor-core operand is tab[f][c] - mid_f with mid_f the midrange of the row
+// over c (the dropped sum_f feat_f(x_t) mid_f is such a g(t)).  This only shrinks the operands the
+// error bound scales with: max_c |tab[f][c] - mid_f| is half the row's range (the constant row
+// log w - (F log 2pi + log|Sigma|)/2 - ..., which dominated S_t, shrinks ~10x at config 2).  The exact
+// FP64 rescoring uses the uncentred table (all its comparisons are within one frame).
+// mids[f] = midrange of row f; maxes[f] = max_c |tab[f][c] - mids[f]| rounded up; exact[c] = column c.
+__global__ void build_aux_kernel(const double* tab, int C, int F, float* maxes, double* mids, double* exact) {
   int f = blockIdx.x;  // one CTA per table row
-  double m = 0.0;
+  double lo = INFINITY, hi = -INFINITY;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     double v = tab[(int64_t)f * C + c];
-    m = fmax(m, fabs(v));
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
     exact[(int64_t)c * (2 * F + 2) + f] = v;
     if (f == 2 * F) exact[(int64_t)c * (2 * F + 2) + 2 * F + 1] = 0.0;
   }
-  __shared__ double red[32];
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __shared__ double rlo[32], rhi[32], mid_s;
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    rlo[threadIdx.x >> 5] = lo;
+    rhi[threadIdx.x >> 5] = hi;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmax(m, red[w]);
-    m = fmax(m, red[0]);
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) {
+      lo = fmin(lo, rlo[w]);
+      hi = fmax(hi, rhi[w]);
+    }
+    const double mid = isfinite(lo) && isfinite(hi) ? 0.5 * lo + 0.5 * hi : 0.0;
+    mids[f] = mid;
+    mid_s = mid;
+  }
+  __syncthreads();
+  // max |v - mid| over the centred values exactly as build_blob_kernel forms them
+  const double mid = mid_s;
+  double m = 0.0;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) m = fmax(m, fabs(tab[(int64_t)f * C + c] - mid));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) rhi[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) m = fmax(m, rhi[w]);
     maxes[f] = __double2float_ru(m) * (1.0f + 1.0f / 1048576.0f);
   }
 }
@@ -939,10 +991,11 @@ int diag_table_tc(const double* tab, int C, int F, cudaStream_t st) {
   uint8_t* base = (uint8_t*)tab;
   int64_t total = (int64_t)stc::nchunks(C) * stc::NC * stc::kp(F);
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-  stc::build_aux_kernel<<<2 * F + 1, 256, 0, st>>>(tab, C, F, (float*)(base + L.maxes),
+  stc::build_aux_kernel<<<2 * F + 1, 256, 0, st>>>(tab, C, F, (float*)(base + L.maxes), (double*)(base + L.mids),
                                                    (double*)(base + L.exact));
   stc::build_blob_kernel<<<blocks, 256, 0, st>>>(tab, C, F, (const float*)(base + L.maxes),
-                                                 (__half*)(base + L.blob), (float*)(base + L.colscale));
+                                                 (const double*)(base + L.mids), (__half*)(base + L.blob),
+                                                 (float*)(base + L.colscale));
   TVK_CHECK_LAUNCH("diag_table tensor-core part");
   return TVK_OK;
 }
@@ -971,10 +1024,15 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   int64_t ntiles = (T + stc::TM - 1) / stc::TM;
   int64_t want = (ntiles + stc::CL - 1) / stc::CL * stc::CL;
   int grid = (int)std::min<int64_t>(want, num_sms() / stc::CL * stc::CL);
-  const char* ek = getenv("TVK_SELECT_KAPPA");
-  const float kappa = ek ? (float)atof(ek) : stc::KAPPA;
+  const float kappa = stc::KAPPA;  // compiled in: the margin is part of the exactness proof
+#ifdef TVK_SELECT_DIAG  // diagnostics build only (tools/): pipeline-only / timeline modes
   const char* ed = getenv("TVK_SELECT_DEBUG");
   const int debug = ed ? atoi(ed) : 0;
+#else
+  const int debug = 0;
+#endif
+  // test hook: the pass-0 slack only moves work between the tensor-core and the exact kernels (the
+  // window check proves every collection complete), so it can cost time but never change a result
   const char* ek1 = getenv("TVK_SELECT_KAPPA1");
   const float kappa1 = ek1 ? (float)atof(ek1) : stc::KAPPA1;
   // group maxima of 32 (or 8, or single scores) while at least 2K groups exist
@@ -982,8 +1040,10 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   // one B stage = the hi words of a chunk pair (pass 0) or hi + lo of one chunk (pass 1): KS * 8 KB
   const int KS = stc::kp(F) / 16;
   stc::Pipe pipe{KS * 8192, KS, KS, 64, 0};
+#ifdef TVK_SELECT_DIAG
   if (const char* ep = getenv("TVK_SEL_PIPE"))  // sleep_prod,sleep_mma (ns back-off of the single-thread roles)
     sscanf(ep, "%d,%d", &pipe.sleep_prod, &pipe.sleep_mma);
+#endif
   TVK_REQUIRE(stc::RING / pipe.stage_bytes >= 2 && stc::RING / pipe.stage_bytes <= stc::MAXST, "select_tc: bad ring");
   // stream-ordered scratch: [flagged count | frame indices], candidate runs, counts, frame params
   const size_t b_flag = stc::al(sizeof(int) * (T + 1), 256);
@@ -1038,11 +1098,13 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
                                                            fpar, debug, flagged, sel, val);
     TVK_CHECK_LAUNCH("select_post");
   }
+#ifdef TVK_SELECT_DIAG
   const char* dbg = getenv("TVK_SELECT");
   if (dbg && strcmp(dbg, "tc_noexact") == 0) {  // diagnostics: leave flagged frames at -1
     cudaFreeAsync(scratch, st);
     return TVK_OK;
   }
+#endif
   const size_t xsm = sizeof(double) * C;
   cudaFuncSetAttribute(stc::select_exact_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
   stc::select_exact_kernel<XT><<<num_sms() * 8, stc::XT_THREADS, xsm, st>>>(x, F, C, K, (const double*)(base + L.exact),

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import os
 import struct
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -160,6 +161,8 @@ def _decode_frames(words, n_frames):
     from . import _lib
 
     words = np.ascontiguousarray(words, dtype="<u4")
+    if n_frames > words.shape[0]:  # every frame needs its count word: reject before allocating
+        raise FormatError("frame record shorter than declared (entry count)")
     starts = np.empty(n_frames, dtype=np.int64)
     counts = np.empty(n_frames, dtype=np.int64)
     end = ctypes.c_int64(0)
@@ -184,40 +187,132 @@ def _decode_frames(words, n_frames):
     return SparseAlignment(offsets, comps, wts), pos
 
 
+class AlignmentReader:
+    """Random access to an ALN1 corpus file through its index (io_formats.py:155-227).
+
+    Each record is bounded by the next record's start (or the index); the count-word walk and the
+    entry gather are vectorized (``_decode_frames``).  One file handle per reader.
+    """
+
+    def __init__(self, path):
+        self.path = path
+        self._fh = open(path, "rb")
+        try:
+            fh = self._fh
+            magic = _need(fh, 4, "magic")
+            if magic != ALIGNMENT_MAGIC:
+                raise FormatError(f"bad magic {magic!r}, expected {ALIGNMENT_MAGIC!r}")
+            self.top_k, n_utts, index_offset = struct.unpack("<IQQ", _need(fh, 20, "header"))
+            if index_offset > os.fstat(fh.fileno()).st_size:
+                raise FormatError("index offset beyond end of file")
+            self._index_offset = index_offset
+            fh.seek(index_offset)
+            self._index, self._order = {}, []
+            for _ in range(n_utts):
+                (n,) = struct.unpack("<I", _need(fh, 4, "index"))
+                _fits(fh, n, "index id")
+                uid = _need(fh, n, "index id").decode("utf-8")
+                (off,) = struct.unpack("<Q", _need(fh, 8, "index offset"))
+                self._index[uid] = off
+                self._order.append(uid)
+            # record end = next record start in file order (one sort, O(U log U))
+            starts = np.unique(np.array(list(self._index.values()) + [index_offset], dtype=np.uint64))
+            self._bounds = starts
+        except Exception:
+            self._fh.close()
+            raise
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def close(self):
+        self._fh.close()
+
+    def ids(self):
+        return list(self._order)
+
+    def _end_of(self, off):
+        b = self._bounds
+        i = int(np.searchsorted(b, np.uint64(off), side="right"))
+        return int(b[i]) if i < b.shape[0] else self._index_offset
+
+    def read(self, utt_id):
+        try:
+            off = self._index[utt_id]
+        except KeyError:
+            raise KeyError(f"utterance {utt_id!r} not in alignment file") from None
+        fh = self._fh
+        end = min(self._end_of(off), self._index_offset)
+        fh.seek(off)
+
+        def bounded(count, what):
+            if fh.tell() + count > self._index_offset:
+                raise FormatError(f"frame record shorter than declared ({what})")
+            return _need(fh, count, what)
+
+        (n,) = struct.unpack("<I", bounded(4, "utterance id"))
+        stored = bounded(n, "utterance id").decode("utf-8")
+        if stored != utt_id:
+            raise FormatError("alignment index does not match record")
+        (n_frames,) = struct.unpack("<Q", bounded(8, "frame count"))
+        body = max(0, end - fh.tell())
+        words = np.frombuffer(_need(fh, body - body % 4, "frame entries"), dtype="<u4")
+        ali, _ = _decode_frames(words, n_frames)
+        return ali
+
+
 def read_alignment(path):
-    """Whole ALN1 file -> {utterance id: SparseAlignment}."""
-    with open(path, "rb") as fh:
-        if _need(fh, 4, "magic") != ALIGNMENT_MAGIC:
-            raise FormatError("bad magic, expected b'ALN1'")
-        top_k, n_utts, index_offset = struct.unpack("<IQQ", _need(fh, 20, "header"))
-        size = os.fstat(fh.fileno()).st_size
-        if index_offset > size:
-            raise FormatError("index offset beyond end of file")
-        fh.seek(index_offset)
-        index = []
-        for _ in range(n_utts):
-            (n,) = struct.unpack("<I", _need(fh, 4, "index"))
-            _fits(fh, n, "index id")
-            uid = _need(fh, n, "index id").decode("utf-8")
-            (off,) = struct.unpack("<Q", _need(fh, 8, "index offset"))
-            index.append((uid, off))
-        out = {}
-        bounds = [off for _, off in index] + [index_offset]
-        order = np.argsort([off for _, off in index], kind="stable")
-        nxt = {}
-        sorted_offs = sorted(bounds)
-        for off in bounds[:-1]:
-            nxt[off] = sorted_offs[sorted_offs.index(off) + 1]
-        del order
-        for uid, off in index:
-            fh.seek(off)
-            (n,) = struct.unpack("<I", _need(fh, 4, "utterance id"))
-            stored = _need(fh, n, "utterance id").decode("utf-8")
-            if stored != uid:
-                raise FormatError("alignment index does not match record")
-            (n_frames,) = struct.unpack("<Q", _need(fh, 8, "frame count"))
-            body = nxt[off] - fh.tell()
-            words = np.frombuffer(_need(fh, body, "frame entries"), dtype="<u4")
-            ali, used = _decode_frames(words, n_frames)
-            out[uid] = ali
-    return out
+    """Whole ALN1 file -> {utterance id: SparseAlignment} (io_formats.py:230-233)."""
+    with AlignmentReader(path) as reader:
+        return {u: reader.read(u) for u in reader.ids()}
+
+
+# ----------------------------------------------------------------------------- trial lists
+# Verification trial files (io_formats.py:299-327): one "enrol test target|nontarget" line per trial.
+# Not on the GPU path; kept so the drop-in's io_formats surface matches the reference's.
+
+_LABELS = {"target": True, "nontarget": False}
+
+
+@dataclass
+class TrialList:
+    """Verification trials: enrol/test id pairs with target flags."""
+
+    enrol_ids: list
+    test_ids: list
+    is_target: np.ndarray
+
+    def __len__(self):
+        return len(self.enrol_ids)
+
+    def validate(self):
+        if len(self.enrol_ids) != len(self.test_ids) or len(self.test_ids) != self.is_target.shape[0]:
+            raise ValueError("trial field lengths differ")
+
+
+def write_trials(path, trials):
+    trials.validate()
+    lines = [f"{e} {t} {'target' if flag else 'nontarget'}\n"
+             for e, t, flag in zip(trials.enrol_ids, trials.test_ids, trials.is_target)]
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.writelines(lines)
+
+
+def read_trials(path):
+    enrol, test, flags = [], [], []
+    with open(path, encoding="utf-8") as fh:
+        for n, raw in enumerate(fh, 1):
+            parts = raw.split()
+            if not parts:
+                continue
+            if len(parts) != 3:
+                raise FormatError(f"{path}:{n}: expected 'enrol test label'")
+            if parts[2] not in _LABELS:
+                raise FormatError(f"{path}:{n}: unknown label {parts[2]!r}")
+            enrol.append(parts[0])
+            test.append(parts[1])
+            flags.append(_LABELS[parts[2]])
+    return TrialList(enrol, test, np.asarray(flags, dtype=bool))

@@ -37,6 +37,7 @@ from .tvm import (AUGMENTED, DEFAULT_PRIOR_OFFSET, SIGMA_FLOOR_SCALE, STANDARD, 
 logger = logging.getLogger(__name__)
 
 ALIGN_CHUNK_FRAMES = 1 << 21  # frames per device alignment launch
+ENTRY_CAPACITY_PER_FRAME = 8  # initial corpus CSR capacity (entries per frame; grows on demand)
 
 
 class PipelineError(RuntimeError):
@@ -79,6 +80,63 @@ class InMemoryFeatureStore:
             return self._mapping[utt_id]
         except KeyError:
             raise KeyError(f"missing features for utterance {utt_id!r}") from None
+
+
+# ----------------------------------------------------------------------------- host batch pool
+
+
+def _map_batches(batches, fn, workers, deterministic):
+    """Yield ``(index, fn(batch))`` over a bounded pool of host threads (pipeline.py:279-350).
+
+    With ``deterministic`` results come out in batch order, otherwise in completion order; at most
+    ``2 * workers`` batches are submitted ahead of the consumer.  The GPU drivers do not run their
+    arithmetic through it (device batching replaces it); it remains for host-side
+    work such as feature loading.  A failing batch stops the pool and raises ``PipelineError``.
+    """
+    import concurrent.futures as cf
+
+    n = len(batches)
+    if workers <= 1 or n <= 1:
+        for i in range(n):
+            yield i, fn(batches[i])
+        return
+    window = 2 * workers
+    with cf.ThreadPoolExecutor(max_workers=workers) as pool:
+        live = {}
+        nxt = 0
+
+        def refill():
+            nonlocal nxt
+            while nxt < n and len(live) < window:
+                live[pool.submit(fn, batches[nxt])] = nxt
+                nxt += 1
+
+        def result(fut):
+            try:
+                return fut.result()
+            except Exception as exc:
+                for f in live:
+                    f.cancel()
+                raise PipelineError("a loader worker failed") from exc
+
+        refill()
+        if deterministic:
+            order = {i: f for f, i in live.items()}
+            for i in range(n):
+                fut = order.pop(i)
+                payload = result(fut)
+                del live[fut]
+                yield i, payload
+                refill()
+                order.update({j: f for f, j in live.items() if j not in order})
+        else:
+            while live:
+                done, _ = cf.wait(list(live), return_when=cf.FIRST_COMPLETED)
+                for fut in sorted(done, key=live.get):
+                    payload = result(fut)
+                    i = live.pop(fut)
+                    yield i, payload
+                refill()
 
 
 # ----------------------------------------------------------------------------- configuration
@@ -239,6 +297,61 @@ class RunMetrics:
 # ----------------------------------------------------------------------------- device corpus
 
 
+STAGE_BYTES = 64 << 20  # pinned staging buffer size of the corpus upload (two buffers)
+_corpus_stage = []
+
+
+def _stream_to_device(mats, n_frames, dim, dtype):
+    """Upload a list of (T_u, F) host matrices into one device (n_frames, F) tensor through two
+    reused pinned staging buffers (copy stream, double-buffered), so the host never holds a
+    concatenated or pinned copy of the whole shard (host memory stays ~1x the corpus)."""
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    esize = np.dtype(dtype).itemsize
+    x = _lib.empty((n_frames, dim), tdt)
+    rows_per = max(1, STAGE_BYTES // (dim * esize))
+    if not _corpus_stage:
+        _corpus_stage.extend(torch.empty(STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2))
+    copy_stream = torch.cuda.Stream()
+    copy_stream.wait_stream(torch.cuda.current_stream())  # x allocated on the current stream
+    done = [None, None]
+    b, fill, row0 = 0, 0, 0
+    view = None
+
+    def flush():
+        nonlocal b, fill, row0
+        with torch.cuda.stream(copy_stream):
+            x[row0:row0 + fill].copy_(view[:fill], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        done[b] = ev
+        row0 += fill
+        fill = 0
+        b ^= 1
+
+    for m in mats:
+        m = m.reshape(-1, dim)
+        pos = 0
+        while pos < m.shape[0]:
+            if fill == 0:
+                if done[b] is not None:
+                    done[b].synchronize()  # this staging buffer's previous copy has landed
+                view = torch.from_numpy(_corpus_stage[b].numpy()[: rows_per * dim * esize].view(dtype)).view(rows_per, dim)
+            n = min(rows_per - fill, m.shape[0] - pos)
+            view.numpy()[fill:fill + n] = m[pos:pos + n]
+            fill += n
+            pos += n
+            if fill == rows_per:
+                flush()
+    if fill:
+        flush()
+    for ev in done:  # the staging buffers are reused by the next upload
+        if ev is not None:
+            ev.synchronize()
+    torch.cuda.current_stream().wait_stream(copy_stream)
+    x.record_stream(copy_stream)
+    return x
+
+
 class DeviceCorpus:
     """The (rank's share of the) corpus resident in HBM: concatenated frames + utterance bounds."""
 
@@ -254,12 +367,10 @@ class DeviceCorpus:
         for m in mats:
             if m.shape[0] and m.shape[1] != self.dim:
                 raise PipelineError("utterances disagree on the feature dimension")
-        f32 = all(m.dtype == np.float32 for m in mats)
-        host = np.concatenate([m.reshape(-1, self.dim) for m in mats]) if mats else np.zeros((0, 1))
-        host = host.astype(np.float32 if f32 else np.float64, copy=False)
+        dtype = np.float32 if all(m.dtype == np.float32 for m in mats) else np.float64
         self.n_frames = int(lens.sum())
-        pinned = torch.from_numpy(np.ascontiguousarray(host)).pin_memory() if self.n_frames else None
-        self.x = pinned.to(_lib.device(), non_blocking=True) if pinned is not None else None
+        self.x = _stream_to_device(mats, self.n_frames, self.dim, dtype) if self.n_frames else \
+            _lib.empty((0, max(self.dim, 1)), torch.float32 if dtype == np.float32 else torch.float64)
         self.utt_frames_host = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
         self.utt_frames = _lib.to_dev(self.utt_frames_host, torch.int64)
 
@@ -275,6 +386,60 @@ class DeviceCorpus:
         return self
 
 
+class DeviceFeatureStore:
+    """A feature store whose frames are already resident in HBM: one (T, F) device matrix plus
+    utterance bounds (e.g. frames produced on the device, or a corpus loaded once and reused by
+    several drivers).  The drivers use its frames in place; ``load`` returns a host copy for
+    callers that want one utterance.  ``ids()`` keeps construction order.
+
+    Under torch.distributed a rank may hold only its shard: pass the corpus-wide id list as
+    ``global_ids`` (the rank's ``ids`` must be its ``_dist.shard`` of it); the drivers then shard
+    ``global_ids`` exactly as they would shard a host store and find every local id resident."""
+
+    def __init__(self, x, utt_frames, ids, global_ids=None):
+        self.x = x
+        self.utt_frames_host = np.asarray(utt_frames, dtype=np.int64)
+        self._ids = list(ids)
+        self._global = list(global_ids) if global_ids is not None else None
+        self._pos = {u: i for i, u in enumerate(self._ids)}
+        if len(self._pos) != len(self._ids) or self.utt_frames_host.shape[0] != len(self._ids) + 1:
+            raise ValueError("DeviceFeatureStore: ids must be unique and match the utterance bounds")
+
+    def ids(self):
+        return list(self._global if self._global is not None else self._ids)
+
+    def load(self, utt_id):
+        try:
+            i = self._pos[utt_id]
+        except KeyError:
+            raise KeyError(f"missing features for utterance {utt_id!r}") from None
+        lo, hi = self.utt_frames_host[i], self.utt_frames_host[i + 1]
+        return _lib.to_host(self.x[lo:hi])
+
+    def device_corpus(self, ids):
+        """DeviceCorpus over ``ids``: a view when they are a contiguous run of the store, else a
+        device gather of their frames."""
+        try:
+            idx = np.array([self._pos[u] for u in ids], dtype=np.int64)
+        except KeyError as exc:
+            raise KeyError(f"utterance {exc.args[0]!r} is not resident on this rank") from None
+        if idx.size and np.all(np.diff(idx) == 1):
+            lo, hi = int(idx[0]), int(idx[-1]) + 1
+            b = self.utt_frames_host[lo:hi + 1]
+            return DeviceCorpus.from_device(self.x[b[0]:b[-1]], b - b[0], ids)
+        lens = self.utt_frames_host[idx + 1] - self.utt_frames_host[idx]
+        rows = np.concatenate([np.arange(self.utt_frames_host[i], self.utt_frames_host[i + 1]) for i in idx]) \
+            if idx.size else np.zeros(0, np.int64)
+        x = self.x[_lib.to_dev(rows, torch.int64)] if rows.size else self.x[:0]
+        return DeviceCorpus.from_device(x, np.concatenate([[0], np.cumsum(lens)]), ids)
+
+
+def _device_corpus(store, ids, workers):
+    if hasattr(store, "device_corpus"):
+        return store.device_corpus(list(ids))
+    return DeviceCorpus(store, ids, workers)
+
+
 class DeviceAlignment:
     """Corpus alignment in device CSR form plus per-utterance entry bounds (host)."""
 
@@ -284,21 +449,34 @@ class DeviceAlignment:
 
     @classmethod
     def compute(cls, corpus, diag_tab, full_tab, top_k, prune):
+        """Align the corpus chunk by chunk into one CSR sized by the entries actually kept.
+
+        The CSR starts at ENTRY_CAPACITY_PER_FRAME entries per frame (prune 0.025 keeps <= 40 by
+        construction and ~4.5 on speech-like data) and grows geometrically only if a chunk needs
+        more, so HBM holds ~44 B/frame instead of a top_k-sized 8*top_k B/frame.
+        """
         T = corpus.n_frames
         k = min(top_k, diag_tab.C)
         offsets = _lib.empty((T + 1,), torch.int64)
-        comps = _lib.empty((max(T * k, 1),), torch.int32)
-        wts = _lib.empty((max(T * k, 1),), torch.float32)
+        cap = max(1, min(T * k, int(T * ENTRY_CAPACITY_PER_FRAME)))
+        comps = _lib.empty((cap,), torch.int32)
+        wts = _lib.empty((cap,), torch.float32)
         offsets[:1].zero_()
         ebase = 0
         for lo in range(0, T, ALIGN_CHUNK_FRAMES):
             hi = min(T, lo + ALIGN_CHUNK_FRAMES)
             res = _device.align(corpus.x[lo:hi], diag_tab, full_tab, k, prune)
             e = res.n_entries
+            if ebase + e > cap:  # grow: at least 1.5x, enough for the rest at this chunk's density
+                need = ebase + e + int((T - hi) * (e / max(hi - lo, 1)) * 1.1)
+                cap = min(T * k, max(need, int(cap * 1.5)))
+                comps = torch.cat([comps[:ebase], _lib.empty((cap - ebase,), torch.int32)])
+                wts = torch.cat([wts[:ebase], _lib.empty((cap - ebase,), torch.float32)])
             offsets[lo + 1:hi + 1] = res.offsets[1:] + ebase
             comps[ebase:ebase + e] = res.components[:e]
             wts[ebase:ebase + e] = res.weights[:e]
             ebase += e
+            del res
         ue = _lib.to_host(offsets[corpus.utt_frames])
         return cls(offsets, comps, wts, ue)
 
@@ -368,7 +546,7 @@ def align_corpus(store, ubm_diag, ubm_full, top_k=20, prune=0.025, workers=1, ba
     """Align every utterance of a store; returns {utterance id: SparseAlignment} (pipeline.py:364-382)."""
     if ids is None:
         ids = store.ids()
-    corpus = DeviceCorpus(store, ids, workers)
+    corpus = _device_corpus(store, ids, workers)
     if corpus.n_frames == 0:
         return {u: SparseAlignment.from_frames([]) for u in ids}
     full_tab = ubm_full.device_table()
@@ -389,7 +567,10 @@ def accumulate_corpus(model, store, alignments, config, ids=None, workspace=None
     if getattr(ws, "bad", np.zeros(0)).size:
         from ._linalg import NumericError
         raise NumericError(f"Sigma[{int(ws.bad[0])}] is not SPD")
-    corpus = DeviceCorpus(store, ids, config.workers)
+    # under torch.distributed each rank accumulates its contiguous shard and the all-reduce in
+    # _accumulate sums the shards, so every rank returns the full-corpus statistics
+    rank, world_size = _dist.world()
+    corpus = _device_corpus(store, _dist.shard(list(ids), rank, world_size), config.workers)
     ali = DeviceAlignment.from_host(corpus, alignments)
     center = dm.bias if model.formulation == STANDARD else None
     acc = _accumulate(dm, ws, corpus, ali, center)
@@ -408,7 +589,7 @@ def extract_corpus(model, store, top_k=20, prune=0.025, workers=1, batch_size=8,
         raise NumericError(f"Sigma[{int(ws.bad[0])}] is not SPD")
     rank, world_size = _dist.world()
     local = _dist.shard(list(ids), rank, world_size)
-    emb = _extract_device(dm, ws, model, DeviceCorpus(store, local, workers), top_k, prune)
+    emb = _extract_device(dm, ws, model, _device_corpus(store, local, workers), top_k, prune)
     counts = [_dist.shard_range(len(ids), r, world_size)[1] - _dist.shard_range(len(ids), r, world_size)[0]
               for r in range(world_size)]
     emb = _lib.to_host(_dist.gather_rows(emb, counts))
@@ -558,6 +739,23 @@ class DeviceTrainer:
         self.alignment = DeviceAlignment.compute(self.corpus, diag_tab, full_tab, self.config.top_k,
                                                  self.config.prune)
 
+    def realign_point(self, it, align_diag):
+        """UBM-mean feedback after iteration ``it`` (pipeline.py:628-638): at a realignment point the
+        alignment means become p*T[:, :, 0] (augmented) or the bias (standard) and the corpus
+        alignment is dropped so the next iteration realigns every frame.  Returns True if so."""
+        cfg = self.config
+        if not (cfg.realign_interval > 0 and it % cfg.realign_interval == 0 and it != cfg.iterations):
+            return False
+        dm = self.dm
+        if dm.formulation == AUGMENTED:
+            means = dm.prior_offset * _lib.to_host(dm.T[:, :, 0])
+        else:
+            means = _lib.to_host(dm.bias)
+        self.model.ubm_means = means.copy()
+        align_diag.means = means.copy()
+        self.alignment = None
+        return True
+
     def iteration(self):
         """E-step + M-step (+ min-div); returns the aux of the E-step."""
         cfg, dm = self.config, self.dm
@@ -655,7 +853,7 @@ def train_extractor(config, store, ubm_diag, ubm_full, seed=None, checkpoint_dir
 
     metrics = RunMetrics()
     local_ids = _dist.shard(ids, rank, world_size)
-    corpus = DeviceCorpus(store, local_ids, config.workers)
+    corpus = _device_corpus(store, local_ids, config.workers)
     trainer = DeviceTrainer(model, corpus, config)
     cache = os.path.join(checkpoint_dir, _ALIGN_CACHE) if checkpoint_dir is not None else None
     have_alignment = False
@@ -674,14 +872,7 @@ def train_extractor(config, store, ubm_diag, ubm_full, seed=None, checkpoint_dir
 
         aux = trainer.iteration()
 
-        if config.realign_interval > 0 and it % config.realign_interval == 0 and it != config.iterations:
-            dm = trainer.dm
-            if dm.formulation == AUGMENTED:
-                means = dm.prior_offset * _lib.to_host(dm.T[:, :, 0])
-            else:
-                means = _lib.to_host(dm.bias)
-            model.ubm_means = means.copy()
-            align_diag.means = model.ubm_means.copy()
+        if trainer.realign_point(it, align_diag):
             have_alignment = False
             if cache is not None and rank == 0 and os.path.exists(cache):
                 os.remove(cache)
@@ -698,3 +889,30 @@ def train_extractor(config, store, ubm_diag, ubm_full, seed=None, checkpoint_dir
             save_model(trainer.sync_host(), _ckpt_model(checkpoint_dir, it))
             _write_state(checkpoint_dir, it, config_hash, seed)
     return trainer.sync_host(), metrics
+
+
+# ----------------------------------------------------------------------------- out of scope
+# The reference pipeline module also hosts the verification back-end drivers (pipeline.py:660-757:
+# EvalProtocol, evaluate_model, ensemble_run).  They score embeddings with the PLDA/LDA back-end,
+# which is outside the GPU hot path.  The names resolve so that code importing them
+# from the drop-in still imports; using one raises and points at the reference package.
+
+_OUT_OF_SCOPE = ("EvalProtocol", "evaluate_model", "ensemble_run")
+
+
+class _OutOfScope:
+    def __init__(self, name):
+        self.__name__ = self.__qualname__ = name
+
+    def __call__(self, *args, **kwargs):
+        raise NotImplementedError(f"tvkit.{self.__name__} is verification back-end scoring, outside the GPU "
+                                  f"i-vector path of this package; use the reference tvkit for it")
+
+    def __repr__(self):
+        return f"<out-of-scope {self.__name__}>"
+
+
+def __getattr__(name):
+    if name in _OUT_OF_SCOPE:
+        return _OutOfScope(name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

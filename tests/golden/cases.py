@@ -139,3 +139,34 @@ def config1_inputs():
                           min_div=True, sigma_update=True, update_mean=False, realign_interval=0,
                           top_k=20, prune=0.025, prior_offset=100.0, batch_size_utts=8)
     return ids, feats, cfg
+
+
+# BASELINE config-3 / config-5 shape (C=2048, F=60, D=400) at a corpus size the reference
+# finishes in minutes: the EM metric's arithmetic (D=400 posteriors, split-K b-GEMM, multi-batch
+# accumulation, update_T at D=400, F=60 workspace) checked against the reference itself.
+EM2048_CASES = [
+    # name, formulation, generator seed, utterances, iterations, min_div, sigma, update_mean, realign
+    ("aug2048", "augmented", 0, 48, 2, True, True, False, 0),
+    ("std2048", "standard", 1, 48, 2, True, False, True, 1),
+]
+EM2048_SHAPE = dict(n_comp=2048, dim=60, rank=400, frames=(300, 300), within=0.3)
+# components whose T / Sigma rows are stored verbatim (the rest is pinned by per-component norms)
+EM2048_SAMPLE_COMPS = (0, 1, 17, 333, 1024, 1500, 2046, 2047)
+
+
+def em2048_inputs(case):
+    """(corpus namespace, TrainConfig kwargs) for an EM2048_CASES row."""
+    name, form, seed, n_utts, iters, md, su, um, ri = case
+    p = EM2048_SHAPE
+    cor = corpus(form, seed, p["n_comp"], p["dim"], p["rank"], n_utts, 1, p["frames"], p["within"])
+    kw = dict(formulation=form, latent_dim=p["rank"], iterations=iters, min_div=md, sigma_update=su,
+              update_mean=um, realign_interval=ri, top_k=20, prune=0.025, prior_offset=100.0,
+              seeds=(0,), batch_size_utts=8, workers=1)
+    return cor, kw
+
+
+def em2048_summary(T, Sigma):
+    """Rotation-sensitive fingerprints of a trained (T, Sigma) small enough to commit."""
+    s = list(EM2048_SAMPLE_COMPS)
+    return dict(T_rows=T[s], Sigma_rows=Sigma[s], T_norm=np.sqrt(np.einsum("cfd,cfd->c", T, T)),
+                T_colsum=T.sum(axis=0), Sigma_trace=np.trace(Sigma, axis1=1, axis2=2))

@@ -222,6 +222,68 @@ def make_ubm():
     save("ubm", **out)
 
 
+def make_em2048():
+    """Reference train_extractor + extract_corpus at C=2048, F=60, D=400 (EM2048_CASES)."""
+    import time
+    from cases import EM2048_CASES, em2048_inputs, em2048_summary
+    out = {}
+    for case in EM2048_CASES:
+        name = case[0]
+        t0 = time.time()
+        cor, kw = em2048_inputs(case)
+        # the oracle generator must reproduce the reference's sample_corpus bit for bit
+        spec = rsynth.SynthSpec(n_components=2048, feat_dim=60, latent_dim=400, n_speakers=case[3],
+                                utts_per_speaker=1, frames_range=(300, 300), seed=case[2],
+                                formulation=case[1], within_noise=0.3, mean_scale=8.0)
+        ref_cor = rsynth.sample_corpus(spec)
+        assert ref_cor.ids == cor.ids
+        for u in cor.ids:
+            assert ref_cor.features[u].tobytes() == cor.features[u].tobytes(), "generator drifted"
+        gen = ref_cor.model
+        ubm_full, ubm_diag = gen.alignment_ubm_full(), gen.alignment_ubm_diag()
+        assert np.array_equal(ubm_full.covariances, cor.full[2])
+        cfg = rpipe.TrainConfig(**kw)
+        store = rpipe.InMemoryFeatureStore(ref_cor.features)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            model, metrics = rpipe.train_extractor(cfg, store, ubm_diag, ubm_full, seed=0)
+            ids, emb = rpipe.extract_corpus(model, store, top_k=20, prune=0.025)
+        d = dict(feat_digest=np.array([digest(*[cor.features[u] for u in cor.ids])]),
+                 aux=np.array([r.aux for r in metrics.records]), prior=np.array(model.prior_offset),
+                 ubm_means=model.ubm_means, bias=model.bias if model.bias is not None else np.zeros(0),
+                 ivectors=emb, **em2048_summary(model.T, model.Sigma))
+        for k, v in d.items():
+            out[f"{name}__{k}"] = v
+        print(f"{name}: {time.time() - t0:.0f} s, aux {d['aux']}", flush=True)
+    save("em2048", **out)
+
+
+
+def make_io():
+    """Files written by the reference's own writers (io_formats.py): an ALN1 alignment corpus (from
+    reference align_frames on seeded data, including an empty utterance), a TVM1 model of each
+    formulation, FMX1 matrices in f32 and f64 and a trial list.  Committed as bytes under
+    tests/golden/io/; the drop-in must read them and write byte-identical files."""
+    from tvkit import io_formats as rio
+    d = os.path.join(HERE, "io")
+    os.makedirs(d, exist_ok=True)
+    diag, full = ubm_pair(80, 16, 5, 1.0)
+    rng = np.random.default_rng(81)
+    alis = []
+    for u, n in (("spk1-utt1", 40), ("spk1-utt2", 0), ("spk2-utt1", 25), ("spk3-utt7", 57)):
+        x = rng.normal(0.0, 1.5, (n, 5)).astype(np.float32)
+        alis.append((u, rgmm.align_frames(diag, full, x, top_k=6, prune=0.025)))
+    rio.write_alignment(os.path.join(d, "ref.aln"), alis, top_k=6)
+    for form, seed in (("augmented", 82), ("standard", 83)):
+        m = rtvm.init_model(full, 3, form, seed=seed)
+        rio.save_model(m, os.path.join(d, f"ref_{form}.tvm"))
+    rio.write_matrix(rng.normal(size=(7, 3)), "f64", os.path.join(d, "ref_f64.fmx"))
+    rio.write_matrix(rng.normal(size=(4, 9)).astype(np.float32), "f32", os.path.join(d, "ref_f32.fmx"))
+    t = rio.TrialList(["a", "a", "b"], ["x", "y", "x"], np.array([True, False, True]))
+    rio.write_trials(os.path.join(d, "ref.trials"), t)
+    print("wrote", sorted(os.listdir(d)))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["align", "tvm", "train", "config1", "ubm"]
     for w in which:

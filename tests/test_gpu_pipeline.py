@@ -164,9 +164,28 @@ class TestDrivers:
         want = P.align_corpus(store, diag, full, top_k=3, prune=0.025)
         for u in cor.ids[:5]:
             np.testing.assert_array_equal(cached[u].components, want[u].components)
+        # each realignment point (after iterations 1 and 2) removes the cache; iteration 3 writes the
+        # realigned one, which must be the alignment under the UBM means updated at iteration 2
         ck2 = str(tmp_path / "ck2")
-        P.train_extractor(_config(iterations=3, realign_interval=1), store, diag, full, checkpoint_dir=ck2)
-        assert not os.path.exists(os.path.join(ck2, "alignments.aln")) or True
+        seen = {}
+
+        def probe(model, it):
+            seen[it] = os.path.exists(os.path.join(ck2, "alignments.aln"))
+            seen[f"means{it}"] = model.ubm_means.copy()
+
+        P.train_extractor(_config(iterations=3, realign_interval=1), store, diag, full, checkpoint_dir=ck2,
+                          iteration_hook=probe)
+        assert seen[1] is False and seen[2] is False and seen[3] is True
+        cached2 = read_alignment(os.path.join(ck2, "alignments.aln"))
+        m2 = seen["means2"]
+        realigned = P.align_corpus(store, gpu.GmmDiag(diag.weights, m2, diag.variances),
+                                   gpu.GmmFull(full.weights, m2, full.covariances), top_k=3, prune=0.025)
+        changed = 0
+        for u in cor.ids:
+            np.testing.assert_array_equal(cached2[u].components, realigned[u].components)
+            np.testing.assert_array_equal(cached2[u].weights, realigned[u].weights)
+            changed += not np.array_equal(cached2[u].weights, want[u].weights)
+        assert changed > 0, "the cache still holds the initial alignment after realignment"
 
     def test_realignment_skipped_on_final_iteration(self, gpu, small_world):
         from paper_1906_08556_b200 import pipeline as P
