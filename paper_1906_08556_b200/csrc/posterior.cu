@@ -11,10 +11,12 @@
 //   lauum : M = Y^T Y (+ phi phi^T) row block by row block, in place (diagonal tile staged),
 //           i.e. the packed moment the A-accumulation GEMM consumes (tvm.py:298-301).
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
 #include "spd_small.cuh"
+#include "tc.cuh"
 
 namespace tvk {
 
@@ -412,6 +414,395 @@ __global__ void __launch_bounds__(PT, 1) spd_solve_rows_kernel(const double* apk
   }
 }
 
+// ------------------------------------------------------------------ block sweep (EM posterior moments)
+//
+// The E-step needs, per utterance, M = L^-1 + phi phi^T with phi = L^-1 b and log|L| (tvm.py:195-200).
+// sweep_posterior_kernel obtains all three from ONE pass of the symmetric block sweep operator over the
+// bordered matrix [[L, b], [b^T, 0]]: sweeping the 32-wide pivot blocks k = 0..nb-1 in turn
+//   P = A_kk,  A_kk <- -P^-1,  B_i = A_ik P^-1,  A_ij <- A_ij - B_i A_jk^T (i, j != k),  A_ik <- B_i
+// leaves [[-L^-1, L^-1 b], [b^T L^-1, -b^T L^-1 b]] (the sweep-operator identity), and
+// log|L| = sum of the log pivots (the Schur complements are SPD exactly when L is, so a non-positive
+// pivot is the not-SPD signal, like a failed Cholesky).  Compared with potrf + trtri + lauum (the
+// posterior_kernel below, still used when only phi and log|L| are needed) every step has the same
+// shape -- 78 independent 32x32x32 tile updates at D = 400 -- so 16 warps stay busy with no
+// triangular dependency chains, and every operand of a step comes from shared memory:
+//   pa = the old column panel A_:k (D x 32, pivot block inverted in place to -P^-1),
+//   pb = the new column panel B_:k;
+// only the updated tile itself travels to and from L2 (read-modify-write in the output buffer, which
+// may alias the input).  The last step writes M = -A + phi phi^T (or Phi) directly.
+// sw::CL = 2 would let two CTAs (a cluster, two SMs) share one matrix: both load the panels and compute
+// B, the bordered row and the look-ahead pivot redundantly, split the tile updates, and order the
+// global tiles with one cluster barrier per step.  74 matrices in flight (47 MB at D = 400) then stay
+// L2-resident (DRAM 0.66 GB read + 0.76 GB written per 1024 matrices, vs 0.86 + 7.3 GB with 148
+// single-SM matrices), but the duplicated per-step work made it 1.4x slower (8.3 vs 5.9 ms), so one
+// CTA per matrix is the default.
+#ifdef TVK_SWEEP_PROF
+__device__ unsigned long long g_sweep_prof[8];
+#define SWP(i)                                                              \
+  do {                                                                      \
+    if (threadIdx.x == 0) {                                                 \
+      const long long t_ = clock64();                                       \
+      atomicAdd(&g_sweep_prof[i], (unsigned long long)(t_ - swp_prev));     \
+      swp_prev = t_;                                                        \
+    }                                                                       \
+  } while (0)
+#else
+#define SWP(i) \
+  do {         \
+  } while (0)
+#endif
+namespace sw {
+constexpr int NT = 512;  // 16 warps, one CTA per SM
+constexpr int CL = 1;    // CTAs (SMs) per matrix (2 = cluster pair: no L2 thrash but slower, see below)
+constexpr int NWARP = NT / 32;
+constexpr int MAXB = 13;  // D <= 416: two 416 x 32 FP64 panels fill 208 KB of shared memory
+constexpr int TILE = 1024;
+// bank swizzle: conflict-free for DMMA fragments (rows 8f+g, cols 4ks+t), for one column across 16
+// consecutive rows (transposed panel loads / write-back / bordered row) and for one row across lanes
+__device__ __forceinline__ int sidx(int r, int c) { return r * 32 + (c ^ (((r & 3) << 2) | ((r >> 2) & 3))); }
+constexpr size_t smem_bytes() { return sizeof(double) * (2 * MAXB * TILE + TILE + MAXB * 32 + 8 + 32); }
+}  // namespace sw
+
+// Old column k of the symmetric matrix held in row-major packed storage -> pa (swizzled 32x32 tiles).
+// With `pivot` (the look-ahead result, already -P^-1) the pivot block is copied from it instead.
+__device__ __forceinline__ void sweep_load_panel(const double* S, int D, int nb, int k, double* pa, bool add_identity,
+                                                 const double* pivot) {
+  const int tid = threadIdx.x;
+  const int k0 = k * 32, kw = min(32, D - k0);
+  // rows above the pivot block: element (R, c) = S(k0 + c, R), R fastest (contiguous in row k0 + c)
+  for (int e = tid; e < k0 * kw; e += sw::NT) {
+    const int c = e / k0, R = e - c * k0;
+    cp_async8(&pa[(R >> 5) * sw::TILE + sw::sidx(R & 31, c)], S + packed_index(k0 + c, R), true);
+  }
+  for (int e = tid; e < k0 * (32 - kw); e += sw::NT) {  // columns past D (only when k is the last block)
+    const int c = kw + e / k0, R = e % k0;
+    pa[(R >> 5) * sw::TILE + sw::sidx(R & 31, c)] = 0.0;
+  }
+  // pivot block and rows below: element (R, c) = S(R, k0 + c) for R >= k0 + c, c fastest
+  const int rows = nb * 32 - k0;
+  for (int e = tid; e < rows * 32; e += sw::NT) {
+    const int r = e >> 5, c = e & 31, R = k0 + r, Cc = k0 + c;
+    double* dst = &pa[(R >> 5) * sw::TILE + sw::sidx(R & 31, c)];
+    if (pivot && r < 32) *dst = pivot[sw::sidx(r, c)];
+    else if (R >= D || Cc >= D) *dst = (R == Cc) ? 1.0 : 0.0;  // padding: identity pivot, zero rows
+    else if (R >= Cc) cp_async8(dst, S + packed_index(R, Cc), true);
+    else cp_async8(dst, S + packed_index(Cc, R), true);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (add_identity && tid < kw) pa[k * sw::TILE + sw::sidx(tid, tid)] += 1.0;
+  __syncthreads();
+}
+
+// In-place scalar sweep of the 32x32 pivot block by ONE warp (lane c holds column c in registers;
+// row p is broadcast through shared memory): pk <- -P^-1.  Returns the sum of log pivots through
+// *ldet and sets *bad when a pivot is not positive (the block is then garbage, the caller stops).
+__device__ __forceinline__ void sweep_pivot_warp(double* pk, double* rowbuf, double* ldet, int* bad, int lane) {
+  double a[32];
+#pragma unroll
+  for (int r = 0; r < 32; r++) a[r] = pk[sw::sidx(r, lane)];
+  double piv = 1.0;
+#pragma unroll
+  for (int p = 0; p < 32; p++) {
+    rowbuf[lane] = a[p];  // row p == column p (symmetric)
+    __syncwarp();
+    const double d = rowbuf[p];
+    const double inv = 1.0 / d;
+    const double apc = a[p] * inv;
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+      if (r == p) continue;
+      const double arp = rowbuf[r];
+      a[r] = (lane == p) ? arp * inv : fma(-arp, apc, a[r]);
+    }
+    a[p] = (lane == p) ? -inv : apc;
+    if (lane == p) piv = d;
+    __syncwarp();
+  }
+#pragma unroll
+  for (int r = 0; r < 32; r++) pk[sw::sidx(r, lane)] = a[r];
+  const double l = warp_sum(log(piv));
+  const unsigned nonpos = __ballot_sync(0xffffffffu, !(piv > 0.0));
+  if (lane == 0) {
+    *ldet += l;
+    if (nonpos) *bad = 1;
+  }
+}
+
+// acc(32x32) += sign * X_i * Y_j^T with X_i, Y_j swizzled 32x32 smem tiles; nfi/nfj/nks limit the
+// 8-row fragments and 4-wide k-steps to the live part of a partial last block.
+__device__ __forceinline__ void sweep_tile_mma(double (&acc)[4][4][2], const double* X, const double* Y, int nfi,
+                                               int nfj, int nks, double sign, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 8; ks++) {
+    if (ks >= nks) break;
+    double a[4], b[4];
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+      a[f] = sign * X[sw::sidx(8 * f + g, 4 * ks + t)];
+      b[f] = Y[sw::sidx(8 * f + g, 4 * ks + t)];
+    }
+#pragma unroll
+    for (int fi = 0; fi < 4; fi++) {
+      if (fi >= nfi) break;
+#pragma unroll
+      for (int fj = 0; fj < 4; fj++)
+        if (fj < nfj) dmma884(acc[fi][fj][0], acc[fi][fj][1], a[fi], b[fj]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double* lpk, double* mpk,
+                                                                    const double* bvec, int U, int D, int flags,
+                                                                    double* phi_out, double* logdet_out,
+                                                                    double* bphi_out, int32_t* status) {
+  extern __shared__ __align__(16) double sm[];
+  double* pa = sm;                        // [MAXB][1024] old column panel (pivot block -> -P^-1)
+  double* pb = pa + sw::MAXB * sw::TILE;  // [MAXB][1024] new column panel B
+  double* vr = pb + sw::MAXB * sw::TILE;  // [nb*32 + 1] bordered row (b -> phi), corner at nb*32
+  double* bd = vr + sw::MAXB * 32 + 8;    // [32] bordered row of B
+  double* pnext = bd + 32;                // [1024] look-ahead pivot: block k+1 after step k, then -P^-1
+  __shared__ double rowbuf[32];
+  __shared__ int tile_ctr;
+  __shared__ int bad;
+  __shared__ double ldet;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nb = (D + 31) / 32, ntile = nb * (nb + 1) / 2;
+  const int nupd = 2 * ((nb - 1) * nb / 2);  // update half-tiles per step
+  const int64_t P = packed_size(D);
+  const bool moment = (flags & TVK_POST_MOMENT) && bvec;
+#ifdef TVK_SWEEP_PROF
+  long long swp_prev = clock64();
+#endif
+  const int rank = sw::CL > 1 ? (int)tc::cluster_ctarank() : 0, ncl = gridDim.x / sw::CL;
+  for (int u = blockIdx.x / sw::CL; u < U; u += ncl) {
+    const double* Lu = lpk + (int64_t)u * P;
+    double* Mu = mpk + (int64_t)u * P;
+    for (int i = tid; i <= nb * 32; i += sw::NT) vr[i] = (bvec && i < D) ? bvec[(int64_t)u * D + i] : 0.0;
+    if (tid == 0) {
+      bad = 0;
+      ldet = 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < nb; k++) {
+      const double* S = k == 0 ? Lu : Mu;
+      const bool addI = k == 0 && (flags & TVK_POST_ADD_IDENTITY);
+      const bool last = k == nb - 1;
+      const int k0 = k * 32;
+      const int nks = min(8, (D - k0 + 3) / 4);
+      SWP(5);
+      if (bad) break;  // uniform (a failed look-ahead pivot of step k-1)
+      sweep_load_panel(S, D, nb, k, pa, addI, k > 0 ? pnext : nullptr);
+      SWP(0);
+      double* pk = pa + k * sw::TILE;
+      if (k == 0) {  // later pivots are swept ahead, during the previous step's tile updates
+        if (warp == 0) sweep_pivot_warp(pk, rowbuf, &ldet, &bad, lane);
+        __syncthreads();
+      }
+      SWP(1);
+      if (bad) break;  // uniform
+      // B_i = A_old_i P^-1 = -(pa_i pk) for the other blocks; the bordered row by the last warp
+      for (int i = warp; i < nb; i += sw::NWARP) {
+        if (i == k) continue;
+        double acc[4][4][2];
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+        const int nfi = min(4, (D - i * 32 + 7) / 8);
+        if (nfi == 4 && nks == 8)
+          sweep_tile_mma(acc, pa + i * sw::TILE, pk, 4, 4, 8, -1.0, lane);
+        else
+          sweep_tile_mma(acc, pa + i * sw::TILE, pk, nfi, 4, nks, -1.0, lane);
+        double* dst = pb + i * sw::TILE;
+#pragma unroll
+        for (int fi = 0; fi < 4; fi++)
+#pragma unroll
+          for (int fj = 0; fj < 4; fj++) {
+            dst[sw::sidx(8 * fi + g, 8 * fj + 2 * t)] = acc[fi][fj][0];
+            dst[sw::sidx(8 * fi + g, 8 * fj + 2 * t + 1)] = acc[fi][fj][1];
+          }
+      }
+      if (tid == 0) tile_ctr = 0;  // read after the barrier below
+      if (bvec && warp == sw::NWARP - 1) {
+        // bd = b_k P^-1 = -(b_k . pk); corner -= bd . b_k (before b_k is replaced by bd)
+        double s = 0.0;
+        for (int c = 0; c < 32; c++) s -= vr[k0 + c] * pk[sw::sidx(c, lane)];
+        bd[lane] = s;
+        const double cs = warp_sum(s * vr[k0 + lane]);
+        if (lane == 0) vr[nb * 32] -= cs;
+      }
+      __syncthreads();
+      SWP(2);
+      if (bvec) {  // vr_j -= bd . A_old(j, k-block) outside the pivot block; vr_k <- bd
+        // thread per row, column order rotated by the row so the 16 rows of a half-warp hit 16 banks
+        for (int j = tid; j < nb * 32; j += sw::NT) {
+          const int jb = j >> 5;
+          if (jb == k) {
+            vr[j] = bd[j - k0];
+            continue;
+          }
+          const double* row = pa + jb * sw::TILE;
+          double s = 0.0;
+#pragma unroll 8
+          for (int c = 0; c < 32; c++) s = fma(bd[c], row[sw::sidx(j & 31, c)], s);
+          vr[j] -= s;
+        }
+      }
+      if (last) __syncthreads();  // phi final before the M epilogue reads it
+      SWP(3);
+      // Tile updates A_ij -= B_i A_old_j^T (i, j != k), whole 32x32 tiles handed out by a shared-memory
+      // counter (dynamic balance).  Look-ahead: warp 0 first updates the next pivot block (k+1, k+1),
+      // keeps it in pnext and sweeps it (-P_{k+1}^-1 is ready when the next step starts), then joins.
+      const bool ahead = !last;
+      const int skip = ahead ? k * (k + 1) / 2 + k : -1;  // reduced index of tile (k+1, k+1)
+      const int ntask = (nb - 1) * nb / 2 - (ahead ? 1 : 0);
+      if (ahead && warp == 0) {
+        const int I0 = k0 + 32;
+        const int nf = min(4, (D - I0 + 7) / 8);
+        double acc[4][4][2];
+#pragma unroll
+        for (int fi = 0; fi < 4; fi++)
+#pragma unroll
+          for (int fj = 0; fj < 4; fj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int r = 8 * fi + g, c = 8 * fj + 2 * t + h, R = I0 + r, Cc = I0 + c;
+              double x = 0.0;
+              if (R < D && Cc <= R) x = S[packed_index(R, Cc)] + ((addI && R == Cc) ? 1.0 : 0.0);
+              acc[fi][fj][h] = x;
+            }
+        sweep_tile_mma(acc, pb + (k + 1) * sw::TILE, pa + (k + 1) * sw::TILE, nf, nf, nks, -1.0, lane);
+#pragma unroll
+        for (int fi = 0; fi < 4; fi++)
+#pragma unroll
+          for (int fj = 0; fj < 4; fj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int r = 8 * fi + g, c = 8 * fj + 2 * t + h, R = I0 + r, Cc = I0 + c;
+              if (c > r) continue;
+              const double v = acc[fi][fj][h];
+              if (R < D) {
+                if (rank == 0) Mu[packed_index(R, Cc)] = v;
+                pnext[sw::sidx(r, c)] = v;
+                pnext[sw::sidx(c, r)] = v;
+              } else {  // padding of a partial last block: identity pivot
+                pnext[sw::sidx(r, c)] = (r == c) ? 1.0 : 0.0;
+                pnext[sw::sidx(c, r)] = (r == c) ? 1.0 : 0.0;
+              }
+            }
+        __syncwarp();
+        sweep_pivot_warp(pnext, rowbuf, &ldet, &bad, lane);
+      }
+      // column-k write-back: (i,k) <- B_i, (k,j) <- B_j^T, (k,k) <- -P^-1
+      for (int i = ahead ? warp - 1 : warp; i < nb && (!ahead || warp > 0); i += ahead ? sw::NWARP - 1 : sw::NWARP) {
+        if (i % sw::CL != rank) continue;
+        const int I0 = i * 32;
+        for (int e = lane; e < 1024; e += 32) {
+          const int r = e >> 5, c = e & 31;
+          int R, Cc;
+          double v;
+          if (i > k) {
+            R = I0 + r, Cc = k0 + c;
+            v = pb[i * sw::TILE + sw::sidx(r, c)];
+          } else if (i < k) {
+            R = k0 + r, Cc = I0 + c;
+            v = pb[i * sw::TILE + sw::sidx(c, r)];
+          } else {
+            if (c > r) continue;
+            R = k0 + r, Cc = k0 + c;
+            v = pk[sw::sidx(r, c)];
+          }
+          if (R >= D || Cc >= D) continue;
+          if (last) v = -v + (moment ? vr[R] * vr[Cc] : 0.0);
+          Mu[packed_index(R, Cc)] = v;
+        }
+      }
+      for (;;) {
+        int m = 0;
+        if (lane == 0) m = atomicAdd(&tile_ctr, 1);
+        m = __shfl_sync(0xffffffffu, m, 0) * sw::CL + rank;
+        if (m >= ntask) break;
+        if (m >= skip && skip >= 0) m++;
+        int i = (int)((sqrt(8.0 * m + 1.0) - 1.0) * 0.5);
+        while ((i + 1) * (i + 2) / 2 <= m) i++;
+        while (i * (i + 1) / 2 > m) i--;
+        int j = m - i * (i + 1) / 2;
+        i += i >= k;
+        j += j >= k;
+        const int I0 = i * 32, J0 = j * 32;
+        const bool dg = i == j;
+        // element (R, J0 + 8fj + 2t + h) of row R = I0 + 8fi + g sits at rowoff[fi] + 8fj + h
+        int64_t rowoff[4];
+#pragma unroll
+        for (int fi = 0; fi < 4; fi++) rowoff[fi] = packed_index(I0 + 8 * fi + g, J0 + 2 * t);
+        double acc[4][4][2];
+#pragma unroll
+        for (int fi = 0; fi < 4; fi++) {
+          const double* rp = S + rowoff[fi];
+#pragma unroll
+          for (int fj = 0; fj < 4; fj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int R = I0 + 8 * fi + g, Cc = J0 + 8 * fj + 2 * t + h;
+              double x = 0.0;
+              if (R < D && Cc < D && (!dg || Cc <= R)) x = rp[8 * fj + h];
+              acc[fi][fj][h] = x;
+            }
+        }
+        if (addI && dg) {  // L = Lpk + I (first step only)
+#pragma unroll
+          for (int fi = 0; fi < 4; fi++)
+#pragma unroll
+            for (int fj = 0; fj < 4; fj++)
+#pragma unroll
+              for (int h = 0; h < 2; h++)
+                if (8 * fi + g == 8 * fj + 2 * t + h) acc[fi][fj][h] += 1.0;
+        }
+        const int nfi = min(4, (D - I0 + 7) / 8), nfj = min(4, (D - J0 + 7) / 8);
+        if (nfi == 4 && nfj == 4 && nks == 8)
+          sweep_tile_mma(acc, pb + i * sw::TILE, pa + j * sw::TILE, 4, 4, 8, -1.0, lane);
+        else
+          sweep_tile_mma(acc, pb + i * sw::TILE, pa + j * sw::TILE, nfi, nfj, nks, -1.0, lane);
+#pragma unroll
+        for (int fi = 0; fi < 4; fi++) {
+          double* wp = Mu + rowoff[fi];
+#pragma unroll
+          for (int fj = 0; fj < 4; fj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int R = I0 + 8 * fi + g, Cc = J0 + 8 * fj + 2 * t + h;
+              if (R >= D || Cc >= D || (dg && Cc > R)) continue;
+              double v = acc[fi][fj][h];
+              if (last) v = -v + (moment ? vr[R] * vr[Cc] : 0.0);
+              wp[8 * fj + h] = v;
+            }
+        }
+      }
+      (void)ntile;
+      if (sw::CL > 1) tc::cluster_sync();  // both CTAs' tiles are in global memory before the next panel load
+      else __syncthreads();
+      SWP(4);
+    }
+    if (rank == 0) {
+      if (tid == 0 && status) status[u] = bad ? TVK_ITEM_NOT_SPD : TVK_ITEM_OK;
+      if (!bad) {
+        for (int i = tid; i < D; i += sw::NT)
+          if (phi_out) phi_out[(int64_t)u * D + i] = vr[i];
+        if (tid == 0) {
+          if (logdet_out) logdet_out[u] = ldet;
+          if (bphi_out) bphi_out[u] = -vr[nb * 32];
+        }
+      }
+    }
+    if (sw::CL > 1) tc::cluster_sync();  // a failed matrix left its step loop early: resynchronize
+    else __syncthreads();
+  }
+}
+
 static int resident_ctas(int items) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -444,6 +835,29 @@ extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, i
     if (bphi) cudaMemsetAsync(bphi, 0, sizeof(double) * U, st);
     if (status) cudaMemsetAsync(status, 0, sizeof(int32_t) * U, st);
     TVK_CHECK_LAUNCH("posterior D=0");
+    return TVK_OK;
+  }
+  if (D <= 32 * sw::MAXB && !getenv("TVK_POSTERIOR_CHOL")) {
+    // one block-sweep pass gives Phi, phi and log|L| together; without mpk it works in place in lpk
+    // (the same arithmetic either way, so extraction and the EM posterior agree bit for bit)
+    const size_t ssm = sw::smem_bytes();
+    cudaFuncSetAttribute(sweep_posterior_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(sw::CL * ((resident_ctas(sw::CL * U) + sw::CL - 1) / sw::CL)));
+    cfg.blockDim = dim3(sw::NT);
+    cfg.dynamicSmemBytes = ssm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = sw::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, sweep_posterior_kernel, lpk, mpk ? mpk : const_cast<double*>(lpk),
+                                              b, U, D, flags, phi, logdet, bphi, status);
+    TVK_REQUIRE(le == cudaSuccess, "sweep_posterior: cluster launch failed");
+    TVK_CHECK_LAUNCH("sweep_posterior");
     return TVK_OK;
   }
   size_t smem = kernel_smem(D);
