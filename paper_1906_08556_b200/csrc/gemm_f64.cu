@@ -104,7 +104,7 @@ __global__ void splitk_reduce(GemmArgs p) {
   }
 }
 
-using BigCfg = GemmCfg<128, 128, 32, 2, 4, 3>;
+using BigCfg = GemmCfg<64, 64, 16, 2, 2, 3>;  // 4 CTAs (16 warps) per SM
 using SmallCfg = GemmCfg<64, 64, 16, 2, 2, 3>;
 
 template <class Cfg, bool TA, bool TB, bool VEC>
@@ -132,8 +132,8 @@ static int launch_cfg(const GemmArgs& p, cudaStream_t st) {
 
 template <bool TA, bool TB, bool VEC>
 static int launch_t(const GemmArgs& p, cudaStream_t st) {
-  int64_t big_tiles = (int64_t)ceil_div(p.M, 128) * ceil_div(p.N, 128) * p.batch * p.splits;
-  bool big = p.M >= 96 && p.N >= 96 && big_tiles >= 148;
+  int64_t big_tiles = (int64_t)ceil_div(p.M, 64) * ceil_div(p.N, 64) * p.batch * p.splits;
+  bool big = p.M >= 48 && p.N >= 48 && big_tiles >= 148;
   return big ? launch_cfg<BigCfg, TA, TB, VEC>(p, st) : launch_cfg<SmallCfg, TA, TB, VEC>(p, st);
 }
 
