@@ -111,10 +111,11 @@ int tvk_full_table(const double* weights, const double* means, const double* cov
                    double* table, int32_t* status, void* stream);
 
 /* Per-component whitening table for the grouped (default) path, stride tvk_precision_table_stride(F)
- * = 64*64 + 64 + 4 doubles: [U_c = L_c^-T (Sigma_c = L_c L_c^T; upper triangular, zero padded to
- * 64 x 64) | mu_c (zero padded to 64) | log w_c - (F log 2pi + log|Sigma_c|)/2 | 0 0 0], so that
- * ll_c(x) = const_c - ||(x - mu_c) U_c||^2 / 2 (gmm.py:111-118's Cholesky + triangular solve).
- * F <= 64.  status as above. */
+ * doubles.  F <= 64: 64*64 + 64 + 4 = [U_c = L_c^-T (Sigma_c = L_c L_c^T; upper triangular, zero
+ * padded to 64 x 64) | mu_c (zero padded to 64) | log w_c - (F log 2pi + log|Sigma_c|)/2 | 0 0 0],
+ * so that ll_c(x) = const_c - ||(x - mu_c) U_c||^2 / 2 (gmm.py:111-118's Cholesky + triangular
+ * solve).  64 < F <= 128: F(F+1)/2 + F + 2 = [L_c^-1 column-packed lower (column m holds rows
+ * m..F-1) | mu_c | const_c | 0].  status as above. */
 int tvk_precision_table(const double* weights, const double* means, const double* covariances, int C, int F,
                         double* table, int32_t* status, void* stream);
 int64_t tvk_precision_table_stride(int F);
@@ -124,7 +125,10 @@ int64_t tvk_precision_table_stride(int F);
 /* Scratch bytes tvk_align_frames needs for T frames, top-K K and C components (either mode). */
 int64_t tvk_align_workspace_bytes(int64_t T, int K, int C);
 
-/* Sparse frame alignment (gmm.py:389-439) of frames x (T x F, f32 or f64 if x_f64): diagonal top-K
+/* Shape envelope: 1 <= K <= min(C, 8192), F <= 128, C <= 24576 (TVK_ERR_INVALID outside).  K <= 32
+ * with F <= 63 runs the tensor-core preselection and F <= 64 the DMMA whitening; other shapes run
+ * the generic kernels of align_wide.cu (same outputs).  TVK_ALIGN_DENSE needs K <= 32, F <= 96.
+ * Sparse frame alignment (gmm.py:389-439) of frames x (T x F, f32 or f64 if x_f64): diagonal top-K
  * preselection (stable, lower index wins ties), full-covariance log-likelihoods of the selected
  * components, softmax over the selection, prune (post >= prune), degenerate rule (argmax in
  * selection order), renormalize, entries sorted by component within a frame.

@@ -122,6 +122,16 @@ def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True, den
     T, F = x.shape
     C = diag_tab.C
     k = min(top_k, C)
+    if k > 32 and T * k > WIDE_PAIRS and not debug:
+        # wide top_k: bound the (T x k) workspace by aligning frame chunks and joining the CSRs
+        step = max(1, WIDE_PAIRS // k)
+        parts = [align(x[i:i + step], diag_tab, full_tab, k, prune, dense=dense) for i in range(0, T, step)]
+        bases = np.cumsum([0] + [p.n_entries for p in parts])
+        offsets = torch.cat([p.offsets[:-1] + int(b) for p, b in zip(parts, bases[:-1])] +
+                            [torch.tensor([int(bases[-1])], dtype=torch.int64, device=x.device)])
+        comps = torch.cat([p.components[:p.n_entries] for p in parts])
+        wts = torch.cat([p.weights[:p.n_entries] for p in parts])
+        return AlignResult(offsets, comps, wts, int(bases[-1]))
     offsets = _lib.empty((T + 1,), torch.int64)
     comps = _lib.empty((max(T * k, 1),), torch.int32)
     wts = _lib.empty((max(T * k, 1),), torch.float32)
@@ -142,6 +152,7 @@ def align(x, diag_tab, full_tab, top_k, prune, debug=False, sync_count=True, den
 
 
 STREAM_CHUNK = 1 << 19  # frames per chunk of the host-input alignment pipeline
+WIDE_PAIRS = 1 << 24    # (frame, component) pairs per align() call / host piece when top_k > 32
 N_SLOTS = 4             # pinned result staging slots = pieces whose host unstaging may run concurrently
 RAMP_PIECE = 1 << 17    # first / last pieces of the host pipeline (only their copies cannot overlap)
 _staging = {}             # (chunk, k) -> pinned host staging slots, reused across calls
@@ -178,7 +189,7 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
         host = torch.from_numpy(np.ascontiguousarray(arr))
     host = host.contiguous()
     k = min(top_k, diag_tab.C)
-    chunk = min(chunk, T)
+    chunk = min(chunk, T, max(1, WIDE_PAIRS // k))
     offsets = np.empty(T + 1, np.int64)
     comps = np.empty(T * k, np.int32)   # untouched capacity is never paged in
     wts = np.empty(T * k, np.float32)

@@ -566,7 +566,8 @@ static int launch_select(const XT* x, int64_t T, int F, const double* diag_table
                          double* val, cudaStream_t st) {
   if (select_tc_supported(F, K, C) && !select_dmma_forced()) return select_tc<XT>(x, T, F, diag_table, C, K, sel, val, st);
   size_t smem = sel::smem_bytes(F, K);
-  TVK_REQUIRE(smem <= 227 * 1024, "align_frames: F too large for the preselection tile");
+  // shapes outside both fast kernels (top_k > 32, wide F): the generic per-frame selection
+  if (K > kMaxTopK || smem > 227 * 1024) return wide_select<XT>(x, T, F, diag_table, C, K, sel, val, st);
   cudaFuncSetAttribute(select_topk_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int64_t grid = (T + sel::BM - 1) / sel::BM;
   TVK_REQUIRE(grid < (1ll << 31), "align_frames: too many frames for one call");
@@ -599,6 +600,7 @@ static int full_ll_dispatch(const XT* x, int64_t T, int F, const double* full_ta
                             int64_t group_bytes, cudaStream_t st) {
   if (flags & TVK_ALIGN_DENSE) {
     TVK_REQUIRE(full_table != nullptr, "align_frames: dense mode needs the quadratic-feature table");
+    TVK_REQUIRE(K <= kMaxTopK, "align_frames: dense mode supports top_k <= 32");
     return launch_full_ll<XT>(x, T, F, full_table, C, K, sel, sel_ll, st);
   }
   TVK_REQUIRE(prec_table != nullptr, "align_frames: grouped mode needs the precision table");
@@ -643,7 +645,7 @@ static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, c
   TVK_REQUIRE(workspace != nullptr && (int64_t)w.bytes <= workspace_bytes, "align_frames: workspace too small");
   TVK_TRY(launch_select<XT>(x, T, F, diag_table, C, K, w.sel, nullptr, st));
   int fb = (int)((T + 127) / 128);
-  if (!(flags & TVK_ALIGN_DENSE) && sel_ll_out == nullptr && !sparse_disabled()) {
+  if (!(flags & TVK_ALIGN_DENSE) && sel_ll_out == nullptr && !sparse_disabled() && K <= kMaxTopK && F <= 64) {
     // FP64 log-likelihoods only where the kept set or its weights need them
     TVK_REQUIRE(prec_table != nullptr, "align_frames: grouped mode needs the precision table");
     TVK_TRY(grouped_align_sparse<XT>(x, T, F, prec_table, C, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad,
@@ -651,8 +653,12 @@ static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, c
   } else {
     TVK_TRY(full_ll_dispatch<XT>(x, T, F, full_table, prec_table, C, K, flags, w.sel, w.sel_ll, w.group,
                                  w.group_bytes, st));
-    finalize_kernel<<<fb, 128, 0, st>>>(T, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts);
-    TVK_CHECK_LAUNCH("finalize");
+    if (K <= kMaxTopK) {
+      finalize_kernel<<<fb, 128, 0, st>>>(T, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts);
+      TVK_CHECK_LAUNCH("finalize");
+    } else {
+      TVK_TRY(finalize_wide(T, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts, st));
+    }
   }
   TVK_TRY(exclusive_scan_counts(w.counts, T, offsets, w.block_sums, st));
   compact_kernel<<<fb, 128, 0, st>>>(T, K, offsets, w.comp_pad, w.w_pad, components, weights);
@@ -672,8 +678,9 @@ extern "C" int tvk_align_frames(const void* x, int x_f64, int64_t T, int F, cons
                                 void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1, "align_frames: bad shape");
-  TVK_REQUIRE(K >= 1 && K <= kMaxTopK && K <= C, "align_frames: top_k must be in [1, min(C, 32)]");
-  TVK_REQUIRE(F <= 255, "align_frames: F too large");
+  TVK_REQUIRE(K >= 1 && K <= kWideMaxK && K <= C, "align_frames: top_k must be in [1, min(C, 8192)]");
+  TVK_REQUIRE(F <= kWideMaxF, "align_frames: F must be <= 128");
+  TVK_REQUIRE(C <= kGroupedMaxC, "align_frames: C must be <= 24576");
   if (T == 0) {
     cudaMemsetAsync(offsets, 0, sizeof(int64_t), st);
     TVK_CHECK_LAUNCH("align_frames memset");
@@ -690,7 +697,7 @@ extern "C" int tvk_select_topk(const void* x, int x_f64, int64_t T, int F, const
                                int32_t* selected, double* values, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1, "select_topk: bad shape");
-  TVK_REQUIRE(K >= 1 && K <= kMaxTopK && K <= C, "select_topk: k must be in [1, min(C, 32)]");
+  TVK_REQUIRE(K >= 1 && K <= kWideMaxK && K <= C, "select_topk: k must be in [1, min(C, 8192)]");
   if (T == 0) return TVK_OK;
   if (x_f64) return launch_select<double>((const double*)x, T, F, diag_table, C, K, selected, values, st);
   return launch_select<float>((const float*)x, T, F, diag_table, C, K, selected, values, st);
@@ -718,7 +725,7 @@ extern "C" int tvk_full_loglik_selected(const void* x, int x_f64, int64_t T, int
                                         const double* prec_table, int C, int K, int flags, const int32_t* selected,
                                         double* sel_ll, void* workspace, int64_t workspace_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1 && K >= 1 && K <= kMaxTopK && K <= C, "full_loglik_selected: bad shape");
+  TVK_REQUIRE(T >= 0 && F >= 1 && C >= 1 && K >= 1 && K <= kWideMaxK && K <= C, "full_loglik_selected: bad shape");
   if (T == 0) return TVK_OK;
   if (x_f64)
     return full_ll_dispatch<double>((const double*)x, T, F, full_table, prec_table, C, K, flags, selected, sel_ll,

@@ -96,7 +96,7 @@ __global__ void pair_hist_kernel(const int32_t* sel, const uint8_t* need, int64_
 }
 
 __global__ void hist_scan_kernel(int* hist, int C, int* start, int* cursor) {
-  // single CTA exclusive scan of C counters (C <= 8192)
+  // single CTA exclusive scan of C counters
   __shared__ int part[1024];
   const int per = (C + blockDim.x - 1) / blockDim.x;
   const int lo = threadIdx.x * per, hi = min(lo + per, C);
@@ -369,6 +369,14 @@ static int launch_whiten(const XT* x, int F, const double* tab, int K, const Gro
   return TVK_OK;
 }
 
+// the bucketing kernels' dynamic shared memory grows with C: allow the largest supported C once
+// (lowering the limit to one call's C would break a later call with a larger C)
+static void set_sort_smem_limits() {
+  cudaFuncSetAttribute(pair_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(int) * 2 * kGroupedMaxC));
+  cudaFuncSetAttribute(pair_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int) * kGroupedMaxC));
+}
+
 // bucket the window's pairs (optionally only those with need[p]) by component into <=128-pair tiles
 static int sort_tiles(const int32_t* wsel, const uint8_t* need, int64_t np, int C, const GroupWs& w,
                       cudaStream_t st) {
@@ -387,14 +395,15 @@ static int sort_tiles(const int32_t* wsel, const uint8_t* need, int64_t np, int 
 template <typename XT>
 int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, int K, const int32_t* sel,
                     double* sel_ll, void* ws_base, int64_t ws_bytes, cudaStream_t st) {
-  TVK_REQUIRE(F <= GP, "grouped full log-likelihood supports F <= 64");
-  TVK_REQUIRE(K >= 1 && K <= 32, "grouped full log-likelihood supports K <= 32");
-  TVK_REQUIRE(C <= 8192, "grouped full log-likelihood supports C <= 8192");
+  TVK_REQUIRE(F <= kWideMaxF, "full log-likelihood supports F <= 128");
+  TVK_REQUIRE(K >= 1 && K <= kWideMaxK, "full log-likelihood supports top_k <= 8192");
+  TVK_REQUIRE(C <= kGroupedMaxC, "full log-likelihood supports C <= 24576");
   const int64_t n_pairs = T * K;
   TVK_REQUIRE(n_pairs < (1ll << 31) - 1, "too many (frame, component) pairs for one call");
   // frame windows sized so the window's frames and the whitening table stay L2-resident while the
-  // window's pairs (sorted by component, i.e. random in frame order) gather their frame rows
-  const int64_t win = std::min<int64_t>(T, kGroupWindowFrames);
+  // window's pairs (sorted by component, i.e. random in frame order) gather their frame rows; a
+  // window holds at most kGroupWindowFrames * 32 pairs (frame = pair / K stays exact, see kinv)
+  const int64_t win = std::min<int64_t>(T, K <= 32 ? kGroupWindowFrames : std::max<int64_t>(1, kGroupWindowFrames * 32 / K));
   const int nwin = (int)((T + win - 1) / win);
   // windows alternate between the caller's stream and a second one, each with its own workspace set,
   // so one window's pair sort and kernel ramp overlap the previous window's whitening tail
@@ -403,8 +412,7 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
   TVK_REQUIRE(ws_base != nullptr && (int64_t)w[0].bytes * (nwin > 1 ? 2 : 1) <= ws_bytes,
               "grouped full log-likelihood: workspace too small");
   if (nwin > 1) w[1] = group_carve((char*)ws_base + w[0].bytes, win * K, C);
-  size_t sc_smem = sizeof(int) * 2 * C;
-  cudaFuncSetAttribute(pair_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
+  set_sort_smem_limits();
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -431,8 +439,12 @@ int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, in
     // the kernel reads the tile count from tile_start[C]
     GroupWs wc = wi;
     wc.tile_start = wi.tile_start + C;
-    rc = vec ? launch_whiten<XT, true>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s)
-             : launch_whiten<XT, false>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s);
+    if (F > GP)  // wide features: FMA whitening of the same component tiles (align_wide.cu)
+      rc = wide_whiten<XT>(x + f0 * F, F, ptab, K, wi.sorted, wi.tiles, wc.tile_start, np / GROWS + C + 1,
+                           sel_ll + f0 * K, s);
+    else
+      rc = vec ? launch_whiten<XT, true>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s)
+               : launch_whiten<XT, false>(x + f0 * F, F, ptab, K, wc, sel_ll + f0 * K, sms, s);
     if (rc != TVK_OK) break;
   }
   if (s2) {  // always join, also after an error
@@ -708,7 +720,7 @@ int grouped_align_sparse(const XT* x, int64_t T, int F, const double* ptab, int 
   const int64_t win = std::min<int64_t>(T, kGroupWindowFrames);
   GroupWs w = group_carve(ws_base, win * K, C);
   TVK_REQUIRE(ws_base != nullptr && (int64_t)w.bytes <= ws_bytes, "grouped full log-likelihood: workspace too small");
-  cudaFuncSetAttribute(pair_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int) * 2 * C));
+  set_sort_smem_limits();
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -750,7 +762,8 @@ template int grouped_full_ll<double>(const double*, int64_t, int, const double*,
 
 extern "C" int tvk_precision_table(const double* weights, const double* means, const double* covariances, int C,
                                    int F, double* table, int32_t* status, void* stream) {
-  TVK_REQUIRE(C >= 1 && F >= 1 && F <= tvk::GP, "precision_table: need 1 <= F <= 64");
+  TVK_REQUIRE(C >= 1 && F >= 1 && F <= tvk::kWideMaxF, "precision_table: need 1 <= F <= 128");
+  if (F > tvk::GP) return tvk::wide_precision_table(weights, means, covariances, C, F, table, status, (cudaStream_t)stream);
   size_t smem = 2 * sizeof(double) * F * F;
   cudaFuncSetAttribute(tvk::whiten_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(2 * sizeof(double) * tvk::GP * tvk::GP));

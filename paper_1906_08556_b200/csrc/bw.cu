@@ -17,7 +17,7 @@
 namespace tvk {
 
 constexpr int kBwThreads = 256;
-constexpr int kBwMaxC = 8192;
+constexpr int kBwMaxC = 49152;  // first-order counting sort: C+1 ints of shared memory
 
 struct BwWs {
   int32_t* ent_frame;   // [Ecap] frame of each entry
@@ -177,18 +177,19 @@ __global__ void __launch_bounds__(kBwThreads) bw_first_order_kernel(
   }
 }
 
-constexpr int kSoBatch = 32;       // entries staged per round
-constexpr int kSoMaxPairs = 8;     // pairs per thread (F(F+1)/2 <= 8*256 -> F <= 63)
 constexpr int kSoUttChunk = 1024;  // utterance runs gathered per pass
+constexpr int kSoMaxF = 128;
 
-template <typename XT>
+// MP = lower-triangle pairs per thread: 8 covers F <= 63 (F(F+1)/2 <= 8*256), 33 covers F <= 128
+template <typename XT, int kSoMaxPairs>
 __global__ void __launch_bounds__(kBwThreads) bw_second_order_kernel(const XT* x, int F, int U, int C,
                                                                      const int64_t* utt_frames,
                                                                      const int64_t* ali_off, const double* center,
                                                                      double* ssum, BwWs ws) {
   __shared__ int run_s[kSoUttChunk], run_n[kSoUttChunk];
   __shared__ int64_t run_r0[kSoUttChunk];
-  __shared__ double xe[kSoBatch][64];
+  constexpr int kSoBatch = kSoMaxPairs > 8 ? 16 : 32;  // entries staged per round (48 KB static smem)
+  __shared__ double xe[kSoBatch][kSoMaxPairs > 8 ? kSoMaxF : 64];
   __shared__ double we[kSoBatch];
   const int c = blockIdx.x, tid = threadIdx.x;
   const int npair = F * (F + 1) / 2;
@@ -279,7 +280,7 @@ extern "C" int tvk_bw_stats(const void* x, int x_f64, int F, const int64_t* utt_
                             void* workspace, int64_t workspace_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TVK_REQUIRE(F >= 1 && C >= 1 && U >= 0, "bw_stats: bad shape");
-  TVK_REQUIRE(C <= kBwMaxC, "bw_stats: C > 8192 not supported");
+  TVK_REQUIRE(C <= kBwMaxC, "bw_stats: C > 49152 not supported");
   if (U == 0) return TVK_OK;
   TVK_REQUIRE(workspace != nullptr, "bw_stats: workspace required");
   TVK_REQUIRE((int64_t)bw_carve(nullptr, entry_capacity, U, C).bytes <= workspace_bytes,
@@ -299,13 +300,22 @@ extern "C" int tvk_bw_stats(const void* x, int x_f64, int F, const int64_t* utt_
   }
   TVK_CHECK_LAUNCH("bw_first_order");
   if (ssum_acc) {
-    TVK_REQUIRE(F <= 63, "bw_stats: corpus second order supports F <= 63");
-    if (x_f64)
-      bw_second_order_kernel<double><<<C, kBwThreads, 0, st>>>((const double*)x, F, U, C, utt_frames, ali_offsets,
-                                                               center, ssum_acc, ws);
-    else
-      bw_second_order_kernel<float><<<C, kBwThreads, 0, st>>>((const float*)x, F, U, C, utt_frames, ali_offsets,
-                                                              center, ssum_acc, ws);
+    TVK_REQUIRE(F <= kSoMaxF, "bw_stats: corpus second order supports F <= 128");
+    if (F <= 63) {
+      if (x_f64)
+        bw_second_order_kernel<double, 8><<<C, kBwThreads, 0, st>>>((const double*)x, F, U, C, utt_frames,
+                                                                    ali_offsets, center, ssum_acc, ws);
+      else
+        bw_second_order_kernel<float, 8><<<C, kBwThreads, 0, st>>>((const float*)x, F, U, C, utt_frames,
+                                                                   ali_offsets, center, ssum_acc, ws);
+    } else {
+      if (x_f64)
+        bw_second_order_kernel<double, 33><<<C, kBwThreads, 0, st>>>((const double*)x, F, U, C, utt_frames,
+                                                                     ali_offsets, center, ssum_acc, ws);
+      else
+        bw_second_order_kernel<float, 33><<<C, kBwThreads, 0, st>>>((const float*)x, F, U, C, utt_frames,
+                                                                    ali_offsets, center, ssum_acc, ws);
+    }
     TVK_CHECK_LAUNCH("bw_second_order");
   }
   return TVK_OK;

@@ -32,7 +32,12 @@ int spd_small(const double* A, int batch, int n, double* chol, double* inv, doub
 
 namespace tvk {
 // grouped (selected-only) full-covariance log-likelihoods, align_grouped.cu
-__host__ __device__ inline int64_t precision_stride(int) { return 64 * 64 + 64 + 4; }  // whitening table row
+// whitening table row: F <= 64 [U = L^-T 64x64 | mu 64 | const | pad]; F > 64 (wide path)
+// [column-packed L^-1 (F(F+1)/2) | mu F | const | pad]
+__host__ __device__ inline int64_t precision_stride(int F) {
+  return F <= 64 ? 64 * 64 + 64 + 4 : (int64_t)F * (F + 1) / 2 + F + 2;
+}
+constexpr int kGroupedMaxC = 24576;  // pair bucketing keeps 2 C counters in shared memory
 int64_t grouped_workspace_bytes(int64_t n_pairs, int C);
 template <typename XT>
 int grouped_full_ll(const XT* x, int64_t T, int F, const double* ptab, int C, int K, const int32_t* sel,
@@ -55,4 +60,20 @@ template <typename XT>
 int grouped_align_sparse(const XT* x, int64_t T, int F, const double* ptab, int C, int K, double prune,
                          const int32_t* sel, double* sel_ll, int32_t* comp_pad, float* w_pad, int64_t* counts,
                          void* ws_base, int64_t ws_bytes, cudaStream_t st);
+}  // namespace tvk
+
+namespace tvk {
+// alignment outside the fast path's envelope, align_wide.cu
+constexpr int kWideMaxK = 8192;
+constexpr int kWideMaxF = 128;
+template <typename XT>
+int wide_select(const XT* x, int64_t T, int F, const double* tab, int C, int K, int32_t* sel, double* val,
+                cudaStream_t st);
+int finalize_wide(int64_t T, int K, double prune, const int32_t* sel, const double* sel_ll, int32_t* comp_pad,
+                  float* w_pad, int64_t* counts, cudaStream_t st);
+int wide_precision_table(const double* w, const double* mu, const double* cov, int C, int F, double* tab,
+                         int32_t* status, cudaStream_t st);
+template <typename XT>
+int wide_whiten(const XT* x, int F, const double* ptab, int K, const int32_t* sorted, const int4* tiles,
+                const int* ntile_dev, int64_t max_tiles, double* sel_ll, cudaStream_t st);
 }  // namespace tvk

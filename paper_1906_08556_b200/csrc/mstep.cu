@@ -13,7 +13,7 @@
 
 namespace tvk {
 
-constexpr int kSigmaMaxF = 64;
+constexpr int kSigmaMaxF = 96;  // r, w, v (3 F^2 doubles) in shared memory: 221 KB at F = 96
 constexpr int ST = 256;
 
 // Parallel cyclic Jacobi on the symmetric n x n matrix a (shared, row stride n); v <- eigenvectors
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(ST) sigma_floor_kernel(const double* ssum, con
 
 extern "C" int tvk_sigma_floor(const double* ssum, const double* tb, const double* N, const double* sigma_old, int C,
                                int F, double floor_scale, double* sigma_out, int32_t* status, void* stream) {
-  TVK_REQUIRE(C >= 0 && F >= 1 && F <= tvk::kSigmaMaxF, "sigma_floor: F must be in [1, 64]");
+  TVK_REQUIRE(C >= 0 && F >= 1 && F <= tvk::kSigmaMaxF, "sigma_floor: F must be in [1, 96]");
   TVK_REQUIRE(status != nullptr, "sigma_floor: status array required");
   if (C == 0) return TVK_OK;
   size_t smem = 3 * sizeof(double) * F * F;

@@ -29,6 +29,7 @@ import numpy as np
 import torch
 
 from . import _device, _dist, _estep, _lib
+from . import gmm
 from .gmm import GmmDiag, GmmFull, SparseAlignment
 from .io_formats import load_model, read_alignment, read_matrix, save_model, write_alignment, write_matrix
 from .tvm import (AUGMENTED, DEFAULT_PRIOR_OFFSET, SIGMA_FLOOR_SCALE, STANDARD, EmAccumulators, TvModel,
@@ -457,6 +458,7 @@ class DeviceAlignment:
         """
         T = corpus.n_frames
         k = min(top_k, diag_tab.C)
+        gmm._check_envelope(k, diag_tab.F, diag_tab.C, "align_corpus")
         offsets = _lib.empty((T + 1,), torch.int64)
         cap = max(1, min(T * k, int(T * ENTRY_CAPACITY_PER_FRAME)))
         comps = _lib.empty((cap,), torch.int32)

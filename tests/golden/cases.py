@@ -26,7 +26,13 @@ ALIGN_CASES = [
     ("c64f20", 40, 64, 20, 0.5, 41, 2000, 1.5, 20, 0.025),
     ("c256f60", 50, 256, 60, 0.3, 51, 600, 1.2, 20, 0.025),
     ("c2048f60", 60, 2048, 60, 0.3, 61, 300, 1.2, 20, 0.025),
+    # outside the fast kernels' envelope (align_wide.cu): top_k > 32, F > 64, top_k == C, no pruning
+    ("c128f20_k40", 42, 128, 20, 0.5, 43, 1000, 1.5, 40, 0.025),
+    ("c64f80", 44, 64, 80, 0.3, 45, 500, 1.2, 20, 0.025),
+    ("c96f80_k48_noprune", 46, 96, 80, 0.3, 47, 300, 1.2, 48, 0.0),
+    ("c40f12_kall", 48, 40, 12, 1.0, 49, 400, 2.0, 40, 0.01),
 ]
+WIDE_ALIGN = ("c128f20_k40", "c64f80", "c96f80_k48_noprune", "c40f12_kall")
 
 TVM_CASES = [
     # name, formulation, seed, C, F, D, speakers, utts/spk, frames, within, rank
@@ -40,7 +46,12 @@ TRAIN_CASES = [
     ("aug", "augmented", 7, 8, 6, 4, 10, 3, (60, 100), 5, 3, True, True, False, 0),
     ("aug_realign", "augmented", 8, 8, 6, 4, 10, 3, (60, 100), 4, 3, True, True, False, 1),
     ("std_mean", "standard", 9, 8, 6, 4, 10, 3, (60, 100), 4, 3, True, False, True, 1),
+    # outside the fast kernels' envelope: 80-dim features (wide selection/whitening, F > 63 BW second
+    # order, F > 64 Sigma floor) and top_k = 40 (wide selection + finalize)
+    ("aug_f80", "augmented", 10, 8, 80, 4, 6, 2, (40, 60), 4, 2, True, True, False, 1),
+    ("aug_k40", "augmented", 11, 48, 6, 4, 6, 2, (60, 100), 4, 2, True, True, False, 1),
 ]
+TRAIN_TOPK = {"aug_k40": 40}  # top_k of the training runs (default 4)
 
 CONFIG1 = dict(n_comp=64, dim=20, rank=100, speakers=50, upc=4, frames=(300, 300), seed=0,
                within=0.3, iterations=5)
@@ -125,7 +136,7 @@ def train_inputs(case):
     (name, form, seed, c, f, d, spk, upc, frames, rank, iters, md, su, um, ri) = case
     cor = corpus(form, seed, c, f, d, spk, upc, frames, 0.5)
     cfg = SimpleNamespace(formulation=form, latent_dim=rank, iterations=iters, min_div=md,
-                          sigma_update=su, update_mean=um, realign_interval=ri, top_k=4,
+                          sigma_update=su, update_mean=um, realign_interval=ri, top_k=TRAIN_TOPK.get(name, 4),
                           prune=0.025, prior_offset=100.0, batch_size_utts=4)
     return cor, cfg
 

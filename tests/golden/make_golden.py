@@ -29,7 +29,7 @@ from tvkit import gmm as rgmm, pipeline as rpipe, synth as rsynth, tvm as rtvm  
 
 from oracle import tvkit_oracle as orc  # noqa: E402
 sys.path.insert(0, HERE)
-from cases import (ALIGN_CASES, TRAIN_CASES, TVM_CASES, UBM_CASES, UBM_EDGE_CASES, UBM_EDGE_ITERS,  # noqa: E402
+from cases import (ALIGN_CASES, TRAIN_CASES, TRAIN_TOPK, TVM_CASES, UBM_CASES, UBM_EDGE_CASES, UBM_EDGE_ITERS,  # noqa: E402
                    digest, ubm_edge_frames, ubm_frames)
 
 
@@ -67,8 +67,8 @@ def make_align():
             offsets=ali.offsets, components=ali.components, weights=ali.weights,
             selected=sel.astype(np.int32), boundary_gap=gap,
             sel_full_ll=np.take_along_axis(full.log_likelihoods(x), sel, axis=1),
-            n=bw.n, f=bw.f, S=bw.S if c <= 64 else np.zeros(0),
-            nc=bwc.n, fc=bwc.f, Sc=bwc.S if c <= 64 else np.zeros(0),
+            n=bw.n, f=bw.f, S=bw.S if c * f * f <= 100_000 else np.zeros(0),
+            nc=bwc.n, fc=bwc.f, Sc=bwc.S if c * f * f <= 100_000 else np.zeros(0),
         )
     flat = {f"{case}__{k}": v for case, d in out.items() for k, v in d.items()}
     save("align", **flat)
@@ -138,14 +138,15 @@ def make_train():
         ubm_full = gen.alignment_ubm_full()
         ubm_diag = gen.alignment_ubm_diag()
         cfg = rpipe.TrainConfig(formulation=form, latent_dim=rank, iterations=iters, min_div=md,
-                                sigma_update=su, update_mean=um, realign_interval=ri, top_k=4,
-                                prune=0.025, seeds=(0,), batch_size_utts=4, workers=1)
+                                sigma_update=su, update_mean=um, realign_interval=ri,
+                                top_k=TRAIN_TOPK.get(name, 4), prune=0.025, seeds=(0,), batch_size_utts=4,
+                                workers=1)
         store = rpipe.InMemoryFeatureStore(corpus.features)
         import warnings
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             model, metrics = rpipe.train_extractor(cfg, store, ubm_diag, ubm_full, seed=0)
-        ids, emb = rpipe.extract_corpus(model, store, top_k=4, prune=0.025)
+        ids, emb = rpipe.extract_corpus(model, store, top_k=TRAIN_TOPK.get(name, 4), prune=0.025)
         d_ = dict(T=model.T, Sigma=model.Sigma, prior=np.array(model.prior_offset),
                   ubm_means=model.ubm_means,
                   bias=model.bias if model.bias is not None else np.zeros(0),

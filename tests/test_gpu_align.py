@@ -60,6 +60,8 @@ def test_align_matches_reference_golden(gpu, case):
 def test_selection_and_full_ll_match_reference(gpu, case, dense):
     g = ALIGN[case[0]]
     diag, full, x, k, prune, _ = cases.align_inputs(case)
+    if dense and (k > 32 or x.shape[1] > 96):
+        pytest.skip("the dense quadratic-feature mode covers top_k <= 32, F <= 96")
     from paper_1906_08556_b200 import _device, _lib
     dm, fm = _models(diag, full)
     xd = _device.frames_to_device(x)

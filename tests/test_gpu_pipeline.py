@@ -51,7 +51,7 @@ def test_train_and_extract_match_reference_golden(gpu, case):
     assert _rel(model.Sigma, g["Sigma"]) < 1e-6
     np.testing.assert_allclose(model.prior_offset, float(g["prior"]), rtol=1e-9)
     np.testing.assert_allclose(model.ubm_means, g["ubm_means"], rtol=1e-6, atol=1e-9)
-    ids, emb = P.extract_corpus(model, store, top_k=4, prune=0.025)
+    ids, emb = P.extract_corpus(model, store, top_k=cfg_ns.top_k, prune=cfg_ns.prune)
     assert ids == sorted(cor.ids)
     assert _rel(emb, g["ivectors"]) < 1e-6
 
