@@ -390,6 +390,14 @@ def bench_ours(args):
             c5["extraction"] = bench_extract_leg(args, pkg, dev, rank, world, barrier, max_over_ranks,
                                                  args.extract_utts)
             log(f"[bench] config 5 extraction: {c5['extraction']['value']:.0f} utts/s")
+    c1 = None
+    if args.config1 and world == 1 and not args.no_cpu:
+        try:
+            c1 = bench_config1(pkg)
+            log(f"[bench] config 1: {c1['value']:.2f} s/run (reference algorithm on the host: "
+                f"{c1['cpu_baseline']['value']:.1f} s)")
+        except Exception as exc:  # reported leg: never kill the headline line
+            c1 = {"error": str(exc)}
     if args.config4_utts > 0:  # config 4: VoxCeleb scale (opt-in: ~1 min per iteration on one GPU)
         c4, _ = bench_em_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, "augmented", args.config4_utts,
                              1, 0, dict(iterations=10 ** 6, min_div=True, sigma_update=True, realign_interval=0),
@@ -464,6 +472,8 @@ def bench_ours(args):
             line["config5"] = c5
         if c4 is not None:
             line["config4"] = c4
+        if c1 is not None:
+            line["config1"] = c1
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -654,6 +664,92 @@ def bench_extract_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, n_gl
             "path": "pipeline extract (alignment + BW stats + posterior mean), frames in HBM, i-vectors to host"}
 
 
+C1 = dict(C=64, F=20, R=100, spk=50, upc=4, frames=300, iters=5, within=0.3)
+
+
+def config1_corpus(seed=1):
+    """BASELINE config 1 shape (64-comp UBM, 20-dim, R=100, 50 speakers x 4 utts x 300 frames), host
+    numpy, synth.py:90-147 recipe (augmented): w ~ Dir(10), mu ~ N(0, 8^2), Sigma = AA'/2F + 0.5 I,
+    T ~ N(0, 1) with T[:, :, 0] = mu / p; x = T_c (p e1 + w_spk) + Sigma_c^(1/2) e."""
+    c, f, r = C1["C"], C1["F"], C1["R"]
+    rng = np.random.default_rng(seed)
+    w = rng.dirichlet(np.full(c, 10.0))
+    mu = rng.normal(0.0, 8.0, (c, f))
+    a = rng.normal(0.0, 1.0, (c, f, 2 * f))
+    sig = np.einsum("cik,cjk->cij", a, a) / (2 * f) + 0.5 * np.eye(f)
+    T = rng.normal(0.0, 1.0, (c, f, r))
+    T[:, :, 0] = mu / P_OFF
+    L = np.linalg.cholesky(sig)
+    feats, ids = {}, []
+    for s_ in range(C1["spk"]):
+        zs = rng.normal(0.0, 1.0, r)
+        zs[0] += P_OFF
+        for u in range(C1["upc"]):
+            z = zs + C1["within"] * rng.normal(0.0, 1.0, r)
+            comp = rng.choice(c, p=w, size=C1["frames"])
+            m = np.einsum("cfr,r->cf", T, z)
+            x = m[comp] + np.einsum("tij,tj->ti", L[comp], rng.standard_normal((C1["frames"], f)))
+            uid = f"s{s_:03d}u{u}"
+            feats[uid] = x.astype(np.float32)
+            ids.append(uid)
+    return dict(w=w, mu=mu, sig=sig, T=T, feats=feats, ids=ids)
+
+
+def bench_config1(pkg):
+    """Config 1 end to end through the public API (train_extractor: 5 EM iterations with min-div and
+    Sigma update, then extract_corpus), host features in (InMemoryFeatureStore: every H2D copy inside
+    the timing) and the trained model / i-vectors out, against the reference algorithm (oracle
+    restatement of pipeline.train_extractor) on the host cores on the same corpus, with a parity check."""
+    import warnings
+    from types import SimpleNamespace
+    from oracle import tvkit_oracle as orc
+    from paper_1906_08556_b200 import pipeline as P
+    cor = config1_corpus()
+    genm = pkg.TvModel("augmented", cor["T"], cor["sig"], cor["w"], cor["mu"], None, P_OFF)
+    full, diag = genm.alignment_ubm_full(), genm.alignment_ubm_diag()
+    cfg = P.TrainConfig(formulation="augmented", latent_dim=C1["R"], iterations=C1["iters"], min_div=True,
+                        sigma_update=True, update_mean=False, realign_interval=0, top_k=K_TOP, prune=PRUNE,
+                        seeds=(0,), batch_size_utts=8, workers=1)
+    store = P.InMemoryFeatureStore(cor["feats"])
+
+    def run():
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            model, metrics = P.train_extractor(cfg, store, diag, full, seed=0)
+            _, emb = P.extract_corpus(model, store, top_k=K_TOP, prune=PRUNE)
+        return model, metrics, emb
+
+    run()  # warm-up (tables, allocator)
+    t0 = time.perf_counter()
+    model, metrics, emb = run()
+    ours = time.perf_counter() - t0
+    ns = SimpleNamespace(formulation="augmented", latent_dim=C1["R"], iterations=C1["iters"], min_div=True,
+                         sigma_update=True, update_mean=False, realign_interval=0, top_k=K_TOP, prune=PRUNE,
+                         prior_offset=P_OFF, batch_size_utts=8)
+    t0 = time.perf_counter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref, ref_aux = orc.train(ns, cor["feats"], cor["ids"], (diag.weights, diag.means, diag.variances),
+                                 (full.weights, full.means, full.covariances), seed=0)
+    cpu = time.perf_counter() - t0
+    rel = lambda a, b: float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))  # noqa: E731
+    aux = np.array([r.aux for r in metrics.records])
+    return {"value": ours, "unit": "s/run", "higher_is_better": False, "iterations": C1["iters"],
+            "s_per_iter": ours / C1["iters"], "utts": len(cor["ids"]), "frames_per_utt": C1["frames"],
+            "config": "config 1: augmented TVM, C=64, F=20, R=100, 200 utts x 300 frames, 5 EM iterations "
+                      "(min-div + Sigma update) + extract_corpus",
+            "path": "pipeline.train_extractor + extract_corpus (public API, host features, models/i-vectors to host)",
+            "cpu_baseline": {"value": cpu, "unit": "s/run (training only)", "cores": len(os.sched_getaffinity(0)),
+                             "kind": "port", "sample": "the whole config-1 training run, oracle restatement of "
+                                                       "tvkit.pipeline.train_extractor (numpy/OpenBLAS, all host cores)"},
+            "vs_cpu": cpu / ours,
+            "parity_vs_reference_algorithm": {"T_rel": rel(model.T, ref.T), "Sigma_rel": rel(model.Sigma, ref.Sigma),
+                                              "aux_rel": float(np.max(np.abs(aux - np.array(ref_aux))
+                                                                      / np.abs(np.array(ref_aux)))),
+                                              "tolerance": "T, Sigma 1e-4 relative; aux 1e-9",
+                                              "ivectors_finite": bool(np.all(np.isfinite(emb)))}}
+
+
 def em_cpu_baseline(n_utts=6, comp_sample=128):
     """The reference EM iteration on the host cores (oracle restatement of tvm.py/pipeline.py), timed on
     a bounded sample and extrapolated per BASELINE.md §4: sec/iter = workspace + 20k x (BW stats +
@@ -788,6 +884,8 @@ def main():
     ap.add_argument("--c5-utts", type=int, default=20000, help="config 5 training utterances (global)")
     ap.add_argument("--extract-utts", type=int, default=150000, help="config 5 extraction utterances (global)")
     ap.add_argument("--config4-utts", type=int, default=0, help="config 4 (opt-in): 1100000 utterances")
+    ap.add_argument("--no-config1", dest="config1", action="store_false",
+                    help="skip the config-1 end-to-end training leg (and its host reference run)")
     ap.add_argument("--exact-frames", type=int, default=2_000_000,
                     help="frames of the tcgen05-vs-FP64 preselection identity check")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (test: ranks may share a GPU)")
