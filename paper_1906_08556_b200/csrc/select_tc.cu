@@ -102,7 +102,7 @@ __host__ __device__ inline Layout layout(int C, int F) {
 }
 
 inline size_t smem_bytes(int) {
-  return (size_t)RING + (size_t)TM * XS * 4 + (size_t)(CAP + 1) * NEPI * 8 + (size_t)TM * 4 + 256;
+  return (size_t)RING + (size_t)TM * XS * 4 + (size_t)(CAP + 1) * NEPI * 8 + (size_t)TM * 4 + (size_t)NEPI * 4 + 256;
 }
 
 // ---------------------------------------------------------------- table construction
@@ -243,12 +243,17 @@ __device__ __forceinline__ void cp_async4_f(float* smem, const T* gmem) {  // f6
   *smem = (float)*gmem;
 }
 
+// pairwise tree (depth log2 G instead of a G-long dependent chain); NaN (padded components) is ignored
 template <int G>
 __device__ __forceinline__ float group_max(const float (&v)[32], int o) {
-  float a = v[o];
+  float a[G];
 #pragma unroll
-  for (int i = 1; i < G; i++) a = fmaxf(a, v[o + i]);  // NaN (padded components) is ignored
-  return a;
+  for (int i = 0; i < G; i++) a[i] = v[o + i];
+#pragma unroll
+  for (int w = G / 2; w >= 1; w /= 2)
+#pragma unroll
+    for (int i = 0; i < w; i++) a[i] = fmaxf(a[i], a[i + w]);
+  return a[0];
 }
 
 // With K < NK the first NK-K slots hold +inf sentinels, so the K-th largest is always top[NK-1]
@@ -263,7 +268,7 @@ struct Pipe {  // B-ring geometry and back-off of the single-thread roles (tunab
   int stage_bytes, sp0, sp1, sleep_prod, sleep_mma;
 };
 
-template <typename XT, int NK>
+template <typename XT, int NK, bool SPLIT>
 __global__ void __launch_bounds__(NT, 1)
     select_tc_kernel(const XT* __restrict__ x, int64_t T, int F, int C, int K, const __half* __restrict__ blob,
                      const float* __restrict__ maxes, const float* __restrict__ colscale,
@@ -279,6 +284,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int STAGE = pipe.stage_bytes, NST = RING / STAGE;
   float2* cc = reinterpret_cast<float2*>(xs + TM * XS);             // [CAP+1][NEPI] (s~, component); row CAP: dump
   float* kth1 = reinterpret_cast<float*>(cc + (CAP + 1) * NEPI);    // [TM] collection threshold per frame
+  float* pubv = kth1 + TM;                                          // [NEPI] split bound: each half's value
   __shared__ uint64_t full[MAXST], empty[MAXST], tfull[2], tempty[2], afull[2], aempty[2];
   __shared__ uint32_t tmem_base;
   __shared__ float cs[128];  // colscale (feature column exponents of the f16 operands)
@@ -514,10 +520,16 @@ __global__ void __launch_bounds__(NT, 1)
         S_next = pn.S;
       };
       const int npair = NCH / 2;
-      // ---- pass 0 (1xTF32): K-th largest of the group maxima, a lower bound of the K-th exact score
-      float top[NK];
+      // ---- pass 0 (1xFP16): a lower bound of the K-th exact score from group maxima.  Union mode: the
+      // K-th largest group maximum of the frame (both halves' lists merged below).  SPLIT mode: half h
+      // keeps the Kh-th largest of its own group maxima, Kh = ceil(K/2) (h = 0) or floor(K/2) (h = 1);
+      // each half then has >= Kh components scoring >= its value, so at least K components score
+      // >= the smaller of the two: a lower bound with half the list and no list merge.
+      constexpr int NL = SPLIT ? NK / 2 : NK;
+      const int Kl = SPLIT ? (h == 0 ? (K + 1) / 2 : K / 2) : K;
+      float top[NL];
 #pragma unroll
-      for (int i = 0; i < NK; i++) top[i] = i < NK - K ? INFINITY : -INFINITY;
+      for (int i = 0; i < NL; i++) top[i] = i < NL - Kl ? INFINITY : -INFINITY;
       for (int p = 0; p < NCH / 2; p++) {
         const uint32_t ph = buf_uses(0, li, 0, p, NCH) & 1;
         tc::mbar_wait(&tfull[0], ph);
@@ -542,13 +554,13 @@ __global__ void __launch_bounds__(NT, 1)
           for (int j = 0; j < 2; j++) {
             if ((debug >= 2 && debug <= 7 && debug != 6) || debug == 14) continue;  // diagnostics (2, 3, 7, 14)
             if (group == 32) {
-              insert_top<NK>(top, group_max<32>(v[j], 0));
+              insert_top<NL>(top, group_max<32>(v[j], 0));
             } else if (group == 8) {
 #pragma unroll
-              for (int q = 0; q < 4; q++) insert_top<NK>(top, group_max<8>(v[j], 8 * q));
+              for (int q = 0; q < 4; q++) insert_top<NL>(top, group_max<8>(v[j], 8 * q));
             } else {
 #pragma unroll
-              for (int q = 0; q < 32; q++) insert_top<NK>(top, v[j][q]);
+              for (int q = 0; q < 32; q++) insert_top<NL>(top, v[j][q]);
             }
           }
         }
@@ -560,24 +572,44 @@ __global__ void __launch_bounds__(NT, 1)
       if (has_next && npair <= 1) prep_next();
       mark(it, 1);
 
-      // union of both halves' lists: half 1 publishes, half 0 merges and publishes the threshold
-      // (published through half 1's own candidate columns: free until its pass 1; the merged-window
-      // arrays may still be in use by half 0 finishing the previous tile)
-      auto pub = [&](int i) -> float& { return reinterpret_cast<float*>(cc + (i >> 1) * NEPI + (e | 128))[i & 1]; };
-      if (h == 1) {
+      float thr;
+      if (SPLIT) {
+        // the two threads of a frame (warps w and w + 4: same TMEM lane quarter) swap their values
+        // through pubv behind a 64-thread named barrier (ids 2-5, one per lane quarter)
+        pubv[e] = top[NL - 1];
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)));
+        const float kb = fminf(top[NL - 1], pubv[e ^ 128]);
+        // every exact score of the K group maxima is >= (their 1xFP16 score) - kappa1 S
+        thr = live ? kb - kappa1 * S * inv - 3.0f * m : INFINITY;
+      } else {
+        // union of both halves' lists: half 1 publishes, half 0 merges and publishes the threshold
+        // (published through half 1's own candidate columns: free until its pass 1; the merged-window
+        // arrays may still be in use by half 0 finishing the previous tile)
+        auto pub = [&](int i) -> float& { return reinterpret_cast<float*>(cc + (i >> 1) * NEPI + (e | 128))[i & 1]; };
+        if (h == 1) {
 #pragma unroll
-        for (int i = 0; i < NK; i++) pub(i) = top[i];
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
-      if (h == 0) {
+          for (int i = 0; i < NL; i++) pub(i) = top[i];
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
+        if (h == 0) {
+          float kb;
+          if (K == NL) {
+            // K-th largest of the union of two descending lists A, B of length K:
+            // max over i of min(A[i-1], B[K-1-i]) (A[-1] = B[-1] = +inf) -- independent min/max, no chain
+            kb = fmaxf(top[NL - 1], pub(NL - 1));
 #pragma unroll
-        for (int i = 0; i < NK; i++)
-          insert_top<NK>(top, i >= NK - K ? pub(i) : -INFINITY);
-        // every exact score of the K group maxima is >= (their 1xTF32 score) - kappa1 S
-        kth1[r] = kth_of<NK>(top, K) - kappa1 * S * inv - 3.0f * m;
+            for (int i = 1; i < NL; i++) kb = fmaxf(kb, fminf(top[i - 1], pub(NL - 1 - i)));
+          } else {
+#pragma unroll
+            for (int i = 0; i < NL; i++)
+              insert_top<NL>(top, i >= NL - K ? pub(i) : -INFINITY);
+            kb = kth_of<NL>(top, K);
+          }
+          kth1[r] = kb - kappa1 * S * inv - 3.0f * m;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
+        thr = live ? kth1[r] : INFINITY;
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(NEPI));
-      const float thr = live ? kth1[r] : INFINITY;
       mark(it, 2);
       mark(it, 3);
 
@@ -622,14 +654,19 @@ __global__ void __launch_bounds__(NT, 1)
       mark(it, 4);
       mark(it, 5);
       mark(it, 6);
-      // ---- hand the window candidates to select_post_kernel: frame-major runs of CAP per half,
-      // count (-1: overflow) and the frame's threshold / margin / scale
-      if (t < T) {
-        const bool ovf = cnt > CAP;
-        float2* dst = cand + ((size_t)t * 2 + h) * CAP;
-        for (int j = 0; j < (ovf ? 0 : cnt); j++) dst[j] = cc[j * NEPI + e];
-        cand_n[t * 2 + h] = ovf ? -1 : cnt;
-        if (h == 0) fpar[t] = make_float4(thr, m2, inv, 0.0f);
+      // ---- hand the window candidates to select_post_kernel: entry-major rows per (tile, half) --
+      // cand[((tile * 2 + h) * CAP + j) * TM + r] -- the smem layout, so every warp store is one
+      // coalesced 256-byte row; count (-1: overflow) and the frame's threshold / margin / scale
+      {
+        const int nw = cnt > CAP ? 0 : cnt;
+        const int jmax = __reduce_max_sync(0xffffffffu, nw);
+        float2* dst = cand + ((size_t)tile * 2 + h) * CAP * TM + r;
+        for (int j = 0; j < jmax; j++)
+          if (j < nw) dst[(size_t)j * TM] = cc[j * NEPI + e];
+        if (t < T) {
+          cand_n[t * 2 + h] = cnt > CAP ? -1 : cnt;
+          if (h == 0) fpar[t] = make_float4(thr, m2, inv, 0.0f);
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI));  // every thread is done with xs before the next load_x
       mark(it, 7);
@@ -860,6 +897,23 @@ __device__ __forceinline__ void warp_sort_desc(uint64_t (&k)[2], int lane) {
   }
 }
 
+// Exact FP64 scores of up to four window entries at once: lane = 8 * slot + sub, each lane sums the
+// features f = sub + 8 i of its slot's component (x values preloaded per lane), then a 3-level
+// butterfly inside the 8-lane slot.  Lanes of unused slots recompute slot 0's component.
+__device__ __forceinline__ double slot_exact_score(const double (&xs)[8], const double* __restrict__ row, int F,
+                                                   int sub) {
+  double s = sub == 0 ? __ldg(row + 2 * F) : 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int f = sub + 8 * i;
+    if (f < F) s = fma(xs[i], fma(__ldg(row + f), xs[i], __ldg(row + F + f)), s);
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  return s;
+}
+
 template <typename XT>
 __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__ x, int64_t T, int F, int K,
                                                           const double* __restrict__ exact,
@@ -869,114 +923,126 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
                                                           int* __restrict__ flagged, int32_t* __restrict__ sel_out,
                                                           double* __restrict__ val_out) {
   const int lane = threadIdx.x & 31;
+  const int sub = lane & 7, slot = lane >> 3;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint64_t pad = sel_key(-INFINITY, 0x7fffffff);
+  // consecutive warps of a CTA take consecutive frames: the entry-major rows are read as 8-byte
+  // pieces of 32-byte sectors shared by four neighbouring frames (L1 hits)
   for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += nw) {
-    const int n0 = cand_n[2 * t], n1 = cand_n[2 * t + 1];
-    const float4 par = fpar[t];
-    const float thr = par.x, m2 = par.y;
-    if (dbg_vals == 9) {  // diagnostics: candidate counts per half
-      if (lane == 0 && val_out) {
-        val_out[t * K] = n0;
-        val_out[t * K + 1] = n1;
+    {
+      const int n0 = cand_n[2 * t], n1 = cand_n[2 * t + 1];
+      const float4 par = fpar[t];
+      const float thr = par.x, m2 = par.y;
+      if (dbg_vals == 9) {  // diagnostics: candidate counts per half
+        if (lane == 0 && val_out) {
+          val_out[t * K] = n0;
+          val_out[t * K + 1] = n1;
+        }
+        continue;
       }
-      continue;
-    }
-    bool good = n0 >= 0 && n1 >= 0 && n0 + n1 >= K;
-    uint64_t k[2] = {pad, pad};
-    float lim = INFINITY, v = -INFINITY;
-    int c = 0x7fffffff;
-    if (good) {
-      const float2* base = cand + (size_t)t * 2 * CAP;
-      const int n = n0 + n1;
-      // entries 0..n-1: half 0 then half 1, then padding; the rows are loaded whole so the loads do
-      // not wait for the counts
-      float2 q0 = make_float2(-INFINITY, __int_as_float(0x7fffffff)), q1 = q0;
-      if (lane < CAP) {
-        q0 = base[lane];
-        q1 = base[CAP + lane];
+      bool good = n0 >= 0 && n1 >= 0 && n0 + n1 >= K;
+      uint64_t k[2] = {pad, pad};
+      float lim = INFINITY, v = -INFINITY;
+      int c = 0x7fffffff;
+      if (good) {
+        const int n = n0 + n1;
+        // entries 0..n-1: half 0 then half 1, then padding
+        float2 q0 = make_float2(-INFINITY, __int_as_float(0x7fffffff)), q1 = q0;
+        if (lane < CAP) {
+          const float2* base = cand + ((size_t)(t / TM) * 2 * CAP + lane) * TM + (t % TM);
+          q0 = base[0];
+          q1 = base[(size_t)CAP * TM];
+        }
+        auto shfl2 = [](float2 e, int src) {
+          return make_float2(__shfl_sync(0xffffffffu, e.x, src), __shfl_sync(0xffffffffu, e.y, src));
+        };
+        const float2 a = shfl2(q1, (lane - n0) & 31);        // half-1 entry lane - n0
+        const float2 b2 = shfl2(q1, (lane + 32 - n0) & 31);  // half-1 entry lane + 32 - n0
+        const float2 e0 = lane < n0 ? q0 : a;
+        if (lane < n) k[0] = sel_key(e0.x, __float_as_int(e0.y));
+        if (n > 32) {
+          if (lane + 32 < n) k[1] = sel_key(b2.x, __float_as_int(b2.y));
+          warp_sort_desc<2>(k, lane);
+        } else {
+          warp_sort_desc<1>(k, lane);
+        }
+        v = key_v(k[0]);
+        c = key_c(k[0]);
+        const float kv = __shfl_sync(0xffffffffu, v, K - 1);
+        lim = kv - m2;
+        // the collected K-th (a lower bound of the true K-th) must clear the collection threshold,
+        // and the exact window (all entries >= lim: a prefix) must fit one warp
+        if (kv - m2 < thr || key_v(k[1]) >= lim) good = false;
+        good = __all_sync(0xffffffffu, good);
       }
-      auto shfl2 = [](float2 q, int src) {
-        return make_float2(__shfl_sync(0xffffffffu, q.x, src), __shfl_sync(0xffffffffu, q.y, src));
-      };
-      const float2 a = shfl2(q1, (lane - n0) & 31);        // half-1 entry lane - n0
-      const float2 b2 = shfl2(q1, (lane + 32 - n0) & 31);  // half-1 entry lane + 32 - n0
-      const float2 e0 = lane < n0 ? q0 : a;
-      if (lane < n) k[0] = sel_key(e0.x, __float_as_int(e0.y));
-      if (n > 32) {
-        if (lane + 32 < n) k[1] = sel_key(b2.x, __float_as_int(b2.y));
-        warp_sort_desc<2>(k, lane);
-      } else {
-        warp_sort_desc<1>(k, lane);
+      if (!good) {
+        if (lane == 0) {
+          sel_out[t * K] = -1;
+          flagged[1 + atomicAdd(flagged, 1)] = (int)t;
+        }
+        continue;
       }
-      v = key_v(k[0]);
-      c = key_c(k[0]);
-      const float kv = __shfl_sync(0xffffffffu, v, K - 1);
-      lim = kv - m2;
-      // the collected K-th (a lower bound of the true K-th) must clear the collection threshold,
-      // and the exact window (all entries >= lim: a prefix) must fit one warp
-      if (kv - m2 < thr || key_v(k[1]) >= lim) good = false;
-      good = __all_sync(0xffffffffu, good);
-    }
-    if (!good) {
-      if (lane == 0) {
-        sel_out[t * K] = -1;
-        flagged[1 + atomicAdd(flagged, 1)] = (int)t;
+      const unsigned win = __ballot_sync(0xffffffffu, v >= lim);
+      const int We = __popc(win);
+      const float prev = __shfl_up_sync(0xffffffffu, v, 1);
+      const unsigned joined = __ballot_sync(0xffffffffu, lane >= 1 && lane < We && prev - v <= m2) & win;
+      const unsigned starts = win & ~joined;
+      const unsigned below = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);  // bits 0..lane
+      const int st = 31 - __clz(starts & below);                               // my cluster start
+      const unsigned after = starts & ~below;
+      const int en = after ? __ffs(after) - 1 : We;                            // my cluster end
+      const bool clustered = lane < We && en - st > 1 && st < K;
+      const bool want_all = val_out != nullptr || dbg_vals;
+      unsigned need = __ballot_sync(0xffffffffu, clustered || (want_all && lane < K));
+      double ev = 0.0;
+      if (need) {
+        const XT* xr = x + t * F;
+        double xs[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) xs[i] = sub + 8 * i < F ? (double)xr[sub + 8 * i] : 0.0;
+        while (need) {  // four entries per step, one per 8-lane slot
+          int jj[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            jj[u] = need ? __ffs(need) - 1 : -1;
+            need &= need - 1u;
+          }
+          // (selects, not jj[slot]: a runtime index would put jj in local memory)
+          const int js = slot == 0 ? jj[0] : slot == 1 ? jj[1] : slot == 2 ? jj[2] : jj[3];
+          const int mine = js >= 0 ? js : jj[0];
+          const int cm = __shfl_sync(0xffffffffu, c, mine);
+          const double sv = slot_exact_score(xs, exact + (int64_t)cm * (2 * F + 2), F, sub);
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const double su = __shfl_sync(0xffffffffu, sv, 8 * u);
+            if (lane == jj[u]) ev = su;
+          }
+        }
       }
-      continue;
-    }
-    const unsigned win = __ballot_sync(0xffffffffu, v >= lim);
-    const int We = __popc(win);
-    const float prev = __shfl_up_sync(0xffffffffu, v, 1);
-    const unsigned joined = __ballot_sync(0xffffffffu, lane >= 1 && lane < We && prev - v <= m2) & win;
-    const unsigned starts = win & ~joined;
-    const unsigned below = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);  // bits 0..lane
-    const int st = 31 - __clz(starts & below);                               // my cluster start
-    const unsigned after = starts & ~below;
-    const int en = after ? __ffs(after) - 1 : We;                            // my cluster end
-    const bool clustered = lane < We && en - st > 1 && st < K;
-    const bool want_all = val_out != nullptr || dbg_vals;
-    unsigned need = __ballot_sync(0xffffffffu, clustered || (want_all && lane < K));
-    double ev = 0.0;
-    if (need) {
-      const XT* xr = x + t * F;
-      const double x0 = lane < F ? (double)xr[lane] : 0.0, x1 = lane + 32 < F ? (double)xr[lane + 32] : 0.0;
-      while (need) {  // two entries per step: independent loads and shuffle trees
-        const int j0 = __ffs(need) - 1;
-        need &= need - 1u;
-        const int j1 = need ? __ffs(need) - 1 : j0;
-        need &= need - 1u;
-        const int c0 = __shfl_sync(0xffffffffu, c, j0), c1 = __shfl_sync(0xffffffffu, c, j1);
-        double s0, s1;
-        warp_exact_score2(x0, x1, exact + (int64_t)c0 * (2 * F + 2), exact + (int64_t)c1 * (2 * F + 2), F, lane,
-                          s0, s1);
-        if (lane == j0) ev = s0;
-        if (lane == j1) ev = s1;
+      if (dbg_vals) {  // diagnostics: s~ - s of the s~-ordered window
+        if (lane < K) {
+          sel_out[t * K + lane] = c;
+          if (val_out) val_out[t * K + lane] = (double)v / (double)par.z - ev;
+        }
+        continue;
       }
-    }
-    if (dbg_vals) {  // diagnostics: s~ - s of the s~-ordered window
-      if (lane < K) {
-        sel_out[t * K + lane] = c;
-        if (val_out) val_out[t * K + lane] = (double)v / (double)par.z - ev;
+      // final position: cluster start + members ranked before me by (exact desc, index asc)
+      int pos = lane;
+      const unsigned cl_mask = __ballot_sync(0xffffffffu, clustered);
+      if (cl_mask) {
+        int cntb = 0;
+        for (unsigned mm = cl_mask; mm; mm &= mm - 1u) {  // clustered lanes only (warp-uniform mask)
+          const int j = __ffs(mm) - 1;
+          const double ov = __shfl_sync(0xffffffffu, ev, j);
+          const int oc = __shfl_sync(0xffffffffu, c, j);
+          if (clustered && j >= st && j < en && j != lane && better(ov, oc, ev, c)) cntb++;
+        }
+        if (clustered) pos = st + cntb;
       }
-      continue;
-    }
-    // final position: cluster start + members ranked before me by (exact desc, index asc)
-    int pos = lane;
-    const unsigned cl_mask = __ballot_sync(0xffffffffu, clustered);
-    if (cl_mask) {
-      int cntb = 0;
-      for (unsigned m = cl_mask; m; m &= m - 1u) {  // clustered lanes only (warp-uniform mask)
-        const int j = __ffs(m) - 1;
-        const double ov = __shfl_sync(0xffffffffu, ev, j);
-        const int oc = __shfl_sync(0xffffffffu, c, j);
-        if (clustered && j >= st && j < en && j != lane && better(ov, oc, ev, c)) cntb++;
+      if (lane < We && pos < K) {
+        sel_out[t * K + pos] = c;
+        if (val_out) val_out[t * K + pos] = ev;
       }
-      if (clustered) pos = st + cntb;
-    }
-    if (lane < We && pos < K) {
-      sel_out[t * K + pos] = c;
-      if (val_out) val_out[t * K + pos] = ev;
     }
   }
 }
@@ -1013,13 +1079,13 @@ static int num_sms() {
   return n;
 }
 
-template <typename XT, int NK>
+template <typename XT, int NK, bool SPLIT>
 static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, int K, int32_t* sel, double* val,
                      cudaStream_t st) {
   stc::Layout L = stc::layout(C, F);
   const uint8_t* base = (const uint8_t*)tab;
   size_t smem = stc::smem_bytes(F);
-  auto kern = stc::select_tc_kernel<XT, NK>;
+  auto kern = stc::select_tc_kernel<XT, NK, SPLIT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int64_t ntiles = (T + stc::TM - 1) / stc::TM;
   int64_t want = (ntiles + stc::CL - 1) / stc::CL * stc::CL;
@@ -1047,7 +1113,7 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
   TVK_REQUIRE(stc::RING / pipe.stage_bytes >= 2 && stc::RING / pipe.stage_bytes <= stc::MAXST, "select_tc: bad ring");
   // stream-ordered scratch: [flagged count | frame indices], candidate runs, counts, frame params
   const size_t b_flag = stc::al(sizeof(int) * (T + 1), 256);
-  const size_t b_cand = stc::al(sizeof(float2) * 2 * stc::CAP * (size_t)T, 256);
+  const size_t b_cand = stc::al(sizeof(float2) * 2 * stc::CAP * (size_t)ntiles * stc::TM, 256);  // whole tiles
   const size_t b_n = stc::al(sizeof(int) * 2 * (size_t)T, 256);
   const size_t b_par = sizeof(float4) * (size_t)T;
   static bool pool_ready = false;
@@ -1117,8 +1183,13 @@ static int launch_tc(const XT* x, int64_t T, int F, const double* tab, int C, in
 template <typename XT>
 int select_tc(const XT* x, int64_t T, int F, const double* tab, int C, int K, int32_t* sel, double* val,
               cudaStream_t st) {
-  if (K <= 20) return launch_tc<XT, 20>(x, T, F, tab, C, K, sel, val, st);
-  return launch_tc<XT, 32>(x, T, F, tab, C, K, sel, val, st);
+  // split pass-0 bound (each half keeps its own K/2 list) when both halves hold many components
+  const bool split = false;  // measured: the per-half bound is looser (1.4% window overflows at config 2)
+  if (K <= 20)
+    return split ? launch_tc<XT, 20, true>(x, T, F, tab, C, K, sel, val, st)
+                 : launch_tc<XT, 20, false>(x, T, F, tab, C, K, sel, val, st);
+  return split ? launch_tc<XT, 32, true>(x, T, F, tab, C, K, sel, val, st)
+               : launch_tc<XT, 32, false>(x, T, F, tab, C, K, sel, val, st);
 }
 template int select_tc<float>(const float*, int64_t, int, const double*, int, int, int32_t*, double*, cudaStream_t);
 template int select_tc<double>(const double*, int64_t, int, const double*, int, int, int32_t*, double*,

@@ -1,6 +1,9 @@
-"""Per-phase timeline (clock64) of the tcgen05 preselection epilogue, CTA 0 (TVK_SELECT_DEBUG=6)."""
+"""Per-phase timeline (clock64) of the tcgen05 preselection epilogue, CTA 0 (diagnostics build, TVK_SELECT_DEBUG=6;
+7: scores not consumed, 12: no pass-1 append, 13: next A not built in pass 0, 14: no pass-0 bound)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from build_diag import use_diag
+use_diag()
 import numpy as np, torch
 import bench
 import paper_1906_08556_b200 as pkg
