@@ -18,6 +18,7 @@
  *   tvk_bw_stats            accumulate_bw_stats                gmm.py:442-492
  *   tvk_spd_small           PosteriorWorkspace per-component   tvm.py:163-171 (chol, inverse, logdet)
  *   tvk_dgemm               every dense contraction            tvm.py:169,190-193,298-302,347,436-444
+ *   tvk_dgemm_i8            E-step contractions (FP64 on int8) tvm.py:183-200, 283-302
  *   tvk_posterior           _posterior_terms                   tvm.py:183-215 (chol, Phi, phi, logdet)
  *   tvk_spd_solve_rows      update_T                           tvm.py:317-334
  *   tvk_sigma_floor         update_sigma + floor_eigenvalues   tvm.py:337-358, _linalg.py:15-24
@@ -70,6 +71,15 @@ int tvk_aln1_scan(const uint32_t* words, int64_t n_words, int64_t n_frames, int6
 int tvk_dgemm(int trans_a, int trans_b, int m, int n, int k, double alpha, const double* a, int64_t lda,
               int64_t stride_a, const double* b, int64_t ldb, int64_t stride_b, double beta, double* c,
               int64_t ldc, int64_t stride_c, int batch, int out_mode, int splits, double* work, void* stream);
+
+/* C = alpha op(A) op(B) + beta C (row-major, dense, unbatched) in FP64 emulated on the int8 tensor cores
+ * (tcgen05 kind::i8): every row of op(A) and column of op(B) is scaled by a power of two and cut into
+ * `digits` (6..8) signed 7-bit digits, the digit products are summed exactly in int32 and combined in
+ * FP64; |error| <= (2 + digits) 2^(-7 digits) K max_k|op(A)_mk| max_k|op(B)_kn| (digits = 7: 2^-45.8 K
+ * max max).  The E-step contractions L = N U, A += N'M, b = F W, B += F' phi (tvm.py:183-200, 283-302)
+ * run here; non-finite inputs give NaN rows / columns.  Bit-reproducible. */
+int tvk_dgemm_i8(int trans_a, int trans_b, int m, int n, int k, double alpha, const double* a, int64_t lda,
+                 const double* b, int64_t ldb, double beta, double* c, int64_t ldc, int digits, void* stream);
 
 /* Fixed-order reductions (bit-reproducible, no atomics):
  *   tvk_colsum: out[j] = beta*out[j] + alpha * sum_r a[r*lda + j]   (rows x cols)

@@ -7,8 +7,10 @@ Data layout in HBM (FP64 throughout, C components, F dims, D latent dims, P = D(
   batch      N (Ub, C), Fm (Ub, C*F)  -> Lpk = N Upk (Ub, P),  b = Fm W + p e1 (Ub, D)
              posterior kernel -> phi (Ub, D), Mpk = packed(Phi + phi phi') (Ub, P)
   acc        Apk (C, P) += N' Mpk;  B (C*F, D) += Fm' phi;  Nsum, phi_sum, moment (P), Ssum
-All contractions are tvk_dgemm calls (DMMA tensor pipe); vector sums are GEMMs against a
-ones vector so every reduction has a fixed order (bit-reproducible, no atomics).
+The four large E-step contractions (L = N U, b = F W, A += N'M, B += F' phi) run as FP64 emulated on
+the int8 tensor cores (tvk_dgemm_i8: 7 Ozaki digits, exact int32 products, error <= 2^-45.8 K
+max|row| max|col|); every other contraction is a tvk_dgemm call (FP64 DMMA tensor pipe).  Vector
+sums are fixed-order reductions (bit-reproducible, no atomics).
 """
 
 from __future__ import annotations
@@ -17,10 +19,25 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import call, dgemm, ptr, stream
+from ._lib import call, dgemm, dgemm_i8, ptr, stream
 
 LOG_2PI = float(np.log(2.0 * np.pi))
 E_STEP_BATCH = 1024  # utterances per device E-step batch
+# engine of the large E-step contractions: "int8" (tvk_dgemm_i8, FP64 emulated on the int8 tensor
+# cores) or "dmma" (tvk_dgemm); products below I8_MIN_WORK multiply-adds stay on DMMA (the digit
+# split is O((M + N) K) and not worth it for small shapes)
+GEMM_ENGINE = "int8"
+I8_DIGITS = 7     # contractions over the occupancies N (L = N U, A += N'M)
+I8_DIGITS_F = 8   # contractions over the first-order statistics (b = F W, B += F' phi): a row of F spans
+                  # components of very different occupancy, so it carries one more digit
+I8_MIN_WORK = 1 << 30
+
+
+def egemm(a, b, c, m, n, k, *, trans_a=False, beta=0.0, splits=1, work=None, digits=None):
+    """One of the E-step contractions C = op(A) B + beta C on the configured engine."""
+    if GEMM_ENGINE == "int8" and m * n * k >= I8_MIN_WORK:
+        return dgemm_i8(a, b, c, m, n, k, trans_a=trans_a, beta=beta, digits=digits or I8_DIGITS)
+    return dgemm(a, b, c, m, n, k, trans_a=trans_a, beta=beta, splits=splits, work=work)
 
 
 def packed_size(d):
@@ -157,13 +174,13 @@ def posterior_batch(dm: DeviceModel, ws: Workspace, n, fm, want_moment=True, sta
     C, F, D = dm.C, dm.F, dm.D
     P = packed_size(D)
     Lpk = _lib.empty((Ub, P))
-    dgemm(n, ws.Upk, Lpk, Ub, P, C)  # L - I = sum_c n_c U_c
+    egemm(n, ws.Upk, Lpk, Ub, P, C)  # L - I = sum_c n_c U_c
     b = _lib.empty((Ub, D))
     b.copy_(torch.from_numpy(dm.prior_mean).to(b.device).expand(Ub, D))
     K = C * F
     splits = max(1, min(16, K // 2048)) if Ub * D < 148 * 128 * 128 else 1
     work = _lib.empty((splits * Ub * D,)) if splits > 1 else None
-    dgemm(fm, ws.W, b, Ub, D, K, beta=1.0, splits=splits, work=work)  # b = p e1 + sum_c W_c' f_c
+    egemm(fm, ws.W, b, Ub, D, K, beta=1.0, splits=splits, work=work, digits=I8_DIGITS_F)  # b = p e1 + sum W_c' f_c
     phi = _lib.empty((Ub, D))
     Mpk = Lpk if want_moment else None  # factored in place: M overwrites L (L2-resident working set)
     logdet = _lib.empty((Ub,))
@@ -195,8 +212,8 @@ def accumulate_batch(dm: DeviceModel, ws: Workspace, acc: DeviceAcc, n, fm, S=No
     phi, Mpk, logdet, bphi, status, _ = posterior_batch(dm, ws, n, fm, want_moment=True)
     check_status(status)
     if acc.Apk is not None:
-        dgemm(n, Mpk, acc.Apk, C, P, Ub, trans_a=True, beta=1.0)  # A_c += sum_u n_uc M_u
-    dgemm(fm, phi, acc.B, C * F, D, Ub, trans_a=True, beta=1.0)  # B_c += sum_u f_uc phi_u'
+        egemm(n, Mpk, acc.Apk, C, P, Ub, trans_a=True, beta=1.0)  # A_c += sum_u n_uc M_u
+    egemm(fm, phi, acc.B, C * F, D, Ub, trans_a=True, beta=1.0, digits=I8_DIGITS_F)  # B_c += sum_u f_uc phi_u'
     col_sum_into(acc.N.view(1, C), n, Ub, C)
     col_sum_into(acc.phi_sum.view(1, D), phi, Ub, D)
     col_sum_into(acc.moment.view(1, P), Mpk, Ub, P)

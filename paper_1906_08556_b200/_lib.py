@@ -38,6 +38,7 @@ SIGNATURES = {
     "tvk_last_error": (_i, [ctypes.c_char_p, _i64]),
     "tvk_dgemm": (_i, [_i, _i, _i, _i, _i, _d, _p, _i64, _i64, _p, _i64, _i64, _d, _p, _i64, _i64, _i, _i, _i,
                        _p, _p]),
+    "tvk_dgemm_i8": (_i, [_i, _i, _i, _i, _i, _d, _p, _i64, _p, _i64, _d, _p, _i64, _i, _p]),
     "tvk_colsum": (_i, [_p, _i64, _i64, _i64, _d, _d, _p, _p]),
     "tvk_ddot_workspace_bytes": (_i64, []),
     "tvk_ddot": (_i, [_p, _p, _i64, _d, _d, _p, _p, _p]),
@@ -204,6 +205,21 @@ def dgemm(a, b, c, m, n, k, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0
         ldc = n
     call("tvk_dgemm", int(trans_a), int(trans_b), m, n, k, alpha, ptr(a), lda, stride_a, ptr(b), ldb, stride_b,
          beta, ptr(c), ldc, stride_c, batch, out_mode, splits, ptr(work), stream())
+    return c
+
+
+def dgemm_i8(a, b, c, m, n, k, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0, lda=None, ldb=None, ldc=None,
+             digits=7):
+    """C = alpha op(A) op(B) + beta C (row-major, FP64) emulated on the int8 tensor cores (Ozaki digits,
+    exact int32 products; include/tvk.h tvk_dgemm_i8)."""
+    if lda is None:
+        lda = m if trans_a else k
+    if ldb is None:
+        ldb = k if trans_b else n
+    if ldc is None:
+        ldc = n
+    call("tvk_dgemm_i8", int(trans_a), int(trans_b), m, n, k, alpha, ptr(a), lda, ptr(b), ldb, beta, ptr(c), ldc,
+         int(digits), stream())
     return c
 
 

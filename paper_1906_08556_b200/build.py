@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libtvk.so")
 SOURCES = ["capi.cu", "gemm_f64.cu", "spd_small.cu", "align.cu", "select_tc.cu", "align_grouped.cu", "align_wide.cu", "bw.cu", "posterior.cu",
-           "mstep.cu", "reduce.cu", "ubm.cu"]
+           "mstep.cu", "ozaki.cu", "reduce.cu", "ubm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]

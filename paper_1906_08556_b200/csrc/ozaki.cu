@@ -1,0 +1,472 @@
+// FP64 GEMM emulated on the int8 tensor cores (tcgen05.mma kind::i8), Ozaki scheme with exact
+// int32 accumulation -- the E-step contractions of the i-vector EM (tvm.py:183-200, 283-302:
+// L = N U, A += N' M, b = F W, B += F' phi).
+//
+// Splitting.  Every row r of the left operand (M x K) and every column n of the right operand
+// (K x N) is scaled by a power of two 2^e (e = max frexp exponent of the row / column, so the
+// scaled values lie in (-1, 1)) and cut into S signed 7-bit digits:
+//     x = 2^e * sum_{s=1..S} d_s 2^(-7 s) + rho,   d_s in [-127, 127] (int8),  |rho| < 2^(e - 7 S),
+// d_s = trunc(128 r_{s-1}), r_s = 128 r_{s-1} - d_s (each step exact in FP64).
+// Product.  C_mn = 2^(e_m + e_n) sum_{s + t <= S + 1} 2^(-7 (s + t)) sum_k a_{s,mk} b_{t,kn} + error;
+// every inner sum is an int8 x int8 product accumulated EXACTLY in int32 (|sum| <= S K 127^2 < 2^31
+// for K <= 18,900 per launch piece), so the only errors are the digit truncation rho and the
+// dropped products s + t > S + 1, each < 2^(-7 S) relative to |row max| * |column max| per term:
+//     |C~ - C| <= (2 + S) 2^(-7 S) K max_k|a_mk| max_k|b_kn|        (S = 7: 2^-45.8 K max|a| max|b|)
+// and the final FP64 combination of the S level sums rounds once per level (2^-53 relative).
+//
+// Level accumulators in TMEM.  Products with the same level L = s + t share one int32 accumulator
+// block of 64 columns (levels 2..S+1 -> S blocks, 64 S <= 512 TMEM columns).  The right operand's S
+// digit tiles are stored consecutively along N (rows 64 (t-1) .. 64 t - 1 of one K-major tile), so
+// ONE MMA of left digit s against right digits t = 1 .. S+1-s (N = 64 (S+1-s), split at 256) writes
+// every product of that digit straight into its level blocks: D column offset 64 (s-1).
+// Per 32-byte k-step: S MMAs of M = 128, N = 448 .. 64 (28 products at S = 7) -- 97% of the int8
+// issue rate at N >= 128 (tools/i8_probe.cu: 4.4 POPS at N = 128).
+//
+// Kernel roles (one CTA per SM, persistent over 128 x 64 output tiles, m fastest so concurrent CTAs
+// share the right operand's tiles in L2): warp 0 lane 0 streams the pre-tiled digit blobs with
+// bulk copies (one A and one B copy per k-step), warp 1 lane 0 issues the MMAs, warps 2-9 drain
+// the level accumulators (tcgen05.ld 32x32b.x8), combine them in FP64 and write C.
+//
+// Determinism: integer products are exact and the FP64 combination has a fixed order, so results
+// are bit-reproducible run to run.  Non-finite inputs make the affected rows / columns NaN.
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tc.cuh"
+
+namespace tvk {
+namespace oz {
+
+constexpr int BM = 128;   // left rows per tile (MMA M, TMEM lanes)
+constexpr int BN = 64;    // right rows (output columns) per tile and per level block
+constexpr int KB = 32;    // bytes (= int8 elements) of K per k-step (one MMA)
+constexpr int NST = 4;    // ring stages
+constexpr int NT = 320;   // producer, MMA, 8 epilogue warps
+constexpr int EXP_BAD = 1 << 20;  // row exponent of a row holding a non-finite value
+
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {  // D s32, A/B signed int8, both K-major
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
+// ---------------------------------------------------------------- operand splitting
+// Logical operand X (R rows x K) with element (r, k) at x[r * rs + k * ks]; digit blob layout
+// [row tile rb][k-step][digit s][RT rows x 32 bytes, K-major core matrices (8 rows x 16 bytes):
+// (rr / 8) * 256 + (k / 16) * 128 + (rr % 8) * 16 + k % 16].
+
+// e[r] = max_k frexp exponent of x_rk (|x_rk| < 2^e[r]), EXP_BAD if the row holds a non-finite value;
+// e starts at EXP_NONE (memset 0xC0) and an all-zero row keeps it.  Blocks take 32-row x K-chunk
+// tiles and fold them with atomicMax (the maximum does not depend on the order).
+constexpr int EXP_NONE = (int)0xC0C0C0C0;
+__global__ void row_exp_kernel(const double* __restrict__ x, int R, int K, int64_t rs, int64_t ks, int kchunk, int* e) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int r0 = blockIdx.x * 32;
+  const int kb = blockIdx.y * kchunk, ke = min(K, kb + kchunk);
+  if (rs == 1 || ks != 1) {  // lanes over rows (coalesced when rows are adjacent), warps over k
+    const int r = r0 + lane;
+    int mx = EXP_NONE;
+    if (r < R)
+      for (int k = kb + warp; k < ke; k += nwarp) {
+        const double v = x[(int64_t)r * rs + (int64_t)k * ks];
+        if (!isfinite(v)) mx = EXP_BAD;
+        else if (v != 0.0) mx = max(mx, ilogb(v) + 1);
+      }
+    if (r < R && mx != EXP_NONE) atomicMax(&e[r], mx);
+  } else {  // k contiguous: lanes over k, warps over the tile's rows
+    for (int i = warp; i < 32; i += nwarp) {
+      const int r = r0 + i;
+      if (r >= R) break;
+      int mx = EXP_NONE;
+      for (int k = kb + lane; k < ke; k += 32) {
+        const double v = x[(int64_t)r * rs + k];
+        if (!isfinite(v)) mx = EXP_BAD;
+        else if (v != 0.0) mx = max(mx, ilogb(v) + 1);
+      }
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if (lane == 0 && mx != EXP_NONE) atomicMax(&e[r], mx);
+    }
+  }
+}
+
+// one thread per (row, 16-element k chunk): S digit bytes x 16 -> S 16-byte stores
+template <int S>
+__global__ void split_kernel(const double* __restrict__ x, int R, int K, int64_t rs, int64_t ks, const int* __restrict__ e,
+                             int RT, int Rp, int KSTEPS, bool rows_fast, int8_t* __restrict__ blob) {
+  const int KC = KSTEPS * 2;
+  const int64_t total = (int64_t)Rp * KC;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rows_fast ? (int)(idx % Rp) : (int)(idx / KC);
+    const int kc = rows_fast ? (int)(idx / Rp) : (int)(idx % KC);
+    uint32_t w[S][4];
+#pragma unroll
+    for (int s = 0; s < S; s++) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0u;
+    if (r < R) {
+      const int er = e[r];
+      const double sc = (er == EXP_BAD || er == EXP_NONE) ? 0.0 : ldexp(1.0, -er);
+#pragma unroll
+      for (int i = 0; i < 16; i++) {
+        const int k = kc * 16 + i;
+        double v = k < K ? x[(int64_t)r * rs + (int64_t)k * ks] * sc : 0.0;  // exact power-of-two scaling
+#pragma unroll
+        for (int s = 0; s < S; s++) {
+          v *= 128.0;
+          const double d = trunc(v);
+          v -= d;
+          w[s][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)d) << (8 * (i & 3));
+        }
+      }
+    }
+    const int rb = r / RT, rr = r % RT, kst = kc >> 1;
+    int8_t* dst = blob + (((int64_t)rb * KSTEPS + kst) * S) * (RT * KB) + (rr >> 3) * 256 + (kc & 1) * 128 + (rr & 7) * 16;
+#pragma unroll
+    for (int s = 0; s < S; s++)
+      *reinterpret_cast<uint4*>(dst + (int64_t)s * RT * KB) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+  }
+}
+
+// ---------------------------------------------------------------- GEMM
+struct Args {
+  const int8_t* A;  // left digits, BM-row tiles
+  const int* ea;
+  const int8_t* B;  // right digits, BN-row tiles
+  const int* eb;
+  int M, N, KSTEPS, mt, nt, nsplit, per;
+  double alpha, beta;
+  double* C;
+  int64_t ldc;
+  double* work;  // nsplit > 1: partials [split][M][N]
+  int dbg;       // diagnostics build only: 1 = epilogue drains TMEM without arithmetic / stores
+};
+
+template <int S>
+__global__ void __launch_bounds__(NT, 1) gemm_i8_kernel(Args p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int ABYTES = S * BM * KB, BBYTES = S * BN * KB, STAGE = ABYTES + BBYTES;
+  __shared__ uint64_t full[NST], empty[NST], tfull, tempty;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int units = p.mt * p.nt * p.nsplit;
+  if (tid == 0) {
+    for (int i = 0; i < NST; i++) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(&tfull, 1);
+    tc::mbar_init(&tempty, 8);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  auto unit_of = [&](int u, int& mtile, int& ntile, int& k0, int& k1) {
+    mtile = u % p.mt;
+    ntile = (u / p.mt) % p.nt;
+    const int sp = u / (p.mt * p.nt);
+    k0 = sp * p.per;
+    k1 = min(p.KSTEPS, k0 + p.per);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------------------- producer
+      uint32_t q = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int mtile, ntile, k0, k1;
+        unit_of(u, mtile, ntile, k0, k1);
+        for (int ks = k0; ks < k1; ks++, q++) {
+          const int slot = q % NST;
+          tc::mbar_wait_backoff(&empty[slot], ((q / NST) & 1) ^ 1, 32);
+          tc::mbar_arrive_expect_tx(&full[slot], STAGE);
+          uint8_t* st = smem + slot * STAGE;
+          tc::bulk_g2s(st, p.A + ((int64_t)mtile * p.KSTEPS + ks) * ABYTES, ABYTES, &full[slot]);
+          tc::bulk_g2s(st + ABYTES, p.B + ((int64_t)ntile * p.KSTEPS + ks) * BBYTES, BBYTES, &full[slot]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------------------------- MMA issuer
+      uint32_t q = 0, li = 0;
+      const uint32_t sb = tc::smem_u32(smem);
+      for (int u = blockIdx.x; u < units; u += gridDim.x, li++) {
+        int mtile, ntile, k0, k1;
+        unit_of(u, mtile, ntile, k0, k1);
+        tc::mbar_wait_backoff(&tempty, (li & 1) ^ 1, 32);  // the epilogue drained the previous unit
+        tc::fence_after_sync();
+        for (int ks = k0; ks < k1; ks++, q++) {
+          const int slot = q % NST;
+          tc::mbar_wait_backoff(&full[slot], (q / NST) & 1, 0);
+          tc::fence_after_sync();
+          const uint32_t a0 = sb + slot * STAGE, b0 = a0 + ABYTES;
+#pragma unroll
+          for (int s = 0; s < S; s++) {  // left digit s + 1 against right digits 1 .. S - s
+            const int Ns = BN * (S - s);
+            const uint64_t ad = tc::smem_desc(a0 + s * BM * KB, 128, 256);
+#pragma unroll
+            for (int n0 = 0; n0 < Ns; n0 += 256) {
+              const int nn = Ns - n0 < 256 ? Ns - n0 : 256;
+              const uint64_t bd = tc::smem_desc(b0 + n0 * KB, 128, 256);
+              mma_i8_ss(tmem + BN * s + n0, ad, bd, idesc_i8(BM, nn), (ks > k0 || s > 0) ? 1u : 0u);
+            }
+          }
+          tc::mma_commit(&empty[slot]);
+        }
+        tc::mma_commit(&tfull);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2-9)
+    // two warps per TMEM lane quarter, each drains 32 of the tile's 64 columns in chunks of 8
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    constexpr int NH = S < 4 ? S : 4;  // levels folded into the high int64 word
+    uint32_t li = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, li++) {
+      int mtile, ntile, k0, k1;
+      unit_of(u, mtile, ntile, k0, k1);
+      const int sp = u / (p.mt * p.nt);
+      const int m = mtile * BM + row;
+      const bool mok = m < p.M;
+      const bool rmw = mok && p.nsplit == 1 && p.beta != 0.0;
+      double* crow = p.C + (int64_t)(mok ? m : 0) * p.ldc;
+      const int nb = ntile * BN + 32 * half;
+      // C values of the first chunk are fetched before the wait (read-modify-write latency off the path)
+      double cpre[8];
+      auto fetch = [&](int j0) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) cpre[j] = (rmw && nb + j0 + j < p.N) ? crow[nb + j0 + j] : 0.0;
+      };
+      fetch(0);
+      const int em = mok ? p.ea[m] : EXP_NONE;
+      tc::mbar_wait(&tfull, li & 1);
+      tc::fence_after_sync();
+#pragma unroll 1
+      for (int j0 = 0; j0 < 32; j0 += 8) {
+        uint32_t v[S][8];
+#pragma unroll
+        for (int L = 0; L < S; L++) tmem_ld8(lane_addr + BN * L + 32 * half + j0, v[L]);
+        double cur[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) cur[j] = cpre[j];
+        if (j0 + 8 < 32) fetch(j0 + 8);
+        tc::tmem_ld_wait();
+        if (!mok || p.dbg == 1) continue;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const int n = nb + j0 + j;
+          if (n >= p.N) break;
+          // level L (0-based) carries the products with s + t = L + 2, weight 2^(-7 (L + 2)); the levels
+          // are folded exactly into two int64 words (|level| < 2^31: hi < 2^53, lo < 2^52)
+          long long hi = 0, lo = 0;
+#pragma unroll
+          for (int L = 0; L < NH; L++) hi += (long long)(int)v[L][j] << (7 * (NH - 1 - L));
+#pragma unroll
+          for (int L = NH; L < S; L++) lo += (long long)(int)v[L][j] << (7 * (S - 1 - L));
+          double c = (double)hi * (1.0 / (double)(1ll << (7 * (NH + 1))));
+          if (S > NH) c = fma((double)lo, ldexp(1.0, -7 * (S + 1)), c);
+          const int en = p.eb[n];
+          double r;
+          if (em == EXP_BAD || en == EXP_BAD) {
+            r = __longlong_as_double(0x7ff8000000000000ll);
+          } else if (em == EXP_NONE || en == EXP_NONE) {
+            r = 0.0;  // an all-zero row or column: all-zero digits
+          } else {
+            const int e2 = em + en;
+            r = p.alpha * (e2 > -1000 && e2 < 1000 ? c * __longlong_as_double((long long)(e2 + 1023) << 52)
+                                                    : ldexp(c, e2));
+          }
+          if (p.nsplit > 1) {
+            p.work[((int64_t)sp * p.M + m) * p.N + n] = r;
+          } else {
+            if (rmw) r += p.beta * cur[j];
+            crow[n] = r;
+          }
+        }
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+__global__ void splitk_sum_kernel(const double* __restrict__ work, int nsplit, int M, int N, double beta, double* C,
+                                  int64_t ldc) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nsplit; k++) s += work[(int64_t)k * total + i];  // fixed order
+    const int64_t r = i / N, c = i % N;
+    double* cp = C + r * ldc + c;
+    *cp = s + (beta != 0.0 ? beta * *cp : 0.0);
+  }
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// digits of a logical R x K operand into blob (RT-row tiles), exponents into e
+template <int S>
+static void split_operand(const double* x, int R, int K, int64_t rs, int64_t ks, int RT, int Rp, int KSTEPS, int* e,
+                          int8_t* blob, cudaStream_t st) {
+  cudaMemsetAsync(e, 0xC0, sizeof(int) * R, st);
+  const int rb = (R + 31) / 32;
+  int kch = std::max(1, (int)std::min<int64_t>(K, (int64_t)K * rb / (num_sms() * 8) + 1));
+  kch = std::max(kch, 256);
+  row_exp_kernel<<<dim3(rb, (K + kch - 1) / kch), 256, 0, st>>>(x, R, K, rs, ks, kch, e);
+  const int64_t total = (int64_t)Rp * KSTEPS * 2;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+  split_kernel<S><<<blocks, 256, 0, st>>>(x, R, K, rs, ks, e, RT, Rp, KSTEPS, rs == 1, blob);
+}
+
+template <int S>
+static int run(const GemmArgs& g, cudaStream_t st) {
+  const int M = g.M, N = g.N, K = g.K;
+  const int mt = ceil_div(M, BM), nt = ceil_div(N, BN), KSTEPS = ceil_div(K, KB);
+  const int Mp = mt * BM, Np = nt * BN;
+  // split K when the tile grid leaves SMs idle (and to keep every int32 level sum below 2^31)
+  int nsplit = 1;
+  const int tiles = mt * nt;
+  while (nsplit < 32 && (int64_t)tiles * nsplit < 2 * num_sms() && KSTEPS / (nsplit * 2) >= 16) nsplit *= 2;
+  while ((int64_t)S * ceil_div(KSTEPS, nsplit) * KB * 127 * 127 >= (1ll << 31)) nsplit *= 2;
+  const int per = ceil_div(KSTEPS, nsplit);
+  nsplit = ceil_div(KSTEPS, per);  // every split non-empty
+  const size_t ba = (size_t)Mp * KSTEPS * KB * S, bb = (size_t)Np * KSTEPS * KB * S;
+  const size_t be = sizeof(int) * (size_t)(Mp + Np);
+  const size_t bw = nsplit > 1 ? sizeof(double) * (size_t)nsplit * M * N : 0;
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  static bool pool_ready = false;
+  if (!pool_ready) {  // keep freed scratch mapped in the stream-ordered pool between calls
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_ready = true;
+  }
+  uint8_t* scratch = nullptr;
+  if (cudaMallocAsync((void**)&scratch, al(ba) + al(bb) + al(be) + bw, st) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("ozaki gemm: cannot allocate %zu bytes of scratch", al(ba) + al(bb) + al(be) + bw);
+    return TVK_ERR_CUDA;
+  }
+  int8_t* blobA = (int8_t*)scratch;
+  int8_t* blobB = (int8_t*)(scratch + al(ba));
+  int* ea = (int*)(scratch + al(ba) + al(bb));
+  int* eb = ea + Mp;
+  double* work = nsplit > 1 ? (double*)(scratch + al(ba) + al(bb) + al(be)) : nullptr;
+  // op(A): (m, k) = A[m lda + k] or A[k lda + m];  op(B) as rows n: (n, k) = B[k ldb + n] or B[n ldb + k]
+  if (g.trans_a) split_operand<S>(g.A, M, K, 1, g.lda, BM, Mp, KSTEPS, ea, blobA, st);
+  else split_operand<S>(g.A, M, K, g.lda, 1, BM, Mp, KSTEPS, ea, blobA, st);
+  if (g.trans_b) split_operand<S>(g.B, N, K, g.ldb, 1, BN, Np, KSTEPS, eb, blobB, st);
+  else split_operand<S>(g.B, N, K, 1, g.ldb, BN, Np, KSTEPS, eb, blobB, st);
+  TVK_CHECK_LAUNCH("ozaki split");
+  Args a{};
+  a.A = blobA;
+  a.ea = ea;
+  a.B = blobB;
+  a.eb = eb;
+  a.M = M;
+  a.N = N;
+  a.KSTEPS = KSTEPS;
+  a.mt = mt;
+  a.nt = nt;
+  a.nsplit = nsplit;
+  a.per = per;
+  a.alpha = g.alpha;
+  a.beta = g.beta;
+  a.C = g.C;
+  a.ldc = g.ldc;
+  a.work = work;
+#ifdef TVK_SELECT_DIAG
+  if (const char* d = getenv("TVK_OZ_DEBUG")) a.dbg = atoi(d);
+#endif
+  const size_t smem = (size_t)NST * S * (BM + BN) * KB;
+  auto kern = gemm_i8_kernel<S>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int units = mt * nt * nsplit;
+  const int grid = std::min(units, num_sms());
+  kern<<<grid, NT, smem, st>>>(a);
+  TVK_CHECK_LAUNCH("ozaki gemm");
+  if (nsplit > 1) {
+    const int64_t total = (int64_t)M * N;
+    splitk_sum_kernel<<<(int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
+        work, nsplit, M, N, g.beta, g.C, g.ldc);
+    TVK_CHECK_LAUNCH("ozaki split-K sum");
+  }
+  cudaFreeAsync(scratch, st);
+  return TVK_OK;
+}
+
+}  // namespace oz
+
+int ozaki_gemm(const GemmArgs& p, int digits, cudaStream_t st) {
+  TVK_REQUIRE(p.M >= 0 && p.N >= 0 && p.K >= 0, "dgemm_i8: negative size");
+  TVK_REQUIRE(digits >= 6 && digits <= 8, "dgemm_i8: digits must be 6, 7 or 8");
+  TVK_REQUIRE(p.K <= (1 << 27), "dgemm_i8: K too large");
+  if (p.M == 0 || p.N == 0) return TVK_OK;
+  if (p.K == 0) {  // C = beta C
+    GemmArgs q = p;
+    q.batch = 1;
+    q.out_mode = TVK_OUT_DENSE;
+    q.splits = 1;
+    return gemm(q, st);
+  }
+  switch (digits) {
+    case 6: return oz::run<6>(p, st);
+    case 8: return oz::run<8>(p, st);
+    default: return oz::run<7>(p, st);
+  }
+}
+
+}  // namespace tvk
+
+extern "C" int tvk_dgemm_i8(int trans_a, int trans_b, int m, int n, int k, double alpha, const double* a, int64_t lda,
+                            const double* b, int64_t ldb, double beta, double* c, int64_t ldc, int digits,
+                            void* stream) {
+  tvk::GemmArgs p{};
+  p.trans_a = trans_a;
+  p.trans_b = trans_b;
+  p.M = m;
+  p.N = n;
+  p.K = k;
+  p.alpha = alpha;
+  p.A = a;
+  p.lda = lda;
+  p.B = b;
+  p.ldb = ldb;
+  p.beta = beta;
+  p.C = c;
+  p.ldc = ldc;
+  p.batch = 1;
+  p.out_mode = TVK_OUT_DENSE;
+  p.splits = 1;
+  return tvk::ozaki_gemm(p, digits, (cudaStream_t)stream);
+}

@@ -32,9 +32,14 @@ def _rel(a, b):
     return float(np.max(np.abs(np.asarray(a) - b)) / max(np.max(np.abs(b)), 1e-300))
 
 
+@pytest.mark.parametrize("engine", ["int8-all", "default"])
 @pytest.mark.parametrize("case", cases.EM2048_CASES, ids=[c[0] for c in cases.EM2048_CASES])
-def test_em_at_metric_shape_matches_reference(gpu, monkeypatch, case):
+def test_em_at_metric_shape_matches_reference(gpu, monkeypatch, case, engine):
+    """``int8-all``: all four E-step contractions on the int8 tensor-core FP64 emulation (the 16-
+    utterance batches fall below the size cut for b = F W and B += F' phi otherwise)."""
     from paper_1906_08556_b200 import _estep, pipeline as P
+    if engine == "int8-all":
+        monkeypatch.setattr(_estep, "I8_MIN_WORK", 0)
     g = GOLD[case[0]]
     cor, kw = cases.em2048_inputs(case)
     assert cases.digest(*[cor.features[u] for u in cor.ids]) == str(g["feat_digest"][0]), "generator drifted"
