@@ -77,9 +77,17 @@ int tvk_dgemm(int trans_a, int trans_b, int m, int n, int k, double alpha, const
  * `digits` (6..8) signed 7-bit digits, the digit products are summed exactly in int32 and combined in
  * FP64; |error| <= (2 + digits) 2^(-7 digits) K max_k|op(A)_mk| max_k|op(B)_kn| (digits = 7: 2^-45.8 K
  * max max).  The E-step contractions L = N U, A += N'M, b = F W, B += F' phi (tvm.py:183-200, 283-302)
- * run here; non-finite inputs give NaN rows / columns.  Bit-reproducible. */
+ * run here; non-finite inputs give NaN rows / columns.  Bit-reproducible.
+ * An operand that is reused across calls (U and W within an EM iteration) can be split once with
+ * tvk_i8_split into a buffer of tvk_i8_operand_bytes(rows, k, row_tile, digits) bytes -- op(A) as its
+ * m rows with row_tile 128, op(B) as its n columns (rows of op(B)^T) with row_tile 64, element (r, kk)
+ * at x[r * rs + kk * ks] -- and passed as a_split / b_split (then a / b are not read). */
+int64_t tvk_i8_operand_bytes(int rows, int k, int row_tile, int digits);
+int tvk_i8_split(const double* x, int rows, int k, int64_t rs, int64_t ks, int row_tile, int digits, void* out,
+                 void* stream);
 int tvk_dgemm_i8(int trans_a, int trans_b, int m, int n, int k, double alpha, const double* a, int64_t lda,
-                 const double* b, int64_t ldb, double beta, double* c, int64_t ldc, int digits, void* stream);
+                 const void* a_split, const double* b, int64_t ldb, const void* b_split, double beta, double* c,
+                 int64_t ldc, int digits, void* stream);
 
 /* Fixed-order reductions (bit-reproducible, no atomics):
  *   tvk_colsum: out[j] = beta*out[j] + alpha * sum_r a[r*lda + j]   (rows x cols)

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import call, dgemm, dgemm_i8, ptr, stream
+from ._lib import call, dgemm, dgemm_i8, i8_split_b, ptr, stream
 
 LOG_2PI = float(np.log(2.0 * np.pi))
 E_STEP_BATCH = 1024  # utterances per device E-step batch
@@ -33,10 +33,18 @@ I8_DIGITS_F = 8   # contractions over the first-order statistics (b = F W, B += 
 I8_MIN_WORK = 1 << 30
 
 
-def egemm(a, b, c, m, n, k, *, trans_a=False, beta=0.0, splits=1, work=None, digits=None):
-    """One of the E-step contractions C = op(A) B + beta C on the configured engine."""
+def egemm(a, b, c, m, n, k, *, trans_a=False, beta=0.0, splits=1, work=None, digits=None, cache=None):
+    """One of the E-step contractions C = op(A) B + beta C on the configured engine.  ``cache``: a dict
+    that keeps B's int8 digits for later calls (B constant within an EM iteration: U, W)."""
     if GEMM_ENGINE == "int8" and m * n * k >= I8_MIN_WORK:
-        return dgemm_i8(a, b, c, m, n, k, trans_a=trans_a, beta=beta, digits=digits or I8_DIGITS)
+        digits = digits or I8_DIGITS
+        b_split = None
+        if cache is not None:
+            key = (digits, k, n)
+            if key not in cache:
+                cache[key] = i8_split_b(b, k, n, digits=digits)
+            b_split = cache[key]
+        return dgemm_i8(a, b, c, m, n, k, trans_a=trans_a, beta=beta, digits=digits, b_split=b_split)
     return dgemm(a, b, c, m, n, k, trans_a=trans_a, beta=beta, splits=splits, work=work)
 
 
@@ -122,6 +130,8 @@ class Workspace:
         self.bad = bad
         self.W = _lib.empty((C, F, D))
         self.Upk = _lib.empty((C, packed_size(D)))
+        self.i8_U = {}  # int8 digits of Upk / W for the E-step contractions (built on first use)
+        self.i8_W = {}
         if D:
             # W_c = Sigma_c^-1 T_c   (C x [F x F . F x D])
             dgemm(self.Sinv, dm.T, self.W, F, D, F, batch=C, stride_a=F * F, stride_b=F * D, stride_c=F * D)
@@ -174,13 +184,14 @@ def posterior_batch(dm: DeviceModel, ws: Workspace, n, fm, want_moment=True, sta
     C, F, D = dm.C, dm.F, dm.D
     P = packed_size(D)
     Lpk = _lib.empty((Ub, P))
-    egemm(n, ws.Upk, Lpk, Ub, P, C)  # L - I = sum_c n_c U_c
+    egemm(n, ws.Upk, Lpk, Ub, P, C, cache=ws.i8_U)  # L - I = sum_c n_c U_c
     b = _lib.empty((Ub, D))
     b.copy_(torch.from_numpy(dm.prior_mean).to(b.device).expand(Ub, D))
     K = C * F
     splits = max(1, min(16, K // 2048)) if Ub * D < 148 * 128 * 128 else 1
     work = _lib.empty((splits * Ub * D,)) if splits > 1 else None
-    egemm(fm, ws.W, b, Ub, D, K, beta=1.0, splits=splits, work=work, digits=I8_DIGITS_F)  # b = p e1 + sum W_c' f_c
+    egemm(fm, ws.W, b, Ub, D, K, beta=1.0, splits=splits, work=work, digits=I8_DIGITS_F,
+          cache=ws.i8_W)  # b = p e1 + sum_c W_c' f_c
     phi = _lib.empty((Ub, D))
     Mpk = Lpk if want_moment else None  # factored in place: M overwrites L (L2-resident working set)
     logdet = _lib.empty((Ub,))

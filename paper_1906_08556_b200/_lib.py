@@ -38,7 +38,9 @@ SIGNATURES = {
     "tvk_last_error": (_i, [ctypes.c_char_p, _i64]),
     "tvk_dgemm": (_i, [_i, _i, _i, _i, _i, _d, _p, _i64, _i64, _p, _i64, _i64, _d, _p, _i64, _i64, _i, _i, _i,
                        _p, _p]),
-    "tvk_dgemm_i8": (_i, [_i, _i, _i, _i, _i, _d, _p, _i64, _p, _i64, _d, _p, _i64, _i, _p]),
+    "tvk_dgemm_i8": (_i, [_i, _i, _i, _i, _i, _d, _p, _i64, _p, _p, _i64, _p, _d, _p, _i64, _i, _p]),
+    "tvk_i8_operand_bytes": (_i64, [_i, _i, _i, _i]),
+    "tvk_i8_split": (_i, [_p, _i, _i, _i64, _i64, _i, _i, _p, _p]),
     "tvk_colsum": (_i, [_p, _i64, _i64, _i64, _d, _d, _p, _p]),
     "tvk_ddot_workspace_bytes": (_i64, []),
     "tvk_ddot": (_i, [_p, _p, _i64, _d, _d, _p, _p, _p]),
@@ -209,18 +211,30 @@ def dgemm(a, b, c, m, n, k, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0
 
 
 def dgemm_i8(a, b, c, m, n, k, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0, lda=None, ldb=None, ldc=None,
-             digits=7):
+             digits=7, a_split=None, b_split=None):
     """C = alpha op(A) op(B) + beta C (row-major, FP64) emulated on the int8 tensor cores (Ozaki digits,
-    exact int32 products; include/tvk.h tvk_dgemm_i8)."""
+    exact int32 products; include/tvk.h tvk_dgemm_i8).  a_split / b_split: operands pre-split with
+    i8_split (then a / b may be None)."""
     if lda is None:
         lda = m if trans_a else k
     if ldb is None:
         ldb = k if trans_b else n
     if ldc is None:
         ldc = n
-    call("tvk_dgemm_i8", int(trans_a), int(trans_b), m, n, k, alpha, ptr(a), lda, ptr(b), ldb, beta, ptr(c), ldc,
-         int(digits), stream())
+    call("tvk_dgemm_i8", int(trans_a), int(trans_b), m, n, k, alpha, ptr(a), lda, ptr(a_split), ptr(b), ldb,
+         ptr(b_split), beta, ptr(c), ldc, int(digits), stream())
     return c
+
+
+def i8_split_b(b, k, n, *, trans_b=False, ldb=None, digits=7):
+    """Split op(B) (k x n, row-major B or B^T) once for repeated dgemm_i8(..., b_split=...) calls."""
+    if ldb is None:
+        ldb = k if trans_b else n
+    nbytes = int(load().tvk_i8_operand_bytes(n, k, 64, digits))
+    out = empty((nbytes,), torch.uint8)
+    rs, ks = (ldb, 1) if trans_b else (1, ldb)
+    call("tvk_i8_split", ptr(b), n, k, rs, ks, 64, int(digits), ptr(out), stream())
+    return out
 
 
 def x_args(x):

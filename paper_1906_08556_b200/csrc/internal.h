@@ -23,7 +23,7 @@ struct GemmArgs {
 
 int gemm(const GemmArgs& p, cudaStream_t st);
 // FP64 GEMM emulated on the int8 tensor cores (ozaki.cu), dense unbatched C = alpha op(A) op(B) + beta C
-int ozaki_gemm(const GemmArgs& p, int digits, cudaStream_t st);
+int ozaki_gemm(const GemmArgs& p, int digits, const void* a_split, const void* b_split, cudaStream_t st);
 
 // small batched SPD factor / inverse / log-determinant (n <= kSmallSpdMax)
 constexpr int kSmallSpdMax = 96;

@@ -101,41 +101,60 @@ __global__ void row_exp_kernel(const double* __restrict__ x, int R, int K, int64
   }
 }
 
-// one thread per (row, 16-element k chunk): S digit bytes x 16 -> S 16-byte stores
+// One CTA per (RT-row tile, 128/RT k-steps): the RT x 32 (x 128/RT) block is staged in shared memory
+// with coalesced loads along whichever of rows / k is contiguous, every thread cuts one (row, 16-k)
+// chunk into S digits, and each digit tile is written as one contiguous, fully coalesced block.
 template <int S>
-__global__ void split_kernel(const double* __restrict__ x, int R, int K, int64_t rs, int64_t ks, const int* __restrict__ e,
-                             int RT, int Rp, int KSTEPS, bool rows_fast, int8_t* __restrict__ blob) {
-  const int KC = KSTEPS * 2;
-  const int64_t total = (int64_t)Rp * KC;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int r = rows_fast ? (int)(idx % Rp) : (int)(idx / KC);
-    const int kc = rows_fast ? (int)(idx / Rp) : (int)(idx % KC);
-    uint32_t w[S][4];
-#pragma unroll
-    for (int s = 0; s < S; s++) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0u;
-    if (r < R) {
-      const int er = e[r];
-      const double sc = (er == EXP_BAD || er == EXP_NONE) ? 0.0 : ldexp(1.0, -er);
-#pragma unroll
-      for (int i = 0; i < 16; i++) {
-        const int k = kc * 16 + i;
-        double v = k < K ? x[(int64_t)r * rs + (int64_t)k * ks] * sc : 0.0;  // exact power-of-two scaling
-#pragma unroll
-        for (int s = 0; s < S; s++) {
-          v *= 128.0;
-          const double d = trunc(v);
-          v -= d;
-          w[s][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)d) << (8 * (i & 3));
-        }
-      }
+__global__ void __launch_bounds__(256) split_tile_kernel(const double* __restrict__ x, int R, int K, int64_t rs,
+                                                         int64_t ks, const int* __restrict__ e, int RT, int KSTEPS,
+                                                         int8_t* __restrict__ blob) {
+  __shared__ double tile[128][KB + 1];
+  const int tid = threadIdx.x;
+  const int per = 128 / RT;  // k-steps per CTA
+  const int rb = blockIdx.x, ks0 = blockIdx.y * per;
+  const int r0 = rb * RT;
+  // stage: local row lr = q * RT + rr holds row r0 + rr, k-step ks0 + q
+  const bool rows_fast = rs == 1;
+  for (int i = tid; i < 128 * KB; i += 256) {
+    int lr, kk;
+    if (rows_fast) {
+      lr = i % 128;
+      kk = i / 128;
+    } else {
+      lr = i / KB;
+      kk = i % KB;
     }
-    const int rb = r / RT, rr = r % RT, kst = kc >> 1;
-    int8_t* dst = blob + (((int64_t)rb * KSTEPS + kst) * S) * (RT * KB) + (rr >> 3) * 256 + (kc & 1) * 128 + (rr & 7) * 16;
-#pragma unroll
-    for (int s = 0; s < S; s++)
-      *reinterpret_cast<uint4*>(dst + (int64_t)s * RT * KB) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+    const int q = lr / RT, rr = lr % RT;
+    const int r = r0 + rr, k = (ks0 + q) * KB + kk;
+    tile[lr][kk] = (r < R && k < K && ks0 + q < KSTEPS) ? x[(int64_t)r * rs + (int64_t)k * ks] : 0.0;
   }
+  __syncthreads();
+  // thread -> (local row, k half) so that consecutive threads write consecutive 16-byte chunks:
+  // chunk offset (rr / 8) * 256 + half * 128 + (rr % 8) * 16 inside a digit tile
+  const int lr = (tid >> 4) * 8 + (tid & 7), half = (tid >> 3) & 1;
+  const int q = lr / RT, rr = lr % RT;
+  if (ks0 + q >= KSTEPS) return;
+  const int r = r0 + rr;
+  const int er = r < R ? e[r] : EXP_NONE;
+  const double sc = (er == EXP_BAD || er == EXP_NONE) ? 0.0 : ldexp(1.0, -er);
+  uint32_t w[S][4];
+#pragma unroll
+  for (int t = 0; t < S; t++) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
+#pragma unroll
+  for (int i = 0; i < 16; i++) {
+    double v = tile[lr][half * 16 + i] * sc;  // exact power-of-two scaling, |v| < 1
+#pragma unroll
+    for (int t = 0; t < S; t++) {
+      v *= 128.0;
+      const double d = trunc(v);
+      v -= d;
+      w[t][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)d) << (8 * (i & 3));
+    }
+  }
+  int8_t* dst = blob + (((int64_t)rb * KSTEPS + ks0 + q) * S) * (RT * KB) + (rr >> 3) * 256 + half * 128 + (rr & 7) * 16;
+#pragma unroll
+  for (int t = 0; t < S; t++)
+    *reinterpret_cast<uint4*>(dst + (int64_t)t * RT * KB) = make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]);
 }
 
 // ---------------------------------------------------------------- GEMM
@@ -333,20 +352,26 @@ static int num_sms() {
 
 // digits of a logical R x K operand into blob (RT-row tiles), exponents into e
 template <int S>
-static void split_operand(const double* x, int R, int K, int64_t rs, int64_t ks, int RT, int Rp, int KSTEPS, int* e,
+static void split_operand(const double* x, int R, int K, int64_t rs, int64_t ks, int RT, int KSTEPS, int* e,
                           int8_t* blob, cudaStream_t st) {
   cudaMemsetAsync(e, 0xC0, sizeof(int) * R, st);
   const int rb = (R + 31) / 32;
   int kch = std::max(1, (int)std::min<int64_t>(K, (int64_t)K * rb / (num_sms() * 8) + 1));
   kch = std::max(kch, 256);
   row_exp_kernel<<<dim3(rb, (K + kch - 1) / kch), 256, 0, st>>>(x, R, K, rs, ks, kch, e);
-  const int64_t total = (int64_t)Rp * KSTEPS * 2;
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
-  split_kernel<S><<<blocks, 256, 0, st>>>(x, R, K, rs, ks, e, RT, Rp, KSTEPS, rs == 1, blob);
+  const int per = 128 / RT;
+  split_tile_kernel<S><<<dim3((R + RT - 1) / RT, (KSTEPS + per - 1) / per), 256, 0, st>>>(x, R, K, rs, ks, e, RT,
+                                                                                         KSTEPS, blob);
+}
+
+// bytes of a split operand: digit blob (rows padded to the row tile, K to 32) then int32 row exponents
+static size_t operand_bytes(int R, int K, int RT, int S) {
+  const size_t Rp = (size_t)(R + RT - 1) / RT * RT, KSTEPS = (size_t)(K + KB - 1) / KB;
+  return ((Rp * KSTEPS * KB * S + 255) & ~size_t(255)) + sizeof(int) * Rp;
 }
 
 template <int S>
-static int run(const GemmArgs& g, cudaStream_t st) {
+static int run(const GemmArgs& g, const void* a_split, const void* b_split, cudaStream_t st) {
   const int M = g.M, N = g.N, K = g.K;
   const int mt = ceil_div(M, BM), nt = ceil_div(N, BN), KSTEPS = ceil_div(K, KB);
   const int Mp = mt * BM, Np = nt * BN;
@@ -357,10 +382,9 @@ static int run(const GemmArgs& g, cudaStream_t st) {
   while ((int64_t)S * ceil_div(KSTEPS, nsplit) * KB * 127 * 127 >= (1ll << 31)) nsplit *= 2;
   const int per = ceil_div(KSTEPS, nsplit);
   nsplit = ceil_div(KSTEPS, per);  // every split non-empty
-  const size_t ba = (size_t)Mp * KSTEPS * KB * S, bb = (size_t)Np * KSTEPS * KB * S;
-  const size_t be = sizeof(int) * (size_t)(Mp + Np);
-  const size_t bw = nsplit > 1 ? sizeof(double) * (size_t)nsplit * M * N : 0;
   auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  const size_t ba = a_split ? 0 : operand_bytes(M, K, BM, S), bb = b_split ? 0 : operand_bytes(N, K, BN, S);
+  const size_t bw = nsplit > 1 ? sizeof(double) * (size_t)nsplit * M * N : 0;
   static bool pool_ready = false;
   if (!pool_ready) {  // keep freed scratch mapped in the stream-ordered pool between calls
     int dev = 0;
@@ -372,21 +396,27 @@ static int run(const GemmArgs& g, cudaStream_t st) {
     pool_ready = true;
   }
   uint8_t* scratch = nullptr;
-  if (cudaMallocAsync((void**)&scratch, al(ba) + al(bb) + al(be) + bw, st) != cudaSuccess) {
+  if (ba + bb + bw > 0 && cudaMallocAsync((void**)&scratch, al(ba) + al(bb) + bw, st) != cudaSuccess) {
     cudaGetLastError();
-    set_error("ozaki gemm: cannot allocate %zu bytes of scratch", al(ba) + al(bb) + al(be) + bw);
+    set_error("ozaki gemm: cannot allocate %zu bytes of scratch", al(ba) + al(bb) + bw);
     return TVK_ERR_CUDA;
   }
-  int8_t* blobA = (int8_t*)scratch;
-  int8_t* blobB = (int8_t*)(scratch + al(ba));
-  int* ea = (int*)(scratch + al(ba) + al(bb));
-  int* eb = ea + Mp;
-  double* work = nsplit > 1 ? (double*)(scratch + al(ba) + al(bb) + al(be)) : nullptr;
+  const uint8_t* opA = a_split ? (const uint8_t*)a_split : scratch;
+  const uint8_t* opB = b_split ? (const uint8_t*)b_split : scratch + al(ba);
+  const int8_t* blobA = (const int8_t*)opA;
+  const int8_t* blobB = (const int8_t*)opB;
+  const int* ea = (const int*)(opA + ((size_t)Mp * KSTEPS * KB * S + 255 & ~size_t(255)));
+  const int* eb = (const int*)(opB + ((size_t)Np * KSTEPS * KB * S + 255 & ~size_t(255)));
+  double* work = nsplit > 1 ? (double*)(scratch + al(ba) + al(bb)) : nullptr;
   // op(A): (m, k) = A[m lda + k] or A[k lda + m];  op(B) as rows n: (n, k) = B[k ldb + n] or B[n ldb + k]
-  if (g.trans_a) split_operand<S>(g.A, M, K, 1, g.lda, BM, Mp, KSTEPS, ea, blobA, st);
-  else split_operand<S>(g.A, M, K, g.lda, 1, BM, Mp, KSTEPS, ea, blobA, st);
-  if (g.trans_b) split_operand<S>(g.B, N, K, g.ldb, 1, BN, Np, KSTEPS, eb, blobB, st);
-  else split_operand<S>(g.B, N, K, 1, g.ldb, BN, Np, KSTEPS, eb, blobB, st);
+  if (!a_split) {
+    if (g.trans_a) split_operand<S>(g.A, M, K, 1, g.lda, BM, KSTEPS, (int*)ea, (int8_t*)blobA, st);
+    else split_operand<S>(g.A, M, K, g.lda, 1, BM, KSTEPS, (int*)ea, (int8_t*)blobA, st);
+  }
+  if (!b_split) {
+    if (g.trans_b) split_operand<S>(g.B, N, K, g.ldb, 1, BN, KSTEPS, (int*)eb, (int8_t*)blobB, st);
+    else split_operand<S>(g.B, N, K, 1, g.ldb, BN, KSTEPS, (int*)eb, (int8_t*)blobB, st);
+  }
   TVK_CHECK_LAUNCH("ozaki split");
   Args a{};
   a.A = blobA;
@@ -421,13 +451,13 @@ static int run(const GemmArgs& g, cudaStream_t st) {
         work, nsplit, M, N, g.beta, g.C, g.ldc);
     TVK_CHECK_LAUNCH("ozaki split-K sum");
   }
-  cudaFreeAsync(scratch, st);
+  if (scratch) cudaFreeAsync(scratch, st);
   return TVK_OK;
 }
 
 }  // namespace oz
 
-int ozaki_gemm(const GemmArgs& p, int digits, cudaStream_t st) {
+int ozaki_gemm(const GemmArgs& p, int digits, const void* a_split, const void* b_split, cudaStream_t st) {
   TVK_REQUIRE(p.M >= 0 && p.N >= 0 && p.K >= 0, "dgemm_i8: negative size");
   TVK_REQUIRE(digits >= 6 && digits <= 8, "dgemm_i8: digits must be 6, 7 or 8");
   TVK_REQUIRE(p.K <= (1 << 27), "dgemm_i8: K too large");
@@ -440,17 +470,41 @@ int ozaki_gemm(const GemmArgs& p, int digits, cudaStream_t st) {
     return gemm(q, st);
   }
   switch (digits) {
-    case 6: return oz::run<6>(p, st);
-    case 8: return oz::run<8>(p, st);
-    default: return oz::run<7>(p, st);
+    case 6: return oz::run<6>(p, a_split, b_split, st);
+    case 8: return oz::run<8>(p, a_split, b_split, st);
+    default: return oz::run<7>(p, a_split, b_split, st);
   }
 }
 
 }  // namespace tvk
 
+extern "C" int64_t tvk_i8_operand_bytes(int rows, int k, int row_tile, int digits) {
+  if (rows < 0 || k < 0 || (row_tile != 64 && row_tile != 128) || digits < 6 || digits > 8) return -1;
+  return (int64_t)tvk::oz::operand_bytes(rows, k, row_tile, digits);
+}
+
+extern "C" int tvk_i8_split(const double* x, int rows, int k, int64_t rs, int64_t ks, int row_tile, int digits,
+                            void* out, void* stream) {
+  TVK_REQUIRE(rows >= 0 && k >= 0 && (row_tile == 64 || row_tile == 128), "i8_split: bad shape / row tile");
+  TVK_REQUIRE(digits >= 6 && digits <= 8, "i8_split: digits must be 6, 7 or 8");
+  if (rows == 0 || k == 0) return TVK_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int KSTEPS = (k + tvk::oz::KB - 1) / tvk::oz::KB;
+  const int Rp = (rows + row_tile - 1) / row_tile * row_tile;
+  int8_t* blob = (int8_t*)out;
+  int* e = (int*)((uint8_t*)out + (((size_t)Rp * KSTEPS * tvk::oz::KB * digits + 255) & ~size_t(255)));
+  switch (digits) {
+    case 6: tvk::oz::split_operand<6>(x, rows, k, rs, ks, row_tile, KSTEPS, e, blob, st); break;
+    case 8: tvk::oz::split_operand<8>(x, rows, k, rs, ks, row_tile, KSTEPS, e, blob, st); break;
+    default: tvk::oz::split_operand<7>(x, rows, k, rs, ks, row_tile, KSTEPS, e, blob, st); break;
+  }
+  TVK_CHECK_LAUNCH("i8_split");
+  return TVK_OK;
+}
+
 extern "C" int tvk_dgemm_i8(int trans_a, int trans_b, int m, int n, int k, double alpha, const double* a, int64_t lda,
-                            const double* b, int64_t ldb, double beta, double* c, int64_t ldc, int digits,
-                            void* stream) {
+                            const void* a_split, const double* b, int64_t ldb, const void* b_split, double beta,
+                            double* c, int64_t ldc, int digits, void* stream) {
   tvk::GemmArgs p{};
   p.trans_a = trans_a;
   p.trans_b = trans_b;
@@ -468,5 +522,5 @@ extern "C" int tvk_dgemm_i8(int trans_a, int trans_b, int m, int n, int k, doubl
   p.batch = 1;
   p.out_mode = TVK_OUT_DENSE;
   p.splits = 1;
-  return tvk::ozaki_gemm(p, digits, (cudaStream_t)stream);
+  return tvk::ozaki_gemm(p, digits, a_split, b_split, (cudaStream_t)stream);
 }

@@ -82,6 +82,22 @@ def test_dgemm_i8_reproducible_and_zero_nan_rows(gpu):
     assert torch.allclose(a[ok], ref[ok], rtol=1e-11, atol=1e-11)
 
 
+def test_presplit_operand_matches_inline_split(gpu):
+    from paper_1906_08556_b200 import _lib
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(5)
+    M, N, K = 300, 200, 1000
+    A = torch.randn(M, K, device=dev, dtype=torch.float64, generator=g)
+    B = torch.randn(K, N, device=dev, dtype=torch.float64, generator=g)
+    for digits in (7, 8):
+        c1 = torch.zeros(M, N, device=dev, dtype=torch.float64)
+        c2 = torch.zeros(M, N, device=dev, dtype=torch.float64)
+        _lib.dgemm_i8(A, B, c1, M, N, K, digits=digits)
+        bs = _lib.i8_split_b(B, K, N, digits=digits)
+        _lib.dgemm_i8(A, None, c2, M, N, K, digits=digits, b_split=bs)
+        assert torch.equal(c1, c2)
+
+
 def test_estep_engine_int8_matches_dmma(gpu, monkeypatch):
     """One E-step accumulation at C=256, F=24, D=96 on both engines (all four contractions forced onto
     the int8 emulation): accumulators agree to 1e-11 relative."""
