@@ -52,6 +52,16 @@ def f16_peak():
     except Exception:
         return 1590.0, "fallback bf16 1.59 PF (B200_PROFILING.md)"
 FP64_PEAK_FILE = os.path.join(REPO, "profiles", "r01_fp64_pipe_peak.txt")
+I8_PEAK_FILE = os.path.join(REPO, "profiles", "r02_i8_peak.txt")
+
+
+def i8_peak():
+    """Measured tcgen05 kind::i8 issue rate (SS operands, N >= 128) on this pool's B200 (tools/i8_probe.cu)."""
+    try:
+        vals = [float(l.split()[-2]) for l in open(I8_PEAK_FILE) if l.startswith("i8 SS")]
+        return max(vals), "measured tcgen05 kind::i8 SS issue rate (profiles/r02_i8_peak.txt)"
+    except Exception:
+        return 4500.0, "nominal B200 dense int8 4.5 POPS"
 
 
 def log(*a):
@@ -545,9 +555,29 @@ def em_setup(pkg, gen, n_local, rank, dev, cfg_kw, first_utt=0):
     return tr, ubm_diag.copy(), ubm_full.covariances, store, model
 
 
+def estep_i8_work(n_utts):
+    """(executed int8 ops, FP64-equivalent 2MNK flops) of the four E-step contractions of one EM
+    iteration over n_utts utterances, batched as _estep does."""
+    from paper_1906_08556_b200 import _estep
+    P = D_TVM * (D_TVM + 1) // 2
+    up = lambda v, t: -(-v // t) * t
+    ops = eq = 0
+    left = n_utts
+    while left > 0:
+        ub = min(left, _estep.E_STEP_BATCH)
+        left -= ub
+        for (m, n, k, s) in ((ub, P, C, _estep.I8_DIGITS), (C, P, ub, _estep.I8_DIGITS),
+                             (ub, D_TVM, C * F, _estep.I8_DIGITS_F), (C * F, D_TVM, ub, _estep.I8_DIGITS_F)):
+            if m * n * k < _estep.I8_MIN_WORK:
+                continue
+            ops += 2 * up(m, 128) * up(n, 64) * up(k, 32) * s * (s + 1) // 2
+            eq += 2 * m * n * k
+    return ops, eq
+
+
 def em_kernel_breakdown(tr, it, align_diag, align_cov):
     """One extra EM iteration under the torch profiler (CUPTI kernel timestamps; outside every timed
-    region): device time per kernel, and the achieved rate of the dominant kernel (gemm_kernel)."""
+    region): device time per kernel, and the achieved rate of the dominant kernel (gemm_i8_kernel)."""
     import torch
     from torch.profiler import ProfilerActivity, profile
     torch.cuda.synchronize()
@@ -613,16 +643,24 @@ def bench_em_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, form, n_g
            "aux_last": auxes[-1]}
     if profile_kernels and rank == 0:
         tot, kern = em_kernel_breakdown(tr, it + 1, align_diag, align_cov)
-        g = kern.get("gemm_kernel")
-        peak, src = fp64_peak()
+        g = kern.get("gemm_i8_kernel")
         if g:
-            gflop = (hi - lo) * FLOP_EM_GEMM_UTT + FLOP_EM_GEMM_FIXED
-            ach = gflop / g["s"] / 1e12
-            out["roofline"] = {"bound": "tensor", "kernel": "gemm_kernel (FP64 DMMA: L = N U, b = F W, A += N'M, "
-                                                            "B += F'phi, workspace, T B', T R)",
-                               "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                               "peak_source": src, "flop_per_iter": gflop, "kernel_s_per_iter": g["s"],
+            ops, fp64_eq = estep_i8_work(hi - lo)
+            peak, src = i8_peak()
+            dpeak, dsrc = fp64_peak()
+            ach = ops / g["s"] / 1e12
+            out["roofline"] = {"bound": "tensor", "kernel": "gemm_i8_kernel (FP64 emulated on the int8 tensor cores: "
+                                                            "L = N U, A += N'M, b = F W, B += F'phi)",
+                               "achieved": ach, "peak": peak, "unit": "TOP/s", "frac": ach / peak,
+                               "peak_source": src, "int8_ops_per_iter": ops, "kernel_s_per_iter": g["s"],
                                "share_of_kernel_time": g["share"],
+                               "fp64_equivalent_tflops": fp64_eq / g["s"] / 1e12,
+                               "fp64_equivalent_vs_dmma_ceiling": fp64_eq / g["s"] / 1e12 / dpeak,
+                               "dmma_ceiling": dpeak, "dmma_ceiling_source": dsrc,
+                               "note": "achieved = executed int8 multiply-adds x 2 of the digit products "
+                                       "(S(S+1)/2 per tile, S = 7 for the N contractions, 8 for the F ones, "
+                                       "padded tiles) / CUPTI kernel time; fp64_equivalent = 2MNK of the four "
+                                       "contractions / the same time",
                                "method": "torch.profiler (CUPTI) kernel durations of one extra iteration"}
         out["kernel_breakdown"] = {"kernel_s_per_iter": tot, "top": kern}
     del tr, store

@@ -22,7 +22,7 @@ from . import _lib
 from ._lib import call, dgemm, dgemm_i8, i8_split_b, ptr, stream
 
 LOG_2PI = float(np.log(2.0 * np.pi))
-E_STEP_BATCH = 1024  # utterances per device E-step batch
+E_STEP_BATCH = 2048  # utterances per device E-step batch
 # engine of the large E-step contractions: "int8" (tvk_dgemm_i8, FP64 emulated on the int8 tensor
 # cores) or "dmma" (tvk_dgemm); products below I8_MIN_WORK multiply-adds stay on DMMA (the digit
 # split is O((M + N) K) and not worth it for small shapes)

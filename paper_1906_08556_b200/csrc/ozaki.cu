@@ -272,6 +272,8 @@ __global__ void __launch_bounds__(NT, 1) gemm_i8_kernel(Args p) {
       };
       fetch(0);
       const int em = mok ? p.ea[m] : EXP_NONE;
+      // column exponents of this warp's 32 columns: lane j holds column nb + j (shuffled below)
+      const int en_l = nb + lane < p.N ? p.eb[nb + lane] : EXP_NONE;
       tc::mbar_wait(&tfull, li & 1);
       tc::fence_after_sync();
 #pragma unroll 1
@@ -283,12 +285,14 @@ __global__ void __launch_bounds__(NT, 1) gemm_i8_kernel(Args p) {
 #pragma unroll
         for (int j = 0; j < 8; j++) cur[j] = cpre[j];
         if (j0 + 8 < 32) fetch(j0 + 8);
+        int en[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) en[j] = __shfl_sync(0xffffffffu, en_l, j0 + j);
         tc::tmem_ld_wait();
         if (!mok || p.dbg == 1) continue;
+        double r[8];
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-          const int n = nb + j0 + j;
-          if (n >= p.N) break;
           // level L (0-based) carries the products with s + t = L + 2, weight 2^(-7 (L + 2)); the levels
           // are folded exactly into two int64 words (|level| < 2^31: hi < 2^53, lo < 2^52)
           long long hi = 0, lo = 0;
@@ -298,23 +302,27 @@ __global__ void __launch_bounds__(NT, 1) gemm_i8_kernel(Args p) {
           for (int L = NH; L < S; L++) lo += (long long)(int)v[L][j] << (7 * (S - 1 - L));
           double c = (double)hi * (1.0 / (double)(1ll << (7 * (NH + 1))));
           if (S > NH) c = fma((double)lo, ldexp(1.0, -7 * (S + 1)), c);
-          const int en = p.eb[n];
-          double r;
-          if (em == EXP_BAD || en == EXP_BAD) {
-            r = __longlong_as_double(0x7ff8000000000000ll);
-          } else if (em == EXP_NONE || en == EXP_NONE) {
-            r = 0.0;  // an all-zero row or column: all-zero digits
+          const int e2 = em + en[j];
+          if (em == EXP_BAD || en[j] == EXP_BAD) {
+            r[j] = __longlong_as_double(0x7ff8000000000000ll);
+          } else if (em == EXP_NONE || en[j] == EXP_NONE) {
+            r[j] = 0.0;  // an all-zero row or column: all-zero digits
+          } else if (e2 > -1000 && e2 < 1000) {
+            r[j] = p.alpha * (c * __longlong_as_double((long long)(e2 + 1023) << 52));
           } else {
-            const int e2 = em + en;
-            r = p.alpha * (e2 > -1000 && e2 < 1000 ? c * __longlong_as_double((long long)(e2 + 1023) << 52)
-                                                    : ldexp(c, e2));
+            r[j] = p.alpha * ldexp(c, e2);
           }
-          if (p.nsplit > 1) {
-            p.work[((int64_t)sp * p.M + m) * p.N + n] = r;
-          } else {
-            if (rmw) r += p.beta * cur[j];
-            crow[n] = r;
-          }
+        }
+        const int n0 = nb + j0;
+        if (p.nsplit > 1) {
+          double* wrow = p.work + ((int64_t)sp * p.M + m) * p.N;
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            if (n0 + j < p.N) wrow[n0 + j] = r[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            if (n0 + j < p.N) crow[n0 + j] = rmw ? r[j] + p.beta * cur[j] : r[j];
         }
       }
       tc::fence_before_sync();
