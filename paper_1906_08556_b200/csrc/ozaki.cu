@@ -24,7 +24,7 @@
 //
 // Kernel roles (one CTA per SM, persistent over 128 x 64 output tiles, m fastest so concurrent CTAs
 // share the right operand's tiles in L2): warp 0 lane 0 streams the pre-tiled digit blobs with
-// bulk copies (one A and one B copy per k-step), warp 1 lane 0 issues the MMAs, warps 2-9 drain
+// bulk copies (one A and one B copy per k-step), warp 1 lane 0 issues the MMAs, warps 2-17 drain
 // the level accumulators (tcgen05.ld 32x32b.x8), combine them in FP64 and write C.
 //
 // Determinism: integer products are exact and the FP64 combination has a fixed order, so results
@@ -44,7 +44,7 @@ constexpr int BM = 128;   // left rows per tile (MMA M, TMEM lanes)
 constexpr int BN = 64;    // right rows (output columns) per tile and per level block
 constexpr int KB = 32;    // bytes (= int8 elements) of K per k-step (one MMA)
 constexpr int NST = 4;    // ring stages
-constexpr int NT = 320;   // producer, MMA, 8 epilogue warps
+constexpr int NT = 576;   // producer, MMA, 16 epilogue warps
 constexpr int EXP_BAD = 1 << 20;  // row exponent of a row holding a non-finite value
 
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {  // D s32, A/B signed int8, both K-major
@@ -55,6 +55,13 @@ __device__ __forceinline__ void mma_i8_ss(uint32_t d, uint64_t a, uint64_t b, ui
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_i8_kernel(Args p) {
       tc::mbar_init(&empty[i], 1);
     }
     tc::mbar_init(&tfull, 1);
-    tc::mbar_init(&tempty, 8);
+    tc::mbar_init(&tempty, 16);
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
@@ -248,11 +255,14 @@ __global__ void __launch_bounds__(NT, 1) gemm_i8_kernel(Args p) {
       }
     }
   } else {
-    // ------------------------------------------------------------------ epilogue (warps 2-9)
-    // two warps per TMEM lane quarter, each drains 32 of the tile's 64 columns in chunks of 8
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    // ------------------------------------------------------------------ epilogue (warps 2-17)
+    // four warps per TMEM lane quarter, each owns 16 of the tile's 64 columns.  The S level blocks are
+    // read one at a time (tcgen05.ld 32x32b.x16) and folded exactly into two int64 words per column,
+    // then the accumulator is released -- the next tile's MMAs run while the FP64 combination, the
+    // scaling and the stores of this one finish.
+    const int quarter = warp & 3, part = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
-    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16) + 16 * part;
     constexpr int NH = S < 4 ? S : 4;  // levels folded into the high int64 word
     uint32_t li = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, li++) {
@@ -262,72 +272,59 @@ __global__ void __launch_bounds__(NT, 1) gemm_i8_kernel(Args p) {
       const int m = mtile * BM + row;
       const bool mok = m < p.M;
       const bool rmw = mok && p.nsplit == 1 && p.beta != 0.0;
-      double* crow = p.C + (int64_t)(mok ? m : 0) * p.ldc;
-      const int nb = ntile * BN + 32 * half;
-      // C values of the first chunk are fetched before the wait (read-modify-write latency off the path)
-      double cpre[8];
-      auto fetch = [&](int j0) {
-#pragma unroll
-        for (int j = 0; j < 8; j++) cpre[j] = (rmw && nb + j0 + j < p.N) ? crow[nb + j0 + j] : 0.0;
-      };
-      fetch(0);
+      const int nb = ntile * BN + 16 * part;
       const int em = mok ? p.ea[m] : EXP_NONE;
-      // column exponents of this warp's 32 columns: lane j holds column nb + j (shuffled below)
-      const int en_l = nb + lane < p.N ? p.eb[nb + lane] : EXP_NONE;
+      // column exponents of this warp's 16 columns: lane j holds column nb + j (shuffled below)
+      const int en_l = (lane < 16 && nb + lane < p.N) ? p.eb[nb + lane] : EXP_NONE;
       tc::mbar_wait(&tfull, li & 1);
       tc::fence_after_sync();
-#pragma unroll 1
-      for (int j0 = 0; j0 < 32; j0 += 8) {
-        uint32_t v[S][8];
+      long long hi[16], lo[16];
 #pragma unroll
-        for (int L = 0; L < S; L++) tmem_ld8(lane_addr + BN * L + 32 * half + j0, v[L]);
-        double cur[8];
+      for (int j = 0; j < 16; j++) hi[j] = lo[j] = 0;
 #pragma unroll
-        for (int j = 0; j < 8; j++) cur[j] = cpre[j];
-        if (j0 + 8 < 32) fetch(j0 + 8);
-        int en[8];
-#pragma unroll
-        for (int j = 0; j < 8; j++) en[j] = __shfl_sync(0xffffffffu, en_l, j0 + j);
+      for (int L = 0; L < S; L++) {
+        uint32_t v[16];
+        tmem_ld16(lane_addr + BN * L, v);
         tc::tmem_ld_wait();
-        if (!mok || p.dbg == 1) continue;
-        double r[8];
+        // level L (0-based) carries the products with s + t = L + 2, weight 2^(-7 (L + 2)); |level| < 2^31
+        // so hi (levels 0..NH-1) < 2^53 and lo (the rest) < 2^52: exact
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-          // level L (0-based) carries the products with s + t = L + 2, weight 2^(-7 (L + 2)); the levels
-          // are folded exactly into two int64 words (|level| < 2^31: hi < 2^53, lo < 2^52)
-          long long hi = 0, lo = 0;
-#pragma unroll
-          for (int L = 0; L < NH; L++) hi += (long long)(int)v[L][j] << (7 * (NH - 1 - L));
-#pragma unroll
-          for (int L = NH; L < S; L++) lo += (long long)(int)v[L][j] << (7 * (S - 1 - L));
-          double c = (double)hi * (1.0 / (double)(1ll << (7 * (NH + 1))));
-          if (S > NH) c = fma((double)lo, ldexp(1.0, -7 * (S + 1)), c);
-          const int e2 = em + en[j];
-          if (em == EXP_BAD || en[j] == EXP_BAD) {
-            r[j] = __longlong_as_double(0x7ff8000000000000ll);
-          } else if (em == EXP_NONE || en[j] == EXP_NONE) {
-            r[j] = 0.0;  // an all-zero row or column: all-zero digits
-          } else if (e2 > -1000 && e2 < 1000) {
-            r[j] = p.alpha * (c * __longlong_as_double((long long)(e2 + 1023) << 52));
-          } else {
-            r[j] = p.alpha * ldexp(c, e2);
-          }
-        }
-        const int n0 = nb + j0;
-        if (p.nsplit > 1) {
-          double* wrow = p.work + ((int64_t)sp * p.M + m) * p.N;
-#pragma unroll
-          for (int j = 0; j < 8; j++)
-            if (n0 + j < p.N) wrow[n0 + j] = r[j];
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; j++)
-            if (n0 + j < p.N) crow[n0 + j] = rmw ? r[j] + p.beta * cur[j] : r[j];
+        for (int j = 0; j < 16; j++) {
+          if (L < NH) hi[j] += (long long)(int)v[j] << (7 * (NH - 1 - L));
+          else lo[j] += (long long)(int)v[j] << (7 * (S - 1 - L));
         }
       }
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty);
+      if (p.dbg == 1) continue;  // (warp-uniform) -- rows past M stay convergent for the shuffles below
+      double* crow = p.C + (int64_t)(mok ? m : 0) * p.ldc;
+      double* dst = p.nsplit > 1 ? p.work + ((int64_t)sp * p.M + (mok ? m : 0)) * p.N : crow;
+#pragma unroll
+      for (int h = 0; h < 16; h += 8) {  // two groups of 8 columns (register budget of 576 threads)
+        double cur[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) cur[j] = (rmw && nb + h + j < p.N) ? crow[nb + h + j] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const int en = __shfl_sync(0xffffffffu, en_l, h + j);
+          double c = (double)hi[h + j] * (1.0 / (double)(1ll << (7 * (NH + 1))));
+          if (S > NH) c = fma((double)lo[h + j], ldexp(1.0, -7 * (S + 1)), c);
+          const int e2 = em + en;
+          double r;
+          if (em == EXP_BAD || en == EXP_BAD) {
+            r = __longlong_as_double(0x7ff8000000000000ll);
+          } else if (em == EXP_NONE || en == EXP_NONE) {
+            r = 0.0;  // an all-zero row or column: all-zero digits
+          } else if (e2 > -1000 && e2 < 1000) {
+            r = p.alpha * (c * __longlong_as_double((long long)(e2 + 1023) << 52));
+          } else {
+            r = p.alpha * ldexp(c, e2);
+          }
+          if (rmw) r += p.beta * cur[j];
+          if (mok && nb + h + j < p.N) dst[nb + h + j] = r;
+        }
+      }
     }
   }
   tc::fence_before_sync();
