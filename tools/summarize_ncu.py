@@ -33,6 +33,10 @@ METRICS = {
     "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_mem_active_pct",
     "l1tex__m_xbar2l1tex_read_bytes.sum": "l2_to_sm",
     "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active": "hmma_inst_pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_cycles_active_pct",
+    "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active": "tc_cycles_active_pct",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_tc_wavefronts_pct",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
          "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
