@@ -33,6 +33,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 #include "tc.cuh"
@@ -86,8 +88,9 @@ __global__ void row_exp_kernel(const double* __restrict__ x, int R, int K, int64
     const int r = r0 + lane;
     int mx = EXP_NONE;
     if (r < R)
+#pragma unroll 8
       for (int k = kb + warp; k < ke; k += nwarp) {
-        const double v = x[(int64_t)r * rs + (int64_t)k * ks];
+        const double v = __ldg(x + (int64_t)r * rs + (int64_t)k * ks);
         if (!isfinite(v)) mx = EXP_BAD;
         else if (v != 0.0) mx = max(mx, ilogb(v) + 1);
       }
@@ -97,8 +100,9 @@ __global__ void row_exp_kernel(const double* __restrict__ x, int R, int K, int64
       const int r = r0 + i;
       if (r >= R) break;
       int mx = EXP_NONE;
+#pragma unroll 8
       for (int k = kb + lane; k < ke; k += 32) {
-        const double v = x[(int64_t)r * rs + k];
+        const double v = __ldg(x + (int64_t)r * rs + k);
         if (!isfinite(v)) mx = EXP_BAD;
         else if (v != 0.0) mx = max(mx, ilogb(v) + 1);
       }
@@ -121,20 +125,27 @@ __global__ void __launch_bounds__(256) split_tile_kernel(const double* __restric
   const int rb = blockIdx.x, ks0 = blockIdx.y * per;
   const int r0 = rb * RT;
   // stage: local row lr = q * RT + rr holds row r0 + rr, k-step ks0 + q
-  const bool rows_fast = rs == 1;
-  for (int i = tid; i < 128 * KB; i += 256) {
-    int lr, kk;
-    if (rows_fast) {
-      lr = i % 128;
-      kk = i / 128;
-    } else {
-      lr = i / KB;
-      kk = i % KB;
+  // all 16 loads of a thread are issued before any shared-memory store (independent, in flight together)
+  constexpr int NIT = 128 * KB / 256;
+  double vals[NIT];
+  auto stage = [&](auto rows_fast) {
+#pragma unroll
+    for (int it = 0; it < NIT; it++) {
+      const int i = tid + 256 * it;
+      const int lr = rows_fast ? i % 128 : i / KB, kk = rows_fast ? i / 128 : i % KB;
+      const int q = lr / RT, rr = lr % RT;
+      const int r = r0 + rr, k = (ks0 + q) * KB + kk;
+      vals[it] = (r < R && k < K && ks0 + q < KSTEPS) ? __ldg(x + (int64_t)r * rs + (int64_t)k * ks) : 0.0;
     }
-    const int q = lr / RT, rr = lr % RT;
-    const int r = r0 + rr, k = (ks0 + q) * KB + kk;
-    tile[lr][kk] = (r < R && k < K && ks0 + q < KSTEPS) ? x[(int64_t)r * rs + (int64_t)k * ks] : 0.0;
-  }
+#pragma unroll
+    for (int it = 0; it < NIT; it++) {
+      const int i = tid + 256 * it;
+      const int lr = rows_fast ? i % 128 : i / KB, kk = rows_fast ? i / 128 : i % KB;
+      tile[lr][kk] = vals[it];
+    }
+  };
+  if (rs == 1) stage(std::true_type{});
+  else stage(std::false_type{});
   __syncthreads();
   // thread -> (local row, k half) so that consecutive threads write consecutive 16-byte chunks:
   // chunk offset (rr / 8) * 256 + half * 128 + (rr % 8) * 16 inside a digit tile
