@@ -268,6 +268,127 @@ __global__ void __launch_bounds__(kBwThreads) bw_second_order_kernel(const XT* x
   }
 }
 
+// F <= 64: the same corpus sum as a tensor-pipe product.  Per component, S_c += X_c^T (w X_c) over the
+// component's entries in utterance / frame order: the entry positions of a chunk of utterances are
+// listed once in shared memory (block scan over the utterances' run lengths), then staged 64 entries
+// at a time (x - m_c and w (x - m_c), all 16 loads of a thread in flight together; rows zero-padded
+// to a multiple of 4, columns to 64) and each warp accumulates its share of the 8x8 blocks of the lower
+// triangle with DMMA.8x8x4 (K = entries).  Diagonal blocks store their lower half and mirror it, so
+// S_c stays exactly symmetric.
+constexpr int kSoDmmaChunk = 256;   // utterances per position list
+constexpr int kSoPosCap = 4096;     // positions per list (a longer chunk is split)
+constexpr int kSoEB = 64;           // entries staged per round
+constexpr int kSoLD = 68;           // = 4 mod 16 doubles: conflict-free DMMA fragment loads
+constexpr size_t so_dmma_smem() {
+  return sizeof(double) * 2 * kSoEB * kSoLD + sizeof(int) * (kSoPosCap + 2 * kSoDmmaChunk + 8);
+}
+template <typename XT>
+__global__ void __launch_bounds__(kBwThreads, 2) bw_second_order_dmma_kernel(const XT* x, int F, int U, int C,
+                                                                             const int64_t* utt_frames,
+                                                                             const int64_t* ali_off,
+                                                                             const double* center, double* ssum,
+                                                                             BwWs ws) {
+  extern __shared__ __align__(16) double sod[];
+  double (*xe)[kSoLD] = reinterpret_cast<double (*)[kSoLD]>(sod);
+  double (*wxe)[kSoLD] = reinterpret_cast<double (*)[kSoLD]>(sod + kSoEB * kSoLD);
+  int* pos = reinterpret_cast<int*>(sod + 2 * kSoEB * kSoLD);  // [kSoPosCap] entry positions
+  int* roff = pos + kSoPosCap;                                 // [kSoDmmaChunk + 1] run offsets
+  int* scan = roff + kSoDmmaChunk + 1;                         // [kSoDmmaChunk] block scan scratch
+  const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nbF = (F + 7) / 8, nblk = nbF * (nbF + 1) / 2;
+  constexpr int MAXQ = 5;  // 36 lower 8x8 blocks at F = 64 over 8 warps
+  int bi[MAXQ], bj[MAXQ];
+  double acc[MAXQ][2];
+#pragma unroll
+  for (int q = 0; q < MAXQ; q++) {
+    int b = warp + 8 * q, i = 0;
+    while ((i + 1) * (i + 2) / 2 <= b) i++;  // block b -> (i, j), j <= i, row-major lower
+    bi[q] = i;
+    bj[q] = b - i * (i + 1) / 2;
+    acc[q][0] = acc[q][1] = 0.0;
+  }
+  const int nq = (nblk - warp + 7) / 8;  // blocks of this warp
+  const int64_t ebase = ali_off[utt_frames[0]];
+  const double* mc = center ? center + (int64_t)c * F : nullptr;
+  for (int u0 = 0; u0 < U;) {
+    int nu = min(kSoDmmaChunk, U - u0);
+    __syncthreads();  // the previous list is consumed
+    // run lengths of this component in utterances u0.., exclusive scan -> roff
+    int len = 0, r0 = 0, s0 = 0;
+    if (tid < nu) {
+      const int32_t* cs = ws.comp_start + (int64_t)(u0 + tid) * (C + 1);
+      s0 = cs[c];
+      len = cs[c + 1] - s0;
+      r0 = (int)(ali_off[utt_frames[u0 + tid]] - ebase);
+    }
+    scan[tid] = len;
+    __syncthreads();
+    for (int o = 1; o < kSoDmmaChunk; o <<= 1) {  // Hillis-Steele inclusive scan
+      const int v = tid >= o ? scan[tid - o] : 0;
+      __syncthreads();
+      scan[tid] += v;
+      __syncthreads();
+    }
+    // the chunk's entries in windows of kSoPosCap positions (a long run spans windows)
+    const int total_all = scan[nu - 1];
+    const int off = scan[tid < nu ? tid : 0] - len;
+    for (int w0 = 0; w0 < total_all; w0 += kSoPosCap) {
+      const int total = min(kSoPosCap, total_all - w0);
+      __syncthreads();  // the previous window is consumed
+      if (tid < nu)
+        for (int rr = max(0, w0 - off); rr < len && off + rr < w0 + kSoPosCap; rr++) pos[off + rr - w0] = r0 + s0 + rr;
+      __syncthreads();
+      for (int e0 = 0; e0 < total; e0 += kSoEB) {
+        const int nb = min(kSoEB, total - e0);
+        double v[kSoEB * 64 / kBwThreads], wv[kSoEB * 64 / kBwThreads];
+#pragma unroll
+        for (int i = 0; i < kSoEB * 64 / kBwThreads; i++) {
+          const int idx = tid + kBwThreads * i, e = idx >> 6, j = idx & 63;
+          v[i] = wv[i] = 0.0;
+          if (e < nb && j < F) {
+            const int p = pos[e0 + e];
+            const int tt = ws.sorted_frame[p];
+            double xv = (double)x[(int64_t)tt * F + j];
+            if (mc) xv -= mc[j];
+            v[i] = xv;
+            wv[i] = ws.sorted_w[p] * xv;
+          }
+        }
+        __syncthreads();  // the previous round's DMMAs are done with xe / wxe
+#pragma unroll
+        for (int i = 0; i < kSoEB * 64 / kBwThreads; i++) {
+          const int idx = tid + kBwThreads * i, e = idx >> 6, j = idx & 63;
+          xe[e][j] = v[i];
+          wxe[e][j] = wv[i];
+        }
+        __syncthreads();
+        const int nks = (nb + 3) >> 2;
+        for (int ks = 0; ks < nks; ks++) {
+          const int e = 4 * ks + t4;
+#pragma unroll
+          for (int q = 0; q < MAXQ; q++)
+            if (q < nq) dmma884(acc[q][0], acc[q][1], xe[e][8 * bi[q] + g], wxe[e][8 * bj[q] + g]);
+        }
+      }
+    }
+    u0 += nu;
+  }
+  double* S = ssum + (int64_t)c * F * F;
+#pragma unroll
+  for (int q = 0; q < MAXQ; q++) {
+    if (q >= nq) continue;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int row = 8 * bi[q] + g, col = 8 * bj[q] + 2 * t4 + h;  // D[g][2t + h]
+      if (row >= F || col >= F || col > row) continue;
+      const double val = S[row * F + col] + acc[q][h];
+      S[row * F + col] = val;
+      if (row != col) S[col * F + row] = val;
+    }
+  }
+}
+
 }  // namespace tvk
 
 using namespace tvk;
@@ -301,13 +422,17 @@ extern "C" int tvk_bw_stats(const void* x, int x_f64, int F, const int64_t* utt_
   TVK_CHECK_LAUNCH("bw_first_order");
   if (ssum_acc) {
     TVK_REQUIRE(F <= kSoMaxF, "bw_stats: corpus second order supports F <= 128");
-    if (F <= 63) {
-      if (x_f64)
-        bw_second_order_kernel<double, 8><<<C, kBwThreads, 0, st>>>((const double*)x, F, U, C, utt_frames,
-                                                                    ali_offsets, center, ssum_acc, ws);
-      else
-        bw_second_order_kernel<float, 8><<<C, kBwThreads, 0, st>>>((const float*)x, F, U, C, utt_frames,
-                                                                   ali_offsets, center, ssum_acc, ws);
+    if (F <= 64) {  // DMMA tensor-pipe product
+      const size_t sm = so_dmma_smem();
+      if (x_f64) {
+        cudaFuncSetAttribute(bw_second_order_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        bw_second_order_dmma_kernel<double><<<C, kBwThreads, sm, st>>>((const double*)x, F, U, C, utt_frames,
+                                                                        ali_offsets, center, ssum_acc, ws);
+      } else {
+        cudaFuncSetAttribute(bw_second_order_dmma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        bw_second_order_dmma_kernel<float><<<C, kBwThreads, sm, st>>>((const float*)x, F, U, C, utt_frames,
+                                                                       ali_offsets, center, ssum_acc, ws);
+      }
     } else {
       if (x_f64)
         bw_second_order_kernel<double, 33><<<C, kBwThreads, 0, st>>>((const double*)x, F, U, C, utt_frames,

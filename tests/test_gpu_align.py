@@ -429,3 +429,44 @@ def test_sparse_align_path_matches_reference_golden(gpu, monkeypatch, case):
     got = gpu.gmm.align_frames(dm, fm, x, top_k=k, prune=prune)
     ties = np.flatnonzero(g["boundary_gap"] < TIE_REL * np.maximum(1.0, np.abs(g["sel_full_ll"][:, 0])))
     _assert_alignment_matches(got, g["offsets"], g["components"], g["weights"], ties)
+
+
+@pytest.mark.parametrize("F,long_run", [(60, False), (60, True), (20, False), (64, True), (80, False)])
+def test_corpus_second_order_sum_matches_numpy(gpu, F, long_run):
+    """tvk_bw_stats' corpus second-order sum Ssum_c += sum w (x - m_c)(x - m_c)^T (tvm.py:304) -- the DMMA
+    kernel for F <= 64, the FMA kernel above -- against numpy, including a component run longer than the
+    kernel's 4096-entry position window (one 9000-frame utterance aligned to component 0)."""
+    import torch
+    from paper_1906_08556_b200 import _device, _lib
+    rng = np.random.default_rng(F + long_run)
+    C = 48
+    lens = [9000, 120, 300] if long_run else list(rng.integers(1, 400, 40))
+    T = int(sum(lens))
+    x = rng.standard_normal((T, F)).astype(np.float32)
+    comps, wts, off = [], [], [0]
+    for t in range(T):
+        k = int(rng.integers(1, 5))
+        cs = np.sort(rng.choice(C, k, replace=False))
+        if long_run and t < 9000:
+            cs = np.unique(np.concatenate([[0], cs]))
+        w = rng.random(len(cs)).astype(np.float32)
+        comps += list(cs)
+        wts += list(w / w.sum())
+        off.append(len(comps))
+    comps, wts, off = np.array(comps, np.int32), np.array(wts, np.float32), np.array(off, np.int64)
+    center = rng.standard_normal((C, F))
+    utt = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ssum = _lib.zeros((C, F, F))
+    _device.bw_stats(_lib.to_dev(x), _lib.to_dev(utt, torch.int64), _lib.to_dev(off, torch.int64),
+                     _lib.to_dev(comps, torch.int32), _lib.to_dev(wts, torch.float32), C,
+                     center=_lib.to_dev(center), ssum_acc=ssum)
+    got = _lib.to_host(ssum)
+    ref = np.zeros((C, F, F))
+    fr = np.repeat(np.arange(T), np.diff(off))
+    xd = x.astype(np.float64)
+    for c in range(C):
+        m = comps == c
+        y = xd[fr[m]] - center[c]
+        ref[c] = (y * wts[m].astype(np.float64)[:, None]).T @ y
+    assert np.array_equal(got, np.swapaxes(got, 1, 2))  # exactly symmetric
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
