@@ -260,8 +260,47 @@ def to_host_acc(acc: DeviceAcc, aux):
 # ------------------------------------------------------------------------------- M-step
 
 
+SWEEP_MAX_D = 416  # tvk_posterior's block-sweep kernel (csrc/posterior.cu)
+_TRIL_DEV = {}
+
+
+def unpack_dev(pk, d):
+    """(n, P) packed lower -> (n, D, D) symmetric dense on device (layout only)."""
+    key = (d, pk.device)
+    if key not in _TRIL_DEV:
+        i, j = tril(d)
+        _TRIL_DEV[key] = (torch.from_numpy(i).to(pk.device), torch.from_numpy(j).to(pk.device))
+    i, j = _TRIL_DEV[key]
+    out = torch.empty((pk.shape[0], d, d), dtype=pk.dtype, device=pk.device)
+    out[:, i, j] = pk
+    out[:, j, i] = pk
+    return out
+
+
 def update_T_device(T_old, Apk, B, N, C, F, D):
-    """T_c = B_c A_c^-1 for N_c > 0 (tvm.py:317-334); returns (T_new, status)."""
+    """T_c = B_c A_c^-1 for N_c > 0 (tvm.py:317-334); returns (T_new, status).
+
+    D <= 416: A_c^-1 for all components from one block-sweep pass (the EM posterior kernel without the
+    identity and without b: it returns -(-A^-1)), then one batched DGEMM B_c A_c^-1; components that are
+    starved (N_c <= 0) or whose A_c is not SPD (a non-positive sweep pivot, the Cholesky failure of the
+    reference) keep T_c."""
+    if 0 < D <= SWEEP_MAX_D:
+        P = packed_size(D)
+        inv = _lib.empty((C, P))
+        zb = _lib.zeros((C, D))
+        phi, ld, bp = _lib.empty((C, D)), _lib.empty((C,)), _lib.empty((C,))
+        status = _lib.empty((C,), torch.int32)
+        call("tvk_posterior", ptr(Apk), ptr(zb), C, D, 0, ptr(phi), ptr(inv), ptr(ld), ptr(bp), ptr(status), None, 0,
+             stream())
+        dense = unpack_dev(inv, D)
+        del inv
+        X = _lib.empty((C, F, D))
+        dgemm(B, dense, X, F, D, D, batch=C, stride_a=F * D, stride_b=D * D, stride_c=F * D)
+        skip = N.view(-1) <= 0
+        status = torch.where(skip, torch.full_like(status, _lib.ITEM_SKIPPED), status)
+        keep = (status != _lib.ITEM_OK).view(C, 1, 1)
+        X = torch.where(keep, T_old.view(C, F, D), X)
+        return X, status
     X = T_old.clone()
     skip = (N <= 0).to(torch.int32)
     status = _lib.empty((C,), torch.int32)
