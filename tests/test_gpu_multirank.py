@@ -110,7 +110,9 @@ def test_two_rank_training_extraction_and_accumulation_match_single_rank(gpu, tm
     np.testing.assert_allclose(r["aux"], single["aux"], rtol=1e-12)
     for k in ("T", "Sigma", "ubm_means", "ivectors", "acc_B", "acc_N", "acc_A"):
         assert _rel(r[k], single[k]) < 1e-10, (k, _rel(r[k], single[k]))
-    np.testing.assert_allclose(r["prior"], single["prior"], rtol=1e-12)
+    # (the all-reduce changes the accumulators' summation order: 1e-16-level differences that the EM
+    # iterations amplify, hence the same 1e-10 as the model arrays)
+    np.testing.assert_allclose(r["prior"], single["prior"], rtol=1e-10)
     # accumulate_corpus on an initialised group sums the shards once (not world_size times)
     assert int(r["acc_U"]) == int(single["acc_U"]) == len(cor.ids)
     np.testing.assert_allclose(r["acc_aux"], single["acc_aux"], rtol=1e-12)
