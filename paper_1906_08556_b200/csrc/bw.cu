@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kBwThreads) bw_first_order_kernel(
   // stable scatter (warp 0, entries in order): cnt[] becomes the running cursor
   if (warp == 0) {
     for (int base = 0; base < ne; base += 32) {
+      __syncwarp();  // the previous round's cursor updates (other lanes) are visible to this round's leaders
       int i = base + lane;
       bool act = i < ne;
       unsigned am = __ballot_sync(0xffffffffu, act);
