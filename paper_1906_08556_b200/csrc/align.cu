@@ -405,6 +405,83 @@ __global__ void finalize_kernel(int64_t T, int K, double prune, const int32_t* s
   counts[t] = n;
 }
 
+// Fixed-K variant (the default top-20): the CTA's 128 frames are staged through shared memory with
+// coalesced loads and stores, and every per-frame array lives in registers (static indices: no local
+// memory).  Arithmetic and summation order are finalize_frame's, so the outputs are bit-identical.
+template <int KT>
+__global__ void __launch_bounds__(128) finalize_fixed_kernel(int64_t T, double prune, const int32_t* __restrict__ sel,
+                                                             const double* __restrict__ sel_ll,
+                                                             int32_t* __restrict__ comp_pad, float* __restrict__ w_pad,
+                                                             int64_t* __restrict__ counts) {
+  constexpr int LD = KT + 1;  // odd row stride: conflict-free row-per-thread accesses
+  __shared__ double sll[128 * LD];
+  __shared__ int sid[128 * LD];
+  __shared__ float sw[128 * LD];
+  const int64_t t0 = (int64_t)blockIdx.x * 128;
+  const int nfr = T - t0 < 128 ? (int)(T - t0) : 128;
+  for (int i = threadIdx.x; i < nfr * KT; i += 128) {
+    const int r = i / KT, c = i - r * KT;
+    sll[r * LD + c] = sel_ll[t0 * KT + i];
+    sid[r * LD + c] = sel[t0 * KT + i];
+  }
+  __syncthreads();
+  const int f = threadIdx.x;
+  if (f < nfr) {
+    double ll[KT];
+    int id[KT];
+#pragma unroll
+    for (int j = 0; j < KT; j++) {
+      ll[j] = sll[f * LD + j];
+      id[j] = sid[f * LD + j];
+    }
+    double mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < KT; j++) mx = fmax(mx, ll[j]);
+    if (!isfinite(mx)) mx = 0.0;  // scipy logsumexp convention
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < KT; j++) s += exp(ll[j] - mx);
+    const double lse = log(s) + mx;
+    int nkeep = 0, best = 0;
+    double bestv = 0.0;
+#pragma unroll
+    for (int j = 0; j < KT; j++) {
+      ll[j] = exp(ll[j] - lse);  // posterior over the selection
+      if (j == 0 || ll[j] > bestv) {
+        best = j;
+        bestv = ll[j];
+      }
+      if (ll[j] >= prune) nkeep++;
+    }
+    const bool degenerate = nkeep == 0;
+    bool keep[KT];
+    double tot = 0.0;
+#pragma unroll
+    for (int j = 0; j < KT; j++) {
+      keep[j] = degenerate ? (j == best) : (ll[j] >= prune);
+      tot += keep[j] ? ll[j] : 0.0;
+    }
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < KT; j++) {
+      if (!keep[j]) continue;
+      int pos = 0;  // kept entries with a smaller component id (ids of a selection are distinct)
+#pragma unroll
+      for (int q = 0; q < KT; q++) pos += (keep[q] && id[q] < id[j]) ? 1 : 0;
+      sid[f * LD + pos] = id[j];
+      sw[f * LD + pos] = (float)(ll[j] / tot);
+      n++;
+    }
+    counts[t0 + f] = n;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nfr * KT; i += 128) {
+    const int r = i / KT, c = i - r * KT;
+    comp_pad[t0 * KT + i] = sid[r * LD + c];
+    w_pad[t0 * KT + i] = sw[r * LD + c];
+  }
+}
+
 // ----------------------------------------------------------------------------- stage 4: scan + compact
 
 constexpr int kScanBlock = 1024;
@@ -467,14 +544,35 @@ __global__ void scan_write_offsets(const int64_t* counts, int64_t T, const int64
   if (base + i == T - 1) offsets[T] = pre + buf[i];
 }
 
+// Warp per 32 consecutive frames: their CSR range [offsets[t0], offsets[t0 + 32]) is contiguous, so
+// lane l writes entries l, l + 32, ... of it (coalesced); the frame of an entry is found by a binary
+// search over the warp's 33 offsets (shuffled), its slot in the padded arrays follows.
 __global__ void compact_kernel(int64_t T, int K, const int64_t* offsets, const int32_t* comp_pad, const float* w_pad,
                                int32_t* comps, float* wts) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  int64_t o = offsets[t], n = offsets[t + 1] - o;
-  for (int e = 0; e < n; e++) {
-    comps[o + e] = comp_pad[t * K + e];
-    wts[o + e] = w_pad[t * K + e];
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+  if (t0 >= T) return;
+  const int nf = T - t0 < 32 ? (int)(T - t0) : 32;
+  const int64_t my = offsets[t0 + min(lane, nf)];  // lane l: offset of frame t0 + l (lane nf: the end)
+  const int64_t o0 = __shfl_sync(0xffffffffu, my, 0);
+  const int64_t oend = __shfl_sync(0xffffffffu, offsets[t0 + nf], 0);
+  const int total = (int)(oend - o0);
+  for (int e = lane; e < total + 31 - (total + 31) % 32; e += 32) {
+    // largest frame f with offset(f) - o0 <= e
+    int lo = 0, hi = nf - 1;
+#pragma unroll 1
+    for (int step = 0; step < 5; step++) {
+      const int mid = (lo + hi + 1) >> 1;
+      const int64_t om = __shfl_sync(0xffffffffu, my, mid);
+      if (om - o0 <= e) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t of = __shfl_sync(0xffffffffu, my, lo);
+    if (e < total) {
+      const int64_t src = (t0 + lo) * K + (o0 + e - of);
+      comps[o0 + e] = comp_pad[src];
+      wts[o0 + e] = w_pad[src];
+    }
   }
 }
 
@@ -653,7 +751,10 @@ static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, c
   } else {
     TVK_TRY(full_ll_dispatch<XT>(x, T, F, full_table, prec_table, C, K, flags, w.sel, w.sel_ll, w.group,
                                  w.group_bytes, st));
-    if (K <= kMaxTopK) {
+    if (K == 20) {
+      finalize_fixed_kernel<20><<<fb, 128, 0, st>>>(T, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts);
+      TVK_CHECK_LAUNCH("finalize");
+    } else if (K <= kMaxTopK) {
       finalize_kernel<<<fb, 128, 0, st>>>(T, K, prune, w.sel, w.sel_ll, w.comp_pad, w.w_pad, w.counts);
       TVK_CHECK_LAUNCH("finalize");
     } else {
@@ -661,7 +762,7 @@ static int align_impl(const XT* x, int64_t T, int F, const double* diag_table, c
     }
   }
   TVK_TRY(exclusive_scan_counts(w.counts, T, offsets, w.block_sums, st));
-  compact_kernel<<<fb, 128, 0, st>>>(T, K, offsets, w.comp_pad, w.w_pad, components, weights);
+  compact_kernel<<<(int)((T + 127) / 128), 128, 0, st>>>(T, K, offsets, w.comp_pad, w.w_pad, components, weights);
   TVK_CHECK_LAUNCH("compact");
   if (selected) cudaMemcpyAsync(selected, w.sel, sizeof(int32_t) * T * K, cudaMemcpyDeviceToDevice, st);
   if (sel_ll_out) cudaMemcpyAsync(sel_ll_out, w.sel_ll, sizeof(double) * T * K, cudaMemcpyDeviceToDevice, st);
