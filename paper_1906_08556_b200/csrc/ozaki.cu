@@ -8,11 +8,13 @@
 //     x = 2^e * sum_{s=1..S} d_s 2^(-7 s) + rho,   d_s in [-127, 127] (int8),  |rho| < 2^(e - 7 S),
 // d_s = trunc(128 r_{s-1}), r_s = 128 r_{s-1} - d_s (each step exact in FP64).
 // Product.  C_mn = 2^(e_m + e_n) sum_{s + t <= S + 1} 2^(-7 (s + t)) sum_k a_{s,mk} b_{t,kn} + error;
-// every inner sum is an int8 x int8 product accumulated EXACTLY in int32 (|sum| <= S K 127^2 < 2^31
-// for K <= 18,900 per launch piece), so the only errors are the digit truncation rho and the
-// dropped products s + t > S + 1, each < 2^(-7 S) relative to |row max| * |column max| per term:
+// every inner sum is an int8 x int8 product accumulated EXACTLY in int32 (|level sum| <= S K 127^2
+// < 2^31: K is split into pieces of <= 16,600 (S = 8) / 19,000 (S = 7), summed in fixed order), so the
+// only errors are the digit truncation rho and the dropped products s + t > S + 1, each < 2^(-7 S)
+// relative to |row max| * |column max| per term:
 //     |C~ - C| <= (2 + S) 2^(-7 S) K max_k|a_mk| max_k|b_kn|        (S = 7: 2^-45.8 K max|a| max|b|)
-// and the final FP64 combination of the S level sums rounds once per level (2^-53 relative).
+// plus the final combination: the S level sums are folded EXACTLY into two int64 words, converted
+// and fused once (<= 2 roundings, 2^-53 relative each).
 //
 // Level accumulators in TMEM.  Products with the same level L = s + t share one int32 accumulator
 // block of 64 columns (levels 2..S+1 -> S blocks, 64 S <= 512 TMEM columns).  The right operand's S
@@ -24,8 +26,9 @@
 //
 // Kernel roles (one CTA per SM, persistent over 128 x 64 output tiles, m fastest so concurrent CTAs
 // share the right operand's tiles in L2): warp 0 lane 0 streams the pre-tiled digit blobs with
-// bulk copies (one A and one B copy per k-step), warp 1 lane 0 issues the MMAs, warps 2-17 drain
-// the level accumulators (tcgen05.ld 32x32b.x8), combine them in FP64 and write C.
+// bulk copies (one A and one B copy per k-step), warp 1 lane 0 issues the MMAs, warps 2-17 (four per
+// TMEM lane quarter, 16 columns each) drain the level accumulators one 32x32b.x16 load per level,
+// fold them into int64, release the accumulator to the next tile's MMAs, then scale and write C.
 //
 // Determinism: integer products are exact and the FP64 combination has a fixed order, so results
 // are bit-reproducible run to run.  Non-finite inputs make the affected rows / columns NaN.
