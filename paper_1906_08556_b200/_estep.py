@@ -177,6 +177,16 @@ POST_ADD_IDENTITY = 1
 POST_MOMENT = 2
 
 
+def prior_mean_dev(dm):
+    """Device copy of dm.prior_mean, refreshed only when the host vector changes (a pageable host->device
+    copy per batch would synchronize the stream)."""
+    key = dm.prior_mean.tobytes()
+    cached = getattr(dm, "_prior_dev", None)
+    if cached is None or cached[0] != key:
+        dm._prior_dev = (key, _lib.to_dev(np.ascontiguousarray(dm.prior_mean, dtype=np.float64)))
+    return dm._prior_dev[1]
+
+
 def posterior_batch(dm: DeviceModel, ws: Workspace, n, fm, want_moment=True, status_out=None, covariance=False):
     """Posterior of a batch: phi (Ub, D), packed Phi + phi phi' (or Phi if ``covariance``) or None,
     logdet (Ub), bphi (Ub), status, b."""
@@ -186,7 +196,7 @@ def posterior_batch(dm: DeviceModel, ws: Workspace, n, fm, want_moment=True, sta
     Lpk = _lib.empty((Ub, P))
     egemm(n, ws.Upk, Lpk, Ub, P, C, cache=ws.i8_U)  # L - I = sum_c n_c U_c
     b = _lib.empty((Ub, D))
-    b.copy_(torch.from_numpy(dm.prior_mean).to(b.device).expand(Ub, D))
+    b.copy_(prior_mean_dev(dm).expand(Ub, D))
     K = C * F
     splits = max(1, min(16, K // 2048)) if Ub * D < 148 * 128 * 128 else 1
     work = _lib.empty((splits * Ub * D,)) if splits > 1 else None
@@ -205,15 +215,21 @@ def posterior_batch(dm: DeviceModel, ws: Workspace, n, fm, want_moment=True, sta
 
 def check_status(status, what="posterior precision not SPD (corrupted Sigma?)"):
     from ._linalg import NumericError
+    if isinstance(status, (list, tuple)):
+        if not status:
+            return
+        status = torch.cat(status)
     st = _lib.to_host(status)
     if np.any(st != _lib.ITEM_OK):
         raise NumericError(what)
 
 
-def accumulate_batch(dm: DeviceModel, ws: Workspace, acc: DeviceAcc, n, fm, S=None):
+def accumulate_batch(dm: DeviceModel, ws: Workspace, acc: DeviceAcc, n, fm, S=None, statuses=None):
     """One E-step batch into the device accumulators (tvm.py:283-309).
 
     n (Ub, C), fm (Ub, C*F) device; S (Ub, C*F*F) device or None (Ssum accumulated elsewhere).
+    ``statuses``: a list that collects the batch's posterior status for one check after the last batch
+    (no host synchronization between batches); None checks it here.
     """
     Ub = n.shape[0]
     if Ub == 0:
@@ -221,7 +237,10 @@ def accumulate_batch(dm: DeviceModel, ws: Workspace, acc: DeviceAcc, n, fm, S=No
     C, F, D = dm.C, dm.F, dm.D
     P = packed_size(D)
     phi, Mpk, logdet, bphi, status, _ = posterior_batch(dm, ws, n, fm, want_moment=True)
-    check_status(status)
+    if statuses is None:
+        check_status(status)
+    else:
+        statuses.append(status)
     if acc.Apk is not None:
         egemm(n, Mpk, acc.Apk, C, P, Ub, trans_a=True, beta=1.0)  # A_c += sum_u n_uc M_u
     egemm(fm, phi, acc.B, C * F, D, Ub, trans_a=True, beta=1.0, digits=I8_DIGITS_F)  # B_c += sum_u f_uc phi_u'
@@ -238,14 +257,24 @@ def accumulate_batch(dm: DeviceModel, ws: Workspace, acc: DeviceAcc, n, fm, S=No
 
 def finalize_aux(dm: DeviceModel, ws: Workspace, acc: DeviceAcc):
     """aux = sum_u loglik_u (tvm.py:202-214) from corpus-level sums."""
+    return aux_value(dm, acc, finalize_aux_dev(dm, ws, acc))
+
+
+def aux_value(dm: DeviceModel, acc: DeviceAcc, out):
+    """Host value of finalize_aux_dev's device scalar."""
+    mu0 = dm.prior_mean
+    return float(out.item()) - 0.5 * float(mu0 @ mu0) * acc.U
+
+
+def finalize_aux_dev(dm: DeviceModel, ws: Workspace, acc: DeviceAcc):
+    """The device part of finalize_aux (fixed-order dot products), no host synchronization."""
     C, F = dm.C, dm.F
     out = acc.aux_post.clone()
     # -0.5 sum_c N_c (F log 2pi + log|Sigma_c|)
     dot_into(out, acc.N, ws.const, C, alpha=-0.5)
     # -0.5 <Sinv, Ssum>
     dot_into(out, ws.Sinv, acc.Ssum, C * F * F, alpha=-0.5)
-    mu0 = dm.prior_mean
-    return float(out.item()) - 0.5 * float(mu0 @ mu0) * acc.U
+    return out
 
 
 def to_host_acc(acc: DeviceAcc, aux):

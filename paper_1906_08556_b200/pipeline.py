@@ -534,9 +534,11 @@ def _accumulate(dm, ws, corpus, ali, center):
     """E-step over a device corpus into a fresh device accumulator (merged across ranks)."""
     acc = _estep.DeviceAcc(dm.C, dm.F, dm.D)
     n_utt = len(corpus.ids)
+    statuses = []  # checked once after the last batch: no host synchronization inside the E-step
     for lo, hi in _batches(n_utt, _estep.E_STEP_BATCH):
         n, f = _stats_batch(corpus, ali, lo, hi, dm.C, center, acc.Ssum)
-        _estep.accumulate_batch(dm, ws, acc, n, f, S=None)
+        _estep.accumulate_batch(dm, ws, acc, n, f, S=None, statuses=statuses)
+    _estep.check_status(statuses)
     _dist.allreduce_sum_(acc.flat)
     return acc
 
@@ -617,11 +619,13 @@ def _extract_device(dm, ws, model, corpus, top_k, prune):
     else:
         ali = DeviceAlignment(_lib.zeros((1,), torch.int64), _lib.zeros((1,), torch.int32),
                               _lib.zeros((1,), torch.float32), np.zeros(len(corpus.ids) + 1, np.int64))
+    statuses = []
     for lo, hi in _batches(len(corpus.ids), _estep.E_STEP_BATCH):
         n, f = _stats_batch(corpus, ali, lo, hi, dm.C, center, None)
         phi, _, _, _, status, _ = _estep.posterior_batch(dm, ws, n, f, want_moment=False)
-        _estep.check_status(status)
+        statuses.append(status)
         out[lo:hi] = phi
+    _estep.check_status(statuses)
     return out
 
 
@@ -699,6 +703,25 @@ class _HostMoments:
         self.phi_sum = _lib.to_host(acc.phi_sum)
         self.moment_sum = _estep.unpack_host(_lib.to_host(acc.moment), acc.D)
 
+    @classmethod
+    def start(cls, acc):
+        """Asynchronous variant: device->pinned copies queued now, ``finish()`` waits for them only."""
+        self = cls.__new__(cls)
+        self.U = acc.U
+        self._D = acc.D
+        self._phi = torch.empty(acc.phi_sum.shape, dtype=torch.float64, pin_memory=True)
+        self._mom = torch.empty(acc.moment.shape, dtype=torch.float64, pin_memory=True)
+        self._phi.copy_(acc.phi_sum, non_blocking=True)
+        self._mom.copy_(acc.moment, non_blocking=True)
+        self._ev = torch.cuda.Event()
+        self._ev.record()
+        return self
+
+    def finish(self):
+        self._ev.synchronize()
+        self.phi_sum = self._phi.numpy().copy()
+        self.moment_sum = _estep.unpack_host(self._mom.numpy(), self._D)
+
     @property
     def h(self):
         return self.phi_sum / self.U
@@ -770,18 +793,31 @@ class DeviceTrainer:
         acc = _accumulate(dm, ws, self.corpus, self.alignment, center)
         if acc.U < 1:
             raise PipelineError("empty corpus")
-        aux = _estep.finalize_aux(dm, ws, acc)
+        aux_dev = _estep.finalize_aux_dev(dm, ws, acc)
+        # the min-divergence moments go to pinned host memory ahead of the M-step kernels, so the host
+        # eigh of compute_min_div runs while the GPU computes update_T / update_sigma; the results are
+        # checked (warnings, errors) and applied in the reference's order afterwards
+        mom = _HostMoments.start(acc) if cfg.min_div else None
         T_new, st = _estep.update_T_device(dm.T, acc.Apk, acc.B, acc.N, C, F, D)
-        _warn_singular(_lib.to_host(st))
         if cfg.sigma_update:
             S_new, st2 = _estep.update_sigma_device(dm.Sigma, T_new, acc.B, acc.N, acc.Ssum, C, F, D,
                                                     SIGMA_FLOOR_SCALE)
+        tr = tr_err = None
+        if mom is not None:
+            mom.finish()
+            try:
+                tr = compute_min_div(mom, dm.formulation)
+            except Exception as exc:  # raised after the M-step's own checks, as the reference orders them
+                tr_err = exc
+        aux = _estep.aux_value(dm, acc, aux_dev)
+        _warn_singular(_lib.to_host(st))
+        if cfg.sigma_update:
             _raise_collapsed(_lib.to_host(st2))
             dm.Sigma = S_new
         dm.T = T_new
         if cfg.min_div:
-            mom = _HostMoments(acc)
-            tr = compute_min_div(mom, dm.formulation)
+            if tr_err is not None:
+                raise tr_err
             h = mom.h
             if cfg.update_mean and dm.formulation == STANDARD:
                 hb = _lib.to_dev(h)
