@@ -452,6 +452,11 @@ __device__ unsigned long long g_sweep_prof[8];
   } while (0)
 #endif
 namespace sw {
+// internal flag (not in the C ABI): no Phi / M output -- phi and log|L| only.  The sweep then runs as
+// block elimination: only the trailing Schur complement (i, j > k) is updated (~1/3 of the tile
+// updates at D = 400), column k below the pivot keeps B_i, the bordered column yields
+// z_k = P_k^-1 y_k, and phi = A^-1 b follows by block back substitution (phi_k = z_k - sum_{i>k} B_i' phi_i).
+constexpr int PHI_ONLY = 1 << 8;
 constexpr int NT = 512;  // 16 warps, one CTA per SM
 constexpr int CL = 1;    // CTAs (SMs) per matrix (2 = cluster pair: no L2 thrash but slower, see below)
 constexpr int NWARP = NT / 32;
@@ -466,15 +471,16 @@ constexpr size_t smem_bytes() { return sizeof(double) * (2 * MAXB * TILE + TILE 
 // Old column k of the symmetric matrix held in row-major packed storage -> pa (swizzled 32x32 tiles).
 // With `pivot` (the look-ahead result, already -P^-1) the pivot block is copied from it instead.
 __device__ __forceinline__ void sweep_load_panel(const double* S, int D, int nb, int k, double* pa, bool add_identity,
-                                                 const double* pivot) {
+                                                 const double* pivot, bool below_only = false) {
   const int tid = threadIdx.x;
   const int k0 = k * 32, kw = min(32, D - k0);
-  // rows above the pivot block: element (R, c) = S(k0 + c, R), R fastest (contiguous in row k0 + c)
-  for (int e = tid; e < k0 * kw; e += sw::NT) {
+  // rows above the pivot block: element (R, c) = S(k0 + c, R), R fastest (contiguous in row k0 + c);
+  // the elimination (phi-only) mode never reads them
+  for (int e = tid; e < (below_only ? 0 : k0 * kw); e += sw::NT) {
     const int c = e / k0, R = e - c * k0;
     cp_async8(&pa[(R >> 5) * sw::TILE + sw::sidx(R & 31, c)], S + packed_index(k0 + c, R), true);
   }
-  for (int e = tid; e < k0 * (32 - kw); e += sw::NT) {  // columns past D (only when k is the last block)
+  for (int e = tid; e < (below_only ? 0 : k0 * (32 - kw)); e += sw::NT) {  // columns past D (last block only)
     const int c = kw + e / k0, R = e % k0;
     pa[(R >> 5) * sw::TILE + sw::sidx(R & 31, c)] = 0.0;
   }
@@ -574,6 +580,7 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
   const int nupd = 2 * ((nb - 1) * nb / 2);  // update half-tiles per step
   const int64_t P = packed_size(D);
   const bool moment = (flags & TVK_POST_MOMENT) && bvec;
+  const bool elim = (flags & sw::PHI_ONLY) != 0;
 #ifdef TVK_SWEEP_PROF
   long long swp_prev = clock64();
 #endif
@@ -595,7 +602,7 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
       const int nks = min(8, (D - k0 + 3) / 4);
       SWP(5);
       if (bad) break;  // uniform (a failed look-ahead pivot of step k-1)
-      sweep_load_panel(S, D, nb, k, pa, addI, k > 0 ? pnext : nullptr);
+      sweep_load_panel(S, D, nb, k, pa, addI, k > 0 ? pnext : nullptr, elim);
       SWP(0);
       double* pk = pa + k * sw::TILE;
       if (k == 0) {  // later pivots are swept ahead, during the previous step's tile updates
@@ -606,7 +613,7 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
       if (bad) break;  // uniform
       // B_i = A_old_i P^-1 = -(pa_i pk) for the other blocks; the bordered row by the last warp
       for (int i = warp; i < nb; i += sw::NWARP) {
-        if (i == k) continue;
+        if (i == k || (elim && i < k)) continue;
         double acc[4][4][2];
 #pragma unroll
         for (int a = 0; a < 4; a++)
@@ -645,6 +652,7 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
             vr[j] = bd[j - k0];
             continue;
           }
+          if (elim && jb < k) continue;  // z_j of an eliminated block stays (back substitution)
           const double* row = pa + jb * sw::TILE;
           double s = 0.0;
 #pragma unroll 8
@@ -658,8 +666,9 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
       // counter (dynamic balance).  Look-ahead: warp 0 first updates the next pivot block (k+1, k+1),
       // keeps it in pnext and sweeps it (-P_{k+1}^-1 is ready when the next step starts), then joins.
       const bool ahead = !last;
-      const int skip = ahead ? k * (k + 1) / 2 + k : -1;  // reduced index of tile (k+1, k+1)
-      const int ntask = (nb - 1) * nb / 2 - (ahead ? 1 : 0);
+      // reduced index of tile (k+1, k+1): full sweep over all (i, j) != k; elimination over i >= j > k only
+      const int skip = ahead ? (elim ? 0 : k * (k + 1) / 2 + k) : -1;
+      const int ntask = (elim ? (nb - k - 1) * (nb - k) / 2 : (nb - 1) * nb / 2) - (ahead ? 1 : 0);
       if (ahead && warp == 0) {
         const int I0 = k0 + 32;
         const int nf = min(4, (D - I0 + 7) / 8);
@@ -700,6 +709,7 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
       // column-k write-back: (i,k) <- B_i, (k,j) <- B_j^T, (k,k) <- -P^-1
       for (int i = ahead ? warp - 1 : warp; i < nb && (!ahead || warp > 0); i += ahead ? sw::NWARP - 1 : sw::NWARP) {
         if (i % sw::CL != rank) continue;
+        if (elim && i <= k) continue;  // only B_i below the pivot is kept (back substitution)
         const int I0 = i * 32;
         for (int e = lane; e < 1024; e += 32) {
           const int r = e >> 5, c = e & 31;
@@ -717,7 +727,7 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
             v = pk[sw::sidx(r, c)];
           }
           if (R >= D || Cc >= D) continue;
-          if (last) v = -v + (moment ? vr[R] * vr[Cc] : 0.0);
+          if (last && !elim) v = -v + (moment ? vr[R] * vr[Cc] : 0.0);
           Mu[packed_index(R, Cc)] = v;
         }
       }
@@ -731,8 +741,13 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
         while ((i + 1) * (i + 2) / 2 <= m) i++;
         while (i * (i + 1) / 2 > m) i--;
         int j = m - i * (i + 1) / 2;
-        i += i >= k;
-        j += j >= k;
+        if (elim) {  // trailing block (i, j) of the Schur complement, i >= j > k
+          i += k + 1;
+          j += k + 1;
+        } else {
+          i += i >= k;
+          j += j >= k;
+        }
         const int I0 = i * 32, J0 = j * 32;
         const bool dg = i == j;
         // element (R, J0 + 8fj + 2t + h) of row R = I0 + 8fi + g sits at rowoff[fi] + 8fj + h
@@ -777,7 +792,7 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
               const int R = I0 + 8 * fi + g, Cc = J0 + 8 * fj + 2 * t + h;
               if (R >= D || Cc >= D || (dg && Cc > R)) continue;
               double v = acc[fi][fj][h];
-              if (last) v = -v + (moment ? vr[R] * vr[Cc] : 0.0);
+              if (last && !elim) v = -v + (moment ? vr[R] * vr[Cc] : 0.0);
               wp[8 * fj + h] = v;
             }
         }
@@ -786,6 +801,26 @@ __global__ void __launch_bounds__(sw::NT, 1) sweep_posterior_kernel(const double
       if (sw::CL > 1) tc::cluster_sync();  // both CTAs' tiles are in global memory before the next panel load
       else __syncthreads();
       SWP(4);
+    }
+    if (elim && !bad) {
+      // block back substitution phi_k = z_k - sum_{R beyond block k} B(R, k0 + lane) phi(R): warps take
+      // rows R (coalesced 256-byte reads of the packed rows), partial sums folded in fixed warp order
+      double* part = pa;  // [NWARP][32] scratch (the panels are free after the last step)
+      for (int k = nb - 1; k >= 0; k--) {
+        const int k0 = k * 32;
+        double sacc = 0.0;
+        if (k0 + lane < D)
+          for (int R = k0 + 32 + warp; R < D; R += sw::NWARP)
+            sacc = fma(Mu[packed_index(R, k0 + lane)], vr[R], sacc);
+        part[warp * 32 + lane] = sacc;
+        __syncthreads();
+        if (warp == 0 && k0 + lane < D) {
+          double t = 0.0;
+          for (int w2 = 0; w2 < sw::NWARP; w2++) t += part[w2 * 32 + lane];
+          vr[k0 + lane] -= t;
+        }
+        __syncthreads();
+      }
     }
     if (rank == 0) {
       if (tid == 0 && status) status[u] = bad ? TVK_ITEM_NOT_SPD : TVK_ITEM_OK;
@@ -838,8 +873,8 @@ extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, i
     return TVK_OK;
   }
   if (D <= 32 * sw::MAXB && !getenv("TVK_POSTERIOR_CHOL")) {
-    // one block-sweep pass gives Phi, phi and log|L| together; without mpk it works in place in lpk
-    // (the same arithmetic either way, so extraction and the EM posterior agree bit for bit)
+    // one block-sweep pass gives Phi, phi and log|L| together; without mpk it works in place in lpk and
+    // only eliminates (phi, log|L|: a third of the tile updates at D = 400)
     const size_t ssm = sw::smem_bytes();
     cudaFuncSetAttribute(sweep_posterior_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     cudaLaunchConfig_t cfg = {};
@@ -854,8 +889,10 @@ extern "C" int tvk_posterior(const double* lpk, const double* b, int U, int D, i
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // without an M / Phi output the sweep runs as block elimination + back substitution (PHI_ONLY)
+    const int f2 = flags | (mpk ? 0 : sw::PHI_ONLY);
     const cudaError_t le = cudaLaunchKernelEx(&cfg, sweep_posterior_kernel, lpk, mpk ? mpk : const_cast<double*>(lpk),
-                                              b, U, D, flags, phi, logdet, bphi, status);
+                                              b, U, D, f2, phi, logdet, bphi, status);
     TVK_REQUIRE(le == cudaSuccess, "sweep_posterior: cluster launch failed");
     TVK_CHECK_LAUNCH("sweep_posterior");
     return TVK_OK;
