@@ -48,7 +48,9 @@ namespace oz {
 constexpr int BM = 128;   // left rows per tile (MMA M, TMEM lanes)
 constexpr int BN = 64;    // right rows (output columns) per tile and per level block
 constexpr int KB = 32;    // bytes (= int8 elements) of K per k-step (one MMA)
-constexpr int NST = 4;    // ring stages
+// ring stages: as many 42 / 48 KB stages (S = 7 / 8 digits) as fit next to the 1 KB of barriers
+template <int S>
+constexpr int nst() { return (227 * 1024 - 2048) / (S * (128 + 64) * 32); }
 constexpr int NT = 576;   // producer, MMA, 16 epilogue warps
 constexpr int EXP_BAD = 1 << 20;  // row exponent of a row holding a non-finite value
 
@@ -196,6 +198,7 @@ template <int S>
 __global__ void __launch_bounds__(NT, 1) gemm_i8_kernel(Args p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ABYTES = S * BM * KB, BBYTES = S * BN * KB, STAGE = ABYTES + BBYTES;
+  constexpr int NST = nst<S>();
   __shared__ uint64_t full[NST], empty[NST], tfull, tempty;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -457,7 +460,7 @@ static int run(const GemmArgs& g, const void* a_split, const void* b_split, cuda
 #ifdef TVK_SELECT_DIAG
   if (const char* d = getenv("TVK_OZ_DEBUG")) a.dbg = atoi(d);
 #endif
-  const size_t smem = (size_t)NST * S * (BM + BN) * KB;
+  const size_t smem = (size_t)nst<S>() * S * (BM + BN) * KB;
   auto kern = gemm_i8_kernel<S>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int units = mt * nt * nsplit;
