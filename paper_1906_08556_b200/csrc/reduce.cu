@@ -10,21 +10,33 @@ namespace tvk {
 constexpr int kDotBlocks = 1024;  // fixed partition (device-independent)
 constexpr int kDotThreads = 256;
 
-__global__ void colsum_kernel(const double* a, int64_t rows, int64_t cols, int64_t lda, double alpha, double beta,
-                              double* out) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= cols) return;
+// 32 columns x 8 row phases per CTA: thread (tx, ty) sums rows ty, ty + 8, ... of column j (coalesced
+// 256-byte row segments, 8x the loads in flight of a thread per column), the 8 phase sums are then
+// combined in fixed order -- deterministic for every launch.
+__global__ void __launch_bounds__(256) colsum_kernel(const double* a, int64_t rows, int64_t cols, int64_t lda,
+                                                     double alpha, double beta, double* out) {
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t j = blockIdx.x * (int64_t)32 + tx;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int64_t r = 0;
-  for (; r + 4 <= rows; r += 4) {
-    s0 += a[r * lda + j];
-    s1 += a[(r + 1) * lda + j];
-    s2 += a[(r + 2) * lda + j];
-    s3 += a[(r + 3) * lda + j];
+  if (j < cols) {
+    int64_t r = ty;
+    for (; r + 24 < rows; r += 32) {
+      s0 += a[r * lda + j];
+      s1 += a[(r + 8) * lda + j];
+      s2 += a[(r + 16) * lda + j];
+      s3 += a[(r + 24) * lda + j];
+    }
+    for (; r < rows; r += 8) s0 += a[r * lda + j];
   }
-  for (; r < rows; r++) s0 += a[r * lda + j];
-  double s = (s0 + s1) + (s2 + s3);
-  out[j] = (beta != 0.0 ? beta * out[j] : 0.0) + alpha * s;
+  red[ty][tx] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (ty == 0 && j < cols) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) s += red[q][tx];
+    out[j] = (beta != 0.0 ? beta * out[j] : 0.0) + alpha * s;
+  }
 }
 
 __global__ void dot_partial_kernel(const double* x, const double* y, int64_t n, double* partial) {
@@ -80,7 +92,7 @@ extern "C" int tvk_colsum(const double* a, int64_t rows, int64_t cols, int64_t l
                           double* out, void* stream) {
   TVK_REQUIRE(rows >= 0 && cols >= 0 && lda >= cols, "colsum: bad shape");
   if (cols == 0) return TVK_OK;
-  int64_t blocks = (cols + 255) / 256;
+  int64_t blocks = (cols + 31) / 32;
   tvk::colsum_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a, rows, cols, lda, alpha, beta, out);
   TVK_CHECK_LAUNCH("colsum");
   return TVK_OK;
