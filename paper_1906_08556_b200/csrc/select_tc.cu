@@ -32,7 +32,9 @@
 //    K-th largest s~_(K); every score >= s~_(K) - 2m is appended to a per-thread smem buffer.  Any
 //    component below that window is strictly below K others in exact arithmetic.
 // 3. Exact order (select_post_kernel, one warp per frame, off the tensor-core pipeline).  The window
-//    is sorted by s~; runs whose consecutive gaps are <= 2m ("clusters") are rescored in FP64 from
+//    is sorted by s~ on 32-bit keys whose low 5-6 bits hold the entry's position, so only scores
+//    closer than q = 2^6 ulps (<< m) can come out swapped; the window is widened by q.  Runs whose
+//    consecutive gaps are <= 2m ("clusters": they contain every such pair) are rescored in FP64 from
 //    the exact table and re-sorted by (exact value desc, index asc) — the stable-argsort rule of the
 //    reference.  Pairs further apart than 2m are ordered by s~ already.
 // Frames whose window overflows the buffer, has fewer than K finite entries, or holds non-finite
@@ -853,50 +855,16 @@ __global__ void __launch_bounds__(XT_THREADS) select_exact_kernel(const XT* __re
 
 // ---------------------------------------------------------------- window merge, exact order, output
 // One warp per frame.  The two half lists (<= CAP each, every entry >= the collection threshold)
-// are bitonic-sorted together (one slot per lane when they fit 32 entries, else two) on 64-bit keys
-// that order (s~ desc, index asc).  The exact frame window is every entry >= s~_(K) - 2m; runs whose
-// consecutive gaps are <= 2m ("clusters") and that start inside the top K are rescored in FP64 — the
-// warp computes one 2F+1-term dot product at a time, F/32 terms per lane and a fixed shuffle tree —
-// and each member's final position is its cluster start plus the number of members that rank before
-// it under the stable-argsort rule.  Frames that cannot be decided (overflow, collected K-th below
-// the threshold, window wider than a warp) go to select_exact_kernel.
-__device__ __forceinline__ uint64_t sel_key(float v, int c) {  // larger key = earlier (s~ desc, index asc)
-  uint32_t u = __float_as_uint(v);
-  u ^= (u >> 31) ? 0xffffffffu : 0x80000000u;
-  return ((uint64_t)u << 32) | (uint32_t)(0x7fffffff - c);
-}
-__device__ __forceinline__ float key_v(uint64_t k) {
-  uint32_t u = (uint32_t)(k >> 32);
-  u ^= (u >> 31) ? 0x80000000u : 0xffffffffu;
-  return __uint_as_float(u);
-}
-__device__ __forceinline__ int key_c(uint64_t k) { return 0x7fffffff - (int)(uint32_t)k; }
-
-// descending bitonic sort of 32*NS keys, key index = 32 * slot + lane
-template <int NS>
-__device__ __forceinline__ void warp_sort_desc(uint64_t (&k)[2], int lane) {
-#pragma unroll
-  for (int w = 2; w <= 32 * NS; w <<= 1) {
-#pragma unroll
-    for (int j = w >> 1; j > 0; j >>= 1) {
-      if (j == 32) {
-        const uint64_t a = k[0], b = k[1];
-        k[0] = a > b ? a : b;
-        k[1] = a > b ? b : a;
-      } else {
-#pragma unroll
-        for (int sl = 0; sl < NS; sl++) {
-          const int i = 32 * sl + lane;
-          const uint64_t o = __shfl_xor_sync(0xffffffffu, k[sl], j);
-          // the lower index of a descending pair keeps the larger key
-          const bool keep_max = ((i & j) == 0) == ((i & w) == 0);
-          k[sl] = keep_max ? (o > k[sl] ? o : k[sl]) : (o < k[sl] ? o : k[sl]);
-        }
-      }
-    }
-  }
-}
-
+// are bitonic-sorted together (one slot per lane when they fit 32 entries, else two) on 32-bit keys:
+// the score's monotone image with its low 5 (6) bits replaced by the entry's source position, so
+// scores closer than 2^5 (2^6) ulps -- far inside the margin m -- may come out in either order.  The
+// frame window is every entry >= s~_(K) - 2m - q (q: that truncation quantum, so the window stays a
+// superset); runs whose consecutive gaps are <= 2m ("clusters", which therefore contain every pair the
+// truncation could swap) and that start inside the top K are rescored in FP64 -- four entries at a
+// time, 8-lane slots -- and each member's final position is its cluster start plus the number of
+// members that rank before it under the stable-argsort rule (value desc, index asc).  Frames that
+// cannot be decided (overflow, collected K-th below the threshold, window wider than a warp) go to
+// select_exact_kernel.
 // Exact FP64 scores of up to four window entries at once: lane = 8 * slot + sub, each lane sums the
 // features f = sub + 8 i of its slot's component (x values preloaded per lane), then a 3-level
 // butterfly inside the 8-lane slot.  Lanes of unused slots recompute slot 0's component.
@@ -914,6 +882,35 @@ __device__ __forceinline__ double slot_exact_score(const double (&xs)[8], const 
   return s;
 }
 
+// descending bitonic sort of 32*NS 32-bit keys, key index = 32 * slot + lane
+template <int NS>
+__device__ __forceinline__ void warp_sort_desc32(uint32_t (&k)[2], int lane) {
+#pragma unroll
+  for (int w = 2; w <= 32 * NS; w <<= 1) {
+#pragma unroll
+    for (int j = w >> 1; j > 0; j >>= 1) {
+      if (j == 32) {
+        const uint32_t a = k[0], b = k[1];
+        k[0] = max(a, b);
+        k[1] = min(a, b);
+      } else {
+#pragma unroll
+        for (int sl = 0; sl < NS; sl++) {
+          const int i = 32 * sl + lane;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, k[sl], j);
+          const bool keep_max = ((i & j) == 0) == ((i & w) == 0);
+          k[sl] = keep_max ? max(o, k[sl]) : min(o, k[sl]);
+        }
+      }
+    }
+  }
+}
+// monotone unsigned image of a float (larger float -> larger key)
+__device__ __forceinline__ uint32_t ord32(float v) {
+  const uint32_t u = __float_as_uint(v);
+  return u ^ ((u >> 31) ? 0xffffffffu : 0x80000000u);
+}
+
 template <typename XT>
 __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__ x, int64_t T, int F, int K,
                                                           const double* __restrict__ exact,
@@ -925,7 +922,6 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
   const int lane = threadIdx.x & 31;
   const int sub = lane & 7, slot = lane >> 3;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const uint64_t pad = sel_key(-INFINITY, 0x7fffffff);
   // consecutive warps of a CTA take consecutive frames: the entry-major rows are read as 8-byte
   // pieces of 32-byte sectors shared by four neighbouring frames (L1 hits)
   for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += nw) {
@@ -941,7 +937,6 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
         continue;
       }
       bool good = n0 >= 0 && n1 >= 0 && n0 + n1 >= K;
-      uint64_t k[2] = {pad, pad};
       float lim = INFINITY, v = -INFINITY;
       int c = 0x7fffffff;
       if (good) {
@@ -959,20 +954,45 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
         const float2 a = shfl2(q1, (lane - n0) & 31);        // half-1 entry lane - n0
         const float2 b2 = shfl2(q1, (lane + 32 - n0) & 31);  // half-1 entry lane + 32 - n0
         const float2 e0 = lane < n0 ? q0 : a;
-        if (lane < n) k[0] = sel_key(e0.x, __float_as_int(e0.y));
-        if (n > 32) {
-          if (lane + 32 < n) k[1] = sel_key(b2.x, __float_as_int(b2.y));
-          warp_sort_desc<2>(k, lane);
-        } else {
-          warp_sort_desc<1>(k, lane);
-        }
-        v = key_v(k[0]);
-        c = key_c(k[0]);
+        // 32-bit keys: the score's monotone image with its low LB bits replaced by the entry's source
+        // position (ties and near-ties within 2^LB ulps come out in source order; such entries are
+        // closer than the margin, so the cluster test below joins them and orders them exactly)
+        const bool two = n > 32;
+        const int LB = two ? 6 : 5;
+        const uint32_t lowm = (1u << LB) - 1u;
+        uint32_t k32[2];
+        k32[0] = lane < n ? (ord32(e0.x) & ~lowm) | (lowm - (uint32_t)lane) : 0u;
+        k32[1] = (two && lane + 32 < n) ? (ord32(b2.x) & ~lowm) | (lowm - (uint32_t)(lane + 32)) : 0u;
+        if (two) warp_sort_desc32<2>(k32, lane);
+        else warp_sort_desc32<1>(k32, lane);
+        // back to the full entries: source position -> (score, component)
+        auto fetch = [&](uint32_t key, float& fv, int& fc) {
+          const int src = (int)(lowm - (key & lowm));
+          const float v0 = __shfl_sync(0xffffffffu, e0.x, src & 31), c0 = __shfl_sync(0xffffffffu, e0.y, src & 31);
+          const float v1 = __shfl_sync(0xffffffffu, b2.x, src & 31), c1 = __shfl_sync(0xffffffffu, b2.y, src & 31);
+          fv = src < 32 ? v0 : v1;
+          fc = __float_as_int(src < 32 ? c0 : c1);
+          if (src >= n) {  // padding
+            fv = -INFINITY;
+            fc = 0x7fffffff;
+          }
+        };
+        fetch(k32[0], v, c);
         const float kv = __shfl_sync(0xffffffffu, v, K - 1);
-        lim = kv - m2;
+        // truncation quantum (2^LB ulps of the window's scores, generously): the window and the checks
+        // below are widened by it, so every entry the exact order can need stays inside
+        const float qt = ldexpf(fabsf(kv) + m2, LB - 22);
+        lim = kv - m2 - qt;
+        float v32 = -INFINITY;
+        if (two) {
+          int c32;
+          float vv;
+          fetch(k32[1], vv, c32);
+          v32 = __shfl_sync(0xffffffffu, vv, 0);  // sorted position 32
+        }
         // the collected K-th (a lower bound of the true K-th) must clear the collection threshold,
-        // and the exact window (all entries >= lim: a prefix) must fit one warp
-        if (kv - m2 < thr || key_v(k[1]) >= lim) good = false;
+        // and the exact window must fit one warp
+        if (lim < thr || v32 + qt >= lim) good = false;
         good = __all_sync(0xffffffffu, good);
       }
       if (!good) {
@@ -982,8 +1002,11 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
         }
         continue;
       }
-      const unsigned win = __ballot_sync(0xffffffffu, v >= lim);
-      const int We = __popc(win);
+      // the window: the prefix up to the last entry >= lim (entries interleaved within the truncation
+      // quantum are included)
+      const unsigned geq = __ballot_sync(0xffffffffu, v >= lim);
+      const int We = geq ? 32 - __clz(geq) : 0;
+      const unsigned win = We >= 32 ? 0xffffffffu : ((1u << We) - 1u);
       const float prev = __shfl_up_sync(0xffffffffu, v, 1);
       const unsigned joined = __ballot_sync(0xffffffffu, lane >= 1 && lane < We && prev - v <= m2) & win;
       const unsigned starts = win & ~joined;
