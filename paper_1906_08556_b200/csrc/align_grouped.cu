@@ -227,16 +227,31 @@ __global__ void __launch_bounds__(GT, 2)
     }
     cp_async_commit();
   };
-  auto issue = [&](int ti, int b) {
-    const int4 d = tiles[ti];
-    for (int r = tid; r < GROWS; r += GT) S.pair[b][r] = r < d.y ? sorted[d.x + r] : -1;
+  // pair indices of a tile, loaded one tile before the tile's rows are requested (the loads are in
+  // flight during a tile's math instead of stalling the copy issue): pp = the pair of row tid (for
+  // S.pair), pf = the pair of row warp + 8 lane (its frame is this lane's to fetch), -1 past the tile
+  struct Pairs {
+    int4 d;
+    int pp, pf;
+  };
+  auto pairs_of = [&](int ti) {
+    Pairs q{make_int4(0, 0, 0, 0), -1, -1};
+    if (ti < te) {
+      q.d = tiles[ti];
+      const int myrow = warp + (GT / 32) * lane;
+      if (tid < GROWS && tid < q.d.y) q.pp = sorted[q.d.x + tid];
+      if (lane < GROWS / (GT / 32) && myrow < q.d.y) q.pf = sorted[q.d.x + myrow];
+    }
+    return q;
+  };
+  auto issue = [&](const Pairs& q, int b) {
+    const int4 d = q.d;
+    if (tid < GROWS) S.pair[b][tid] = q.pp;
     // frame rows: row r <- x[sorted / K], F elements; warp w copies rows w, w+8, ... (lanes over
-    // 16-byte pieces), lane j first fetches the frame index of the warp's j-th row
+    // 16-byte pieces), lane j holds the frame index of the warp's j-th row
     const int per_row = VEC ? (F * (int)sizeof(XT)) / 16 : F;
     // frame = pair / K by a 40-bit reciprocal (exact for pair < 2^31, K <= 32)
-    const int myrow = warp + (GT / 32) * lane;
-    const int myframe = (lane < GROWS / (GT / 32) && myrow < d.y)
-                            ? (int)(((uint64_t)(uint32_t)sorted[d.x + myrow] * kinv) >> 40) : 0;
+    const int myframe = q.pf >= 0 ? (int)(((uint64_t)(uint32_t)q.pf * kinv) >> 40) : 0;
     if (VEC && per_row <= 16) {  // two rows per warp step: lanes 0-15 and 16-31
       const int sub = lane >> 4, c = lane & 15;
       for (int j = 0; j < GROWS / (GT / 32); j += 2) {
@@ -264,7 +279,8 @@ __global__ void __launch_bounds__(GT, 2)
   };
 
   int comp = -1;
-  issue(tb, 0);
+  issue(pairs_of(tb), 0);
+  Pairs nxt = pairs_of(tb + 1);
   for (int ti = tb; ti < te; ti++) {
     const int xb = (ti - tb) & 1;
     const int4 d = tiles[ti];
@@ -276,7 +292,8 @@ __global__ void __launch_bounds__(GT, 2)
     cp_async_wait<0>();
     __syncthreads();
     // prefetch the next tile's frame rows into the other buffer (its last readers passed the barrier)
-    if (ti + 1 < te) issue(ti + 1, xb ^ 1);
+    if (ti + 1 < te) issue(nxt, xb ^ 1);
+    nxt = pairs_of(ti + 2);
     // warp w owns rows 16w..16w+15 of the tile: Z rows, q = rowsum(Z o Z), ll, store -- no more barriers
     if (warp * 16 < d.y) {
       double acc[2][8][2];
