@@ -345,7 +345,7 @@ def bench_ours(args):
                  "full_ll_kernel": {"launch_ms": d2_ms, "flop_per_frame": FLOP_FULL_PER_FRAME,
                                     "achieved_tflops": FLOP_FULL_PER_FRAME * n / (d2_ms / 1e3) / 1e12,
                                     "frac_of_peak": FLOP_FULL_PER_FRAME * n / (d2_ms / 1e3) / 1e12 / peak}}
-    prof = os.path.join(REPO, "profiles", "r01_ncu_summary_v5.json")
+    prof = os.path.join(REPO, "profiles", "r02_ncu_summary.json")
     traffic = None
     if os.path.exists(prof):
         try:  # DRAM bytes/frame of the dominant kernel from the committed ncu --set full capture

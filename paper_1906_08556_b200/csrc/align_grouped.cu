@@ -279,11 +279,13 @@ __global__ void __launch_bounds__(GT, 2)
   };
 
   int comp = -1;
-  issue(pairs_of(tb), 0);
-  Pairs nxt = pairs_of(tb + 1);
+  Pairs nxt = pairs_of(tb);
+  issue(nxt, 0);
+  int4 dcur = nxt.d;  // descriptor of tile ti (also loaded a tile ahead)
+  nxt = pairs_of(tb + 1);
   for (int ti = tb; ti < te; ti++) {
     const int xb = (ti - tb) & 1;
-    const int4 d = tiles[ti];
+    const int4 d = dcur;
     if (d.z != comp) {  // new component: stage U once every warp is done with the previous tile
       __syncthreads();
       stage_U(d.z);
@@ -293,6 +295,7 @@ __global__ void __launch_bounds__(GT, 2)
     __syncthreads();
     // prefetch the next tile's frame rows into the other buffer (its last readers passed the barrier)
     if (ti + 1 < te) issue(nxt, xb ^ 1);
+    dcur = nxt.d;
     nxt = pairs_of(ti + 2);
     // warp w owns rows 16w..16w+15 of the tile: Z rows, q = rowsum(Z o Z), ll, store -- no more barriers
     if (warp * 16 < d.y) {
