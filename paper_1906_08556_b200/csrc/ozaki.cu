@@ -83,46 +83,85 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 
 // e[r] = max_k frexp exponent of x_rk (|x_rk| < 2^e[r]), EXP_BAD if the row holds a non-finite value;
 // e starts at EXP_NONE (memset 0xC0) and an all-zero row keeps it.  Blocks take 32-row x K-chunk
-// tiles and fold them with atomicMax (the maximum does not depend on the order).
+// tiles and fold them with atomicMax (the maximum does not depend on the order).  The scan keeps the
+// largest |x| bit pattern (for non-negative doubles integer order is magnitude order, and every
+// non-finite pattern lies above +inf's): one integer max per element, one ilogb per row chunk.
 constexpr int EXP_NONE = (int)0xC0C0C0C0;
+__device__ __forceinline__ int exp_of_absmax(unsigned long long m) {
+  if (m >= 0x7FF0000000000000ull) return EXP_BAD;
+  if (m == 0ull) return EXP_NONE;
+  return ilogb(__longlong_as_double((long long)m)) + 1;
+}
+__device__ __forceinline__ unsigned long long absbits(double v) {
+  return (unsigned long long)__double_as_longlong(v) & 0x7FFFFFFFFFFFFFFFull;
+}
 __global__ void row_exp_kernel(const double* __restrict__ x, int R, int K, int64_t rs, int64_t ks, int kchunk, int* e) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int r0 = blockIdx.x * 32;
   const int kb = blockIdx.y * kchunk, ke = min(K, kb + kchunk);
-  if (rs == 1 || ks != 1) {  // lanes over rows (coalesced when rows are adjacent), warps over k
-    const int r = r0 + lane;
-    int mx = EXP_NONE;
+  if (rs == 1) {  // rows adjacent: one row per thread, a block reads 2 KB contiguous per k
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long m = 0ull;
     if (r < R)
 #pragma unroll 8
-      for (int k = kb + warp; k < ke; k += nwarp) {
-        const double v = __ldg(x + (int64_t)r * rs + (int64_t)k * ks);
-        if (!isfinite(v)) mx = EXP_BAD;
-        else if (v != 0.0) mx = max(mx, ilogb(v) + 1);
-      }
+      for (int k = kb; k < ke; k++) m = max(m, absbits(__ldg(x + r + (int64_t)k * ks)));
+    const int mx = exp_of_absmax(m);
+    if (r < R && mx != EXP_NONE) atomicMax(&e[r], mx);
+  } else if (ks != 1) {  // general strides: lanes over rows, warps over k
+    const int r = r0 + lane;
+    unsigned long long m = 0ull;
+    if (r < R)
+#pragma unroll 8
+      for (int k = kb + warp; k < ke; k += nwarp) m = max(m, absbits(__ldg(x + (int64_t)r * rs + (int64_t)k * ks)));
+    const int mx = exp_of_absmax(m);
     if (r < R && mx != EXP_NONE) atomicMax(&e[r], mx);
   } else {  // k contiguous: lanes over k, warps over the tile's rows
     for (int i = warp; i < 32; i += nwarp) {
       const int r = r0 + i;
       if (r >= R) break;
-      int mx = EXP_NONE;
+      unsigned long long m = 0ull;
 #pragma unroll 8
-      for (int k = kb + lane; k < ke; k += 32) {
-        const double v = __ldg(x + (int64_t)r * rs + k);
-        if (!isfinite(v)) mx = EXP_BAD;
-        else if (v != 0.0) mx = max(mx, ilogb(v) + 1);
-      }
-      mx = __reduce_max_sync(0xffffffffu, mx);
+      for (int k = kb + lane; k < ke; k += 32) m = max(m, absbits(__ldg(x + (int64_t)r * rs + k)));
+      const int mx = __reduce_max_sync(0xffffffffu, exp_of_absmax(m));
       if (lane == 0 && mx != EXP_NONE) atomicMax(&e[r], mx);
     }
   }
 }
 
+// The S digits of one element x of a row with exponent er, 7 bits each (sign-magnitude, then two's
+// complement per byte), as 8 bytes: lo = digits S, S-1, S-2, S-3 (bytes 0..3), hi = digits S-4 ..
+// S-7.  f = floor(|x| 2^(7S - er)) < 2^(7S) is formed from the mantissa with one shift, and digit s
+// is bits [7(S - s), 7(S - s) + 7) of f -- exactly the FP64 recurrence d_s = trunc(128 r_{s-1}),
+// r_s = 128 r_{s-1} - d_s on x 2^-er, every step of which is exact.  Integer work only (the FP64
+// recurrence spent 2S conversions per element on the 16/clk conversion pipe).
+template <int S>
+__device__ __forceinline__ void cut_digits(double x, int er, bool ok, uint32_t& lo, uint32_t& hi) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const unsigned long long a = b & 0x7FFFFFFFFFFFFFFFull;
+  const int be = (int)(a >> 52);
+  const unsigned long long mant = (a & 0xFFFFFFFFFFFFFull) | ((unsigned long long)(be != 0) << 52);
+  const int sh = max(be, 1) - 1075 + 7 * S - er;  // |x| = mant 2^(max(be,1) - 1075)
+  unsigned long long f = sh >= 0 ? mant << min(sh, 63) : mant >> min(-sh, 63);
+  if (!ok) f = 0ull;
+  uint32_t l = (uint32_t)f & 0x0FFFFFFFu, h = (uint32_t)(f >> 28) & 0x0FFFFFFFu;  // 7-bit groups 0-3, 4-7
+  l = (l & 0x3FFFu) | ((l << 2) & 0x3FFF0000u);
+  h = (h & 0x3FFFu) | ((h << 2) & 0x3FFF0000u);
+  l = (l & 0x007F007Fu) | ((l << 1) & 0x7F007F00u);
+  h = (h & 0x007F007Fu) | ((h << 1) & 0x7F007F00u);
+  if (b >> 63) {  // per-byte -d for d in [0, 127]: (0x80 - d) ^ 0x80, no borrow between bytes
+    l = (0x80808080u - l) ^ 0x80808080u;
+    h = (0x80808080u - h) ^ 0x80808080u;
+  }
+  lo = l;
+  hi = h;
+}
+
 // One CTA per (RT-row tile, 128/RT k-steps): the RT x 32 (x 128/RT) block is staged in shared memory
 // with coalesced loads along whichever of rows / k is contiguous, every thread cuts one (row, 16-k)
 // chunk into S digits, and each digit tile is written as one contiguous, fully coalesced block.
-template <int S>
+template <int S, int RT>
 __global__ void __launch_bounds__(256) split_tile_kernel(const double* __restrict__ x, int R, int K, int64_t rs,
-                                                         int64_t ks, const int* __restrict__ e, int RT, int KSTEPS,
+                                                         int64_t ks, const int* __restrict__ e, int KSTEPS,
                                                          int8_t* __restrict__ blob) {
   __shared__ double tile[128][KB + 1];
   const int tid = threadIdx.x;
@@ -159,20 +198,32 @@ __global__ void __launch_bounds__(256) split_tile_kernel(const double* __restric
   if (ks0 + q >= KSTEPS) return;
   const int r = r0 + rr;
   const int er = r < R ? e[r] : EXP_NONE;
-  const double sc = (er == EXP_BAD || er == EXP_NONE) ? 0.0 : ldexp(1.0, -er);
+  const bool ok = er != EXP_BAD && er != EXP_NONE;
   uint32_t w[S][4];
 #pragma unroll
-  for (int t = 0; t < S; t++) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
+  for (int j = 0; j < 4; j++) {  // four elements -> their digit bytes, transposed to one word per digit
+    uint32_t lo[4], hi[4];
 #pragma unroll
-  for (int i = 0; i < 16; i++) {
-    double v = tile[lr][half * 16 + i] * sc;  // exact power-of-two scaling, |v| < 1
-#pragma unroll
-    for (int t = 0; t < S; t++) {
-      v *= 128.0;
-      const double d = trunc(v);
-      v -= d;
-      w[t][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)d) << (8 * (i & 3));
+    for (int i = 0; i < 4; i++) cut_digits<S>(tile[lr][half * 16 + 4 * j + i], er, ok, lo[i], hi[i]);
+    uint32_t g[8];
+    {
+      const uint32_t p0 = __byte_perm(lo[0], lo[1], 0x5140), p1 = __byte_perm(lo[0], lo[1], 0x7362);
+      const uint32_t p2 = __byte_perm(lo[2], lo[3], 0x5140), p3 = __byte_perm(lo[2], lo[3], 0x7362);
+      g[0] = __byte_perm(p0, p2, 0x5410);
+      g[1] = __byte_perm(p0, p2, 0x7632);
+      g[2] = __byte_perm(p1, p3, 0x5410);
+      g[3] = __byte_perm(p1, p3, 0x7632);
     }
+    {
+      const uint32_t p0 = __byte_perm(hi[0], hi[1], 0x5140), p1 = __byte_perm(hi[0], hi[1], 0x7362);
+      const uint32_t p2 = __byte_perm(hi[2], hi[3], 0x5140), p3 = __byte_perm(hi[2], hi[3], 0x7362);
+      g[4] = __byte_perm(p0, p2, 0x5410);
+      g[5] = __byte_perm(p0, p2, 0x7632);
+      g[6] = __byte_perm(p1, p3, 0x5410);
+      g[7] = __byte_perm(p1, p3, 0x7632);
+    }
+#pragma unroll
+    for (int t = 0; t < S; t++) w[t][j] = g[S - 1 - t];  // digit t + 1 = 7-bit group S - 1 - t
   }
   int8_t* dst = blob + (((int64_t)rb * KSTEPS + ks0 + q) * S) * (RT * KB) + (rr >> 3) * 256 + half * 128 + (rr & 7) * 16;
 #pragma unroll
@@ -377,12 +428,14 @@ template <int S>
 static void split_operand(const double* x, int R, int K, int64_t rs, int64_t ks, int RT, int KSTEPS, int* e,
                           int8_t* blob, cudaStream_t st) {
   cudaMemsetAsync(e, 0xC0, sizeof(int) * R, st);
-  const int rb = (R + 31) / 32;
+  // (rs == 1: 256 rows per block, else 32); k chunks so that about 8 blocks per SM exist
+  const int rb = rs == 1 ? (R + 255) / 256 : (R + 31) / 32;
   int kch = std::max(1, (int)std::min<int64_t>(K, (int64_t)K * rb / (num_sms() * 8) + 1));
-  kch = std::max(kch, 256);
+  kch = std::max(kch, rs == 1 ? 64 : 256);
   row_exp_kernel<<<dim3(rb, (K + kch - 1) / kch), 256, 0, st>>>(x, R, K, rs, ks, kch, e);
   const int per = 128 / RT;
-  split_tile_kernel<S><<<dim3((R + RT - 1) / RT, (KSTEPS + per - 1) / per), 256, 0, st>>>(x, R, K, rs, ks, e, RT,
+  auto kern = RT == 64 ? split_tile_kernel<S, 64> : split_tile_kernel<S, 128>;
+  kern<<<dim3((R + RT - 1) / RT, (KSTEPS + per - 1) / per), 256, 0, st>>>(x, R, K, rs, ks, e,
                                                                                          KSTEPS, blob);
 }
 

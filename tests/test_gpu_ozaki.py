@@ -123,3 +123,73 @@ def test_estep_engine_int8_matches_dmma(gpu, monkeypatch):
         a, b = res["int8"][k], res["dmma"][k]
         rel = float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
         assert rel < 1e-11, (k, rel)
+
+
+def _split_ref(X, RT, S):
+    """numpy restatement of the operand split (csrc/ozaki.cu header): row exponents e_r = max frexp
+    exponent, digits by the FP64 recurrence d_s = trunc(128 r_{s-1}) on x 2^-e, K-major core-matrix
+    tiles [row tile][k-step][digit][RT x 32]."""
+    R, K = X.shape
+    KST = (K + 31) // 32
+    Rp = (R + RT - 1) // RT * RT
+    fin = np.isfinite(X).all(1)
+    nz = (X != 0).any(1)
+    e = np.full(R, np.int32(-1061109568), dtype=np.int64)  # 0xC0C0C0C0
+    with np.errstate(invalid="ignore"):
+        ex = np.frexp(np.where(np.isfinite(X), X, 0.0))[1]
+    ex = np.where(X != 0, ex, -(1 << 30)).max(1)
+    e[nz] = ex[nz]
+    e[~fin] = 1 << 20
+    ok = fin & nz
+    V = np.zeros((Rp, KST * 32))
+    V[:R, :K] = np.where(ok[:, None], np.ldexp(np.nan_to_num(X), -np.where(ok, e, 0)[:, None].astype(np.int32)), 0.0)
+    D = np.zeros((S, Rp, KST * 32), dtype=np.int8)
+    for s in range(S):
+        V = V * 128.0
+        d = np.trunc(V)
+        V = V - d
+        D[s] = d.astype(np.int8)
+    blob = np.zeros((Rp // RT, KST, S, RT * 32), dtype=np.int8)
+    rr = np.arange(RT)[:, None]
+    kk = np.arange(32)[None, :]
+    off = (rr // 8) * 256 + (kk // 16) * 128 + (rr % 8) * 16 + kk % 16
+    for rb in range(Rp // RT):
+        for ks in range(KST):
+            for s in range(S):
+                blob[rb, ks, s, off] = D[s, rb * RT:(rb + 1) * RT, ks * 32:(ks + 1) * 32]
+    return blob.reshape(-1), e.astype(np.int32)
+
+
+@pytest.mark.parametrize("digits", [6, 7, 8])
+@pytest.mark.parametrize("rows_contiguous", [False, True])
+def test_split_digits_match_fp64_recurrence(gpu, digits, rows_contiguous):
+    """The integer digit cut is bit-identical to the FP64 recurrence it replaces, signs, zero rows,
+    non-finite rows, subnormals and rows spanning many binades included."""
+    from paper_1906_08556_b200 import _lib
+    rng = np.random.default_rng(11 + digits)
+    R, K = 150, 77
+    X = rng.standard_normal((R, K)) * np.exp2(rng.integers(-40, 40, (R, 1)))
+    X *= np.exp2(rng.integers(-30, 1, (R, K)))  # elements far below their row maximum
+    X[3] = 0.0
+    X[4, 5] = np.nan
+    X[6, 7] = -np.inf
+    X[8] = rng.standard_normal(K) * 2.0 ** -1060  # subnormal row
+    X[9, :40] = 5e-324
+    X[10] = -X[10]
+    X[11, 0] = 1.0
+    X[11, 1:] = 2.0 ** -60  # digits beyond the last -> 0
+    for RT in (64, 128):
+        nbytes = int(_lib.load().tvk_i8_operand_bytes(R, K, RT, digits))
+        out = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        if rows_contiguous:  # element (r, k) at r + k R
+            src = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
+            rs, ks = 1, R
+        else:
+            src = torch.from_numpy(X).cuda()
+            rs, ks = K, 1
+        _lib.call("tvk_i8_split", _lib.ptr(src), R, K, rs, ks, RT, digits, _lib.ptr(out), _lib.stream())
+        got = out.cpu().numpy()
+        blob, e = _split_ref(X, RT, digits)
+        assert np.array_equal(got[:blob.size].view(np.int8), blob)
+        eoff = (blob.size + 255) // 256 * 256
+        assert np.array_equal(got[eoff:eoff + 4 * R].view(np.int32), e)
