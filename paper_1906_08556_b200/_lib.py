@@ -143,20 +143,22 @@ _stage_pool = None
 
 def _stage_copy(dst, src):
     """dst[:] = src for equal-shape CPU tensors, row blocks copied by a small thread pool (numpy copies
-    release the GIL), so a large host array reaches pinned memory at memory bandwidth."""
+    release the GIL), so a large host array reaches pinned memory at memory bandwidth.  (Queuing each
+    block's upload as soon as it is staged measured slower: 7 vs 5 ms for a 59 MB covariance stack.)"""
     global _stage_pool
     import concurrent.futures as cf
     if _stage_pool is None:
         _stage_pool = cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1), thread_name_prefix="tvk-stage")
     d, s_ = dst.numpy().reshape(-1), src.numpy().reshape(-1)
     n = d.shape[0]
-    step = -(-n // _stage_pool._max_workers)
+    step = -(-n // (2 * _stage_pool._max_workers))
     list(_stage_pool.map(lambda lo: np.copyto(d[lo:lo + step], s_[lo:lo + step]), range(0, n, step)))
 
 
 def to_dev(a, dtype=torch.float64):
     """Host array -> contiguous device tensor.  Large arrays (>= 8 MiB, e.g. a 2048 x 60 x 60 covariance
-    stack) are staged through one reused pinned buffer and copied asynchronously."""
+    stack) are staged through one reused pinned buffer and copied asynchronously (small ones through
+    pinned blocks of torch's host allocator measured no faster end to end)."""
     if isinstance(a, torch.Tensor):
         return a.to(device=device(), dtype=dtype).contiguous()
     arr = np.ascontiguousarray(a)
