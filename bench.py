@@ -641,7 +641,7 @@ def bench_em_leg(args, pkg, dev, rank, world, barrier, max_over_ranks, form, n_g
            "scaling": "strong", "alignment_s": align_s, "config": label,
            "achieved_tflops": n_global * FLOP_EM_UTT / sec / 1e12, "flop_per_utt": FLOP_EM_UTT,
            "aux_last": auxes[-1]}
-    if profile_kernels and rank == 0:
+    if profile_kernels:  # every rank: the extra iteration's all-reduce needs all of them
         tot, kern = em_kernel_breakdown(tr, it + 1, align_diag, align_cov)
         g = kern.get("gemm_i8_kernel")
         if g:

@@ -129,3 +129,31 @@ def test_two_rank_checkpoint_resume_is_bit_exact(gpu, tmp_path):
         assert list(resumed[r]["iters"]) == [2, 3]
         for k in ("T", "Sigma", "ivectors", "prior"):
             assert resumed[r][k].tobytes() == plain[r][k].tobytes(), k
+
+
+def test_bench_torchrun_two_ranks(gpu):
+    """bench.py's multi-rank path as the driver launches it (torchrun, one process per rank; gloo here
+    so both ranks can share the one GPU): frames sharded with no collective, the EM leg's one
+    all-reduce per iteration, max-over-ranks timing, and ONE JSON line from rank 0 whose whole-job
+    value counts both ranks' frames."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", "bench.py", "--gpus", "2", "--steps", "2",
+           "--warmup", "3", "--frames", "300000", "--em-utts", "512", "--em-steps", "1", "--c5-utts", "256",
+           "--extract-utts", "1024", "--exact-frames", "0", "--dense-steps", "0", "--no-cpu", "--no-config1",
+           "--dist-backend", "gloo"]
+    env = dict(os.environ, OMP_NUM_THREADS="4")
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["config"]["global_frames_per_step"] == 600000
+    assert abs(rec["value"] - 600000 / (rec["ms_per_step"] / 1e3)) <= 1e-6 * rec["value"]
+    em = rec["em_iteration"]
+    assert em["global_utts"] == 512 and em["utts_per_gpu"] == 256 and em["value"] > 0
+    assert np.isfinite(em["aux_last"])
+    assert rec["config5"]["extraction"]["global_utts"] == 1024
