@@ -215,6 +215,11 @@ __device__ __forceinline__ bool better(double v, int i, double w, int j) {
   if (a) return i < j;
   return v > w || (v == w && i < j);
 }
+// the same order without branches (for warp-uniform loops whose body should stay predicated)
+__device__ __forceinline__ bool better_nb(double v, int i, double w, int j) {
+  const bool a = isnan(v), b = isnan(w), lt = i < j;
+  return (!a & (b | (v > w) | ((v == w) & lt))) | (a & b & lt);
+}
 
 // value-only descending top list: insert t (branch-free min/max chain), read the K-th entry
 template <int NK>
@@ -926,6 +931,14 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
   // pieces of 32-byte sectors shared by four neighbouring frames (L1 hits)
   for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += nw) {
     {
+      // the frame's features, requested before the window work so their DRAM latency overlaps it
+      // (nearly every frame rescores a cluster; lane = 8 slot + sub holds features sub + 8 i)
+      XT xv[8];
+      {
+        const XT* xr = x + t * F;
+#pragma unroll
+        for (int i = 0; i < 8; i++) xv[i] = sub + 8 * i < F ? xr[sub + 8 * i] : (XT)0;
+      }
       const int n0 = cand_n[2 * t], n1 = cand_n[2 * t + 1];
       const float4 par = fpar[t];
       const float thr = par.x, m2 = par.y;
@@ -1019,10 +1032,9 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
       unsigned need = __ballot_sync(0xffffffffu, clustered || (want_all && lane < K));
       double ev = 0.0;
       if (need) {
-        const XT* xr = x + t * F;
         double xs[8];
 #pragma unroll
-        for (int i = 0; i < 8; i++) xs[i] = sub + 8 * i < F ? (double)xr[sub + 8 * i] : 0.0;
+        for (int i = 0; i < 8; i++) xs[i] = (double)xv[i];
         while (need) {  // four entries per step, one per 8-lane slot
           int jj[4];
 #pragma unroll
@@ -1058,7 +1070,7 @@ __global__ void __launch_bounds__(256) select_post_kernel(const XT* __restrict__
           const int j = __ffs(mm) - 1;
           const double ov = __shfl_sync(0xffffffffu, ev, j);
           const int oc = __shfl_sync(0xffffffffu, c, j);
-          if (clustered && j >= st && j < en && j != lane && better(ov, oc, ev, c)) cntb++;
+          cntb += (int)(clustered & (j >= st) & (j < en) & (j != lane) & better_nb(ov, oc, ev, c));
         }
         if (clustered) pos = st + cntb;
       }
