@@ -188,7 +188,37 @@ __global__ void __launch_bounds__(256) split_tile_kernel(const double* __restric
       tile[lr][kk] = vals[it];
     }
   };
-  if (rs == 1) stage(std::true_type{});
+  // interior blocks (every row and k of the block in range) with one unit stride: one base pointer
+  // per thread advanced by a constant, no per-element bounds, all 16 loads in flight before a store
+  const bool full = r0 + RT <= R && (int64_t)(ks0 + per) * KB <= K;
+  auto stage_fast = [&](auto rows_fast) {
+    const double* p;
+    int64_t step;
+    if (rows_fast) {  // i = tid + 256 it: lr = tid % 128 (q = lr / RT, rr = lr % RT), kk = 2 it + tid / 128
+      const int lr = tid & 127;
+      p = x + (r0 + lr % RT) + ((int64_t)(ks0 + lr / RT) * KB + (tid >> 7)) * ks;
+      step = 2 * ks;
+    } else {  // lr = tid / 32 + 8 it (q = lr / RT, rr = lr % RT), kk = tid % 32
+      p = x + (int64_t)(r0 + (tid >> 5)) * rs + (int64_t)ks0 * KB + (tid & 31);
+      step = 8 * rs;
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; it++) {
+      if (!rows_fast && RT == 64 && it == 8)  // rows wrap to the next k-step of the same row tile
+        p += KB - (int64_t)64 * rs;
+      vals[it] = __ldg(p);
+      p += step;
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; it++) {
+      const int i = tid + 256 * it;
+      const int lr = rows_fast ? i % 128 : i / KB, kk = rows_fast ? i / 128 : i % KB;
+      tile[lr][kk] = vals[it];
+    }
+  };
+  if (full && rs == 1) stage_fast(std::true_type{});
+  else if (full && ks == 1) stage_fast(std::false_type{});
+  else if (rs == 1) stage(std::true_type{});
   else stage(std::false_type{});
   __syncthreads();
   // thread -> (local row, k half) so that consecutive threads write consecutive 16-byte chunks:
