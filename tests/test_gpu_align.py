@@ -470,3 +470,34 @@ def test_corpus_second_order_sum_matches_numpy(gpu, F, long_run):
         ref[c] = (y * wts[m].astype(np.float64)[:, None]).T @ y
     assert np.array_equal(got, np.swapaxes(got, 1, 2))  # exactly symmetric
     np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+def test_tensor_core_preselection_exact_at_scale(gpu, monkeypatch):
+    """2e5 config-2 frames (1563 frame tiles, every window / overflow / flagged-frame path exercised
+    many times): the tcgen05 preselection is index-identical to the FP64 DMMA kernel; a 3000-frame
+    slice also matches the oracle's stable argsort (gmm.py:409-410)."""
+    (w, mu, var), _, x = orc.posterior_ubm(2048, 60, 0.3, seed=77, n_frames=200_000)
+    dm = gpu.gmm.GmmDiag(w, mu, var)
+    a, _ = _select(gpu, x, dm, 20, "tc", monkeypatch)
+    b, _ = _select(gpu, x, dm, 20, "dmma", monkeypatch)
+    np.testing.assert_array_equal(a, b)
+    ll = orc.diag_loglik(w, mu, var, x[:3000].astype(np.float64))
+    np.testing.assert_array_equal(a[:3000], np.argsort(-ll, axis=1, kind="stable")[:, :20])
+
+
+def test_align_host_many_pieces_full_entries_match_device_path(gpu, monkeypatch):
+    """The host pipeline at prune 0 (every top-K entry kept: the largest copy-outs) over many pieces,
+    including the ramp pieces: piece outputs freed on the compute stream must not be reused while
+    their device->host copies run (record_stream on the drain stream), so the CSR is identical to the
+    one-shot device alignment."""
+    import torch
+    (w, mu, var), full, x = orc.posterior_ubm(256, 20, 0.5, seed=5, n_frames=200_000)
+    dm, fm = gpu.gmm.GmmDiag(w, mu, var), gpu.gmm.GmmFull(*full)
+    ref = gpu.gmm.align_frames(dm, fm, torch.from_numpy(x).cuda(), top_k=20, prune=0.0)
+    monkeypatch.setattr(gpu._device, "STREAM_CHUNK", 8192)
+    monkeypatch.setattr(gpu._device, "RAMP_PIECE", 2048)
+    got = gpu.gmm.align_frames(dm, fm, torch.from_numpy(x).pin_memory(), top_k=20, prune=0.0)
+    assert got.components.shape[0] == 20 * x.shape[0]
+    np.testing.assert_array_equal(got.offsets, ref.offsets)
+    np.testing.assert_array_equal(got.components, ref.components)
+    np.testing.assert_array_equal(got.weights, ref.weights)
