@@ -23,3 +23,21 @@ tm("H2D from pinned", lambda: out.copy_(pin, non_blocking=True))
 tm("pageable .to(cuda)", lambda: t.to("cuda"))
 tm("pageable copy_ into out", lambda: out.copy_(t))
 tm("memcpy8 + H2D", lambda: (mc(8), out.copy_(pin, non_blocking=True)))
+
+# page-lock the numpy buffer in place (no staging copy), upload, unlock
+from cuda.bindings import runtime as rt  # noqa: E402
+
+
+def registered():
+    ptr = cov.ctypes.data
+    err, = rt.cudaHostRegister(ptr, cov.nbytes, 0)
+    assert err == rt.cudaError_t.cudaSuccess, err
+    out.copy_(torch.from_numpy(cov), non_blocking=True)
+    torch.cuda.synchronize()
+    rt.cudaHostUnregister(ptr)
+
+
+try:
+    tm("cudaHostRegister + H2D + unregister", registered)
+except Exception as exc:  # cuda-python missing or registration refused
+    print("cudaHostRegister probe failed:", exc)
