@@ -340,11 +340,13 @@ __global__ void __launch_bounds__(kBwThreads, 2) bw_second_order_dmma_kernel(con
       if (tid < nu)
         for (int rr = max(0, w0 - off); rr < len && off + rr < w0 + kSoPosCap; rr++) pos[off + rr - w0] = r0 + s0 + rr;
       __syncthreads();
-      for (int e0 = 0; e0 < total; e0 += kSoEB) {
-        const int nb = min(kSoEB, total - e0);
-        double v[kSoEB * 64 / kBwThreads], wv[kSoEB * 64 / kBwThreads];
+      // rounds of kSoEB entries; the gathers of round r + 1 (position -> frame -> features, two
+      // dependent global loads) are issued before round r's DMMAs, so their latency overlaps the math
+      constexpr int NV = kSoEB * 64 / kBwThreads;
+      double v[NV], wv[NV];
+      auto gather = [&](int e0, int nb) {
 #pragma unroll
-        for (int i = 0; i < kSoEB * 64 / kBwThreads; i++) {
+        for (int i = 0; i < NV; i++) {
           const int idx = tid + kBwThreads * i, e = idx >> 6, j = idx & 63;
           v[i] = wv[i] = 0.0;
           if (e < nb && j < F) {
@@ -356,14 +358,19 @@ __global__ void __launch_bounds__(kBwThreads, 2) bw_second_order_dmma_kernel(con
             wv[i] = ws.sorted_w[p] * xv;
           }
         }
+      };
+      if (total > 0) gather(0, min(kSoEB, total));
+      for (int e0 = 0; e0 < total; e0 += kSoEB) {
+        const int nb = min(kSoEB, total - e0);
         __syncthreads();  // the previous round's DMMAs are done with xe / wxe
 #pragma unroll
-        for (int i = 0; i < kSoEB * 64 / kBwThreads; i++) {
+        for (int i = 0; i < NV; i++) {
           const int idx = tid + kBwThreads * i, e = idx >> 6, j = idx & 63;
           xe[e][j] = v[i];
           wxe[e][j] = wv[i];
         }
         __syncthreads();
+        if (e0 + kSoEB < total) gather(e0 + kSoEB, min(kSoEB, total - e0 - kSoEB));
         const int nks = (nb + 3) >> 2;
         for (int ks = 0; ks < nks; ks++) {
           const int e = 4 * ks + t4;
