@@ -131,24 +131,32 @@ __global__ void __launch_bounds__(kBwThreads) bw_first_order_kernel(
       continue;
     }
     const double* mc = center ? center + (int64_t)c * F : nullptr;
+    // one pass over the component's entries for all features (lane j takes j, j + 32, j + 64, j + 96):
+    // each f_c[j] and n_c still sums in entry order, as the reference's stable-sorted sums do
+    double acc[4] = {0.0, 0.0, 0.0, 0.0}, mcj[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      if (mc && lane + 32 * q < F) mcj[q] = mc[lane + 32 * q];
     double occ = 0.0;
-    for (int j0 = 0; j0 < F; j0 += 32) {
-      int j = j0 + lane;
-      double acc = 0.0;
-      double occ_j = 0.0;
-      for (int r = 0; r < n; r++) {
-        int t = ws.sorted_frame[r0 + s + r];
-        double w = ws.sorted_w[r0 + s + r];
-        occ_j += w;
-        if (j < F) {
-          double xv = (double)x[(int64_t)t * F + j];
-          if (mc) xv -= mc[j];
-          acc += w * xv;
+#pragma unroll 4
+    for (int r = 0; r < n; r++) {
+      const int t = ws.sorted_frame[r0 + s + r];
+      const double w = ws.sorted_w[r0 + s + r];
+      occ += w;
+      const XT* xr = x + (int64_t)t * F;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int j = lane + 32 * q;
+        if (32 * q < F && j < F) {
+          double xv = (double)xr[j];
+          if (mc) xv -= mcj[q];
+          acc[q] += w * xv;
         }
       }
-      if (j < F) fc[j] = acc;
-      occ = occ_j;
     }
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      if (lane + 32 * q < F) fc[lane + 32 * q] = acc[q];
     if (lane == 0) nrow[c] = occ;
   }
   if (S_out == nullptr) return;
