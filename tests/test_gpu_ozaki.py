@@ -193,3 +193,19 @@ def test_split_digits_match_fp64_recurrence(gpu, digits, rows_contiguous):
         assert np.array_equal(got[:blob.size].view(np.int8), blob)
         eoff = (blob.size + 255) // 256 * 256
         assert np.array_equal(got[eoff:eoff + 4 * R].view(np.int32), e)
+
+
+def test_colsum_paths_bit_identical_and_match_torch(gpu):
+    """tvk_colsum: the two-column (16-byte) kernel and the scalar kernel sum every column in the same
+    fixed order (bit-identical), and both agree with torch's FP64 sum."""
+    from paper_1906_08556_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(9)
+    R, Cn = 1037, 4002
+    A = torch.randn(R, Cn, device="cuda", dtype=torch.float64, generator=g)
+    out_vec = torch.full((Cn,), 0.5, device="cuda", dtype=torch.float64)
+    _lib.call("tvk_colsum", _lib.ptr(A), R, Cn, Cn, 2.0, 1.0, _lib.ptr(out_vec), _lib.stream())
+    sub = A[:, 1:]  # 8-byte aligned start, odd width: the scalar kernel
+    out_sc = torch.full((Cn - 1,), 0.5, device="cuda", dtype=torch.float64)
+    _lib.call("tvk_colsum", _lib.ptr(sub), R, Cn - 1, Cn, 2.0, 1.0, _lib.ptr(out_sc), _lib.stream())
+    assert torch.equal(out_vec[1:], out_sc)
+    assert torch.allclose(out_vec, 0.5 + 2.0 * A.sum(0), rtol=1e-12, atol=1e-12)
