@@ -169,13 +169,17 @@ def _pinned_slots(chunk, k):
     return _staging[key]
 
 
-def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
+def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK, tables=None):
     """Frame posteriors of HOST frames with every copy overlapped (align_frames' host path).
 
     The frames are cut into ``chunk``-frame pieces.  Piece i+1's host->device copy (copy stream),
     piece i's alignment kernels (compute stream), piece i-1's device->host copy of its CSR into
     pinned staging (drain stream) and piece i-2's copy from staging into the returned arrays (a
     host worker thread) all run concurrently.  Returns host (offsets, components, weights).
+
+    ``tables``: instead of ``diag_tab`` / ``full_tab``, a callable returning them that is run once
+    the first piece's host->device copy is queued, so the model upload and table builds (and their
+    checks) overlap that copy; ``top_k`` must then already be at most C.
     """
     global _copier
     import concurrent.futures as cf
@@ -188,7 +192,7 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
             arr = arr.astype(np.float64, copy=False)
         host = torch.from_numpy(np.ascontiguousarray(arr))
     host = host.contiguous()
-    k = min(top_k, diag_tab.C)
+    k = min(top_k, diag_tab.C) if tables is None else top_k
     chunk = min(chunk, T, max(1, WIDE_PAIRS // k))
     offsets = np.empty(T + 1, np.int64)
     comps = np.empty(T * k, np.int32)   # untouched capacity is never paged in
@@ -262,6 +266,12 @@ def align_host(features, diag_tab, full_tab, top_k, prune, chunk=STREAM_CHUNK):
             buf.copy_(host[lo:lo + n], non_blocking=True)
             copied = torch.cuda.Event()
             copied.record(copy_stream)
+        if i == 0 and tables is not None:
+            try:
+                diag_tab, full_tab = tables()
+            except BaseException:
+                copy_stream.synchronize()  # the queued copy still writes into bufs: let it land first
+                raise
         comp_stream.wait_event(copied)
         res = align(buf, diag_tab, full_tab, k, prune, sync_count=False)
         done = torch.cuda.Event()

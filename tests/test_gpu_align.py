@@ -501,3 +501,19 @@ def test_align_host_many_pieces_full_entries_match_device_path(gpu, monkeypatch)
     np.testing.assert_array_equal(got.offsets, ref.offsets)
     np.testing.assert_array_equal(got.components, ref.components)
     np.testing.assert_array_equal(got.weights, ref.weights)
+
+
+def test_align_host_path_rejects_non_spd_model(gpu, monkeypatch):
+    """Host pipeline: the full-covariance tables are built while the first piece of frames is copied,
+    and a non-SPD covariance still raises the reference's LinAlgError before any alignment kernel."""
+    import torch
+    (w, mu, var), (wf, muf, cov), x = orc.posterior_ubm(64, 20, 0.5, seed=23, n_frames=5000)
+    cov = cov.copy()
+    cov[5] = -np.eye(20)
+    dm, fm = gpu.gmm.GmmDiag(w, mu, var), gpu.gmm.GmmFull(wf, muf, cov)
+    monkeypatch.setattr(gpu._device, "STREAM_CHUNK", 1000)
+    with pytest.raises(np.linalg.LinAlgError):
+        gpu.gmm.align_frames(dm, fm, torch.from_numpy(x).pin_memory(), top_k=20, prune=0.025)
+    good = gpu.gmm.GmmFull(wf, muf, orc.posterior_ubm(64, 20, 0.5, seed=23)[1][2])
+    ali = gpu.gmm.align_frames(dm, good, torch.from_numpy(x).pin_memory(), top_k=20, prune=0.025)
+    assert ali.offsets.shape[0] == 5001  # the pipeline is usable after the failed call
